@@ -1,0 +1,118 @@
+/* hetermoe.h — C ABI of libhetermoe_kernels.so, the B200 (sm_100a) expert-layer hot path.
+ *
+ * The reference (zpsim, /root/reference/pkg) has no native layer: every hot-path operator is an
+ * opaque duration inside a Task. These entry points are the kernels that the
+ * reference's task kinds stand for; each comment names the reference interface it replaces:
+ *
+ *   ATTN_F  (taskgraph.py:220-246, costmodel.py:19-25)   -> hm_router_topk, hm_dispatch_permute, hm_combine
+ *   EXP_F / OFF_EXP_F (costmodel.py:28-37 expert_duration) -> hm_grouped_ffn_fwd
+ *   EXP_B / OFF_EXP_B (same, x gamma, taskgraph.py:441-451) -> hm_grouped_ffn_bwd
+ *   ATTN_B  (taskgraph.py:476)                            -> hm_combine_bwd, hm_router_bwd / hm_unpermute_sum
+ *
+ * Conventions:
+ *   - every pointer is a DEVICE pointer owned by the caller; the library never allocates;
+ *   - bf16 tensors are passed as `const void*` / `void*` (IEEE bfloat16, row-major, contiguous);
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); every call is asynchronous and
+ *     stream-ordered, no host synchronisation happens inside;
+ *   - return 0 on success, a cudaError_t value on a CUDA error, or an HM_E_* code on a shape /
+ *     alignment error; hm_last_error() returns a thread-local message for the last failure;
+ *   - calls are reentrant across threads when streams and buffers are distinct.
+ */
+#ifndef HETERMOE_H_
+#define HETERMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HM_ABI_VERSION 1
+
+#define HM_E_SHAPE 1001     /* unsupported or inconsistent shape */
+#define HM_E_ALIGN 1002     /* pointer / stride alignment violated (16 bytes) */
+#define HM_E_DRIVER 1003    /* driver entry point (cuTensorMapEncodeTiled) unavailable */
+#define HM_E_ARG 1004       /* bad enum / null argument */
+
+/* grouped GEMM modes (see paper_2504_03871_b200/csrc/grouped_gemm.cuh) */
+#define HM_GEMM_FWD_UPGATE 0 /* act,h = SwiGLU(A[rows,K] . B[e][N][K]^T)           (N = 2f) */
+#define HM_GEMM_FWD_DOWN 1   /* out = A[rows,K] . B[e][N][K]^T                                 */
+#define HM_GEMM_BWD_DACT 2   /* dH = SwiGLU'(A[rows,K] . B[e][K][N], h)              (N = f)  */
+#define HM_GEMM_BWD_DX 3     /* out = A[rows,K] . B[e][K][N]                                   */
+#define HM_GEMM_WGRAD 4      /* out[e][M][N] = A[seg_e, M]^T . B[seg_e, N]                     */
+
+int hm_abi_version(void);
+const char* hm_last_error(void);
+/* number of SMs of the current device (grid sizing for max_ctas) */
+int hm_num_sms(void);
+
+/* ---- K1 router: logits (fixed-order fp32), top-k, softmax over the k, histogram, offsets ----
+ * x[T,d] bf16, wg[d,E] bf16 (logits = x . wg). Outputs: idx[T,k] int32, w[T,k] fp32,
+ * logits[T,E] fp32 (required scratch, also a result), counts[E], offsets[E+1] int32,
+ * chunk_base[hm_router_chunk_elems(T,E)] int32 (consumed by hm_dispatch_permute).
+ * Requires d % 256 == 0, 1 <= k <= 8, k <= E <= 256.
+ * Replaces: the router/gate folded into ATTN_F (taskgraph.py:220-246). */
+int hm_router_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
+                   float* w, float* logits, int32_t* counts, int32_t* offsets,
+                   int32_t* chunk_base, void* stream);
+size_t hm_router_chunk_elems(int T, int E);
+
+/* ---- K2 dispatch permute: x[T,d] -> x_perm[T*k,d] grouped by expert, stable in token order --
+ * row_src[T*k] = source token of each permuted row, row_of[T,k] = permuted row of (t, slot).
+ * Replaces: the dispatch side of DISP_F (taskgraph.py:244). */
+int hm_dispatch_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, int T, int d,
+                        int E, int k, void* x_perm, int32_t* row_src, int32_t* row_of,
+                        void* stream);
+/* dx[t] = sum_s dx_perm[row_of[t,s]] (backward of the permute) */
+int hm_unpermute_sum(const void* dx_perm, const int32_t* row_of, int T, int d, int k, void* dx,
+                     void* stream);
+
+/* ---- K4 combine: y[t] = sum_s w[t,s] * y_perm[row_of[t,s]] ----
+ * Replaces: the combine folded into ATTN_F(l+1) after COMB_F (taskgraph.py:266-283). */
+int hm_combine(const void* y_perm, const int32_t* row_of, const float* w, int T, int d, int k,
+               void* y, void* stream);
+/* dy_perm[row_of[t,s]] = w[t,s] * dy[t];  dw[t,s] = <dy[t], y_perm[row_of[t,s]]> */
+int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, const float* w,
+                   int T, int d, int k, void* dy_perm, float* dw, void* stream);
+
+/* ---- router backward fused with the unpermute-sum ----
+ * dlogit = softmax-backward of the k selected weights; dx = unpermute_sum(dx_perm) + dlogit . wg^T;
+ * dwg[d,E] (bf16) = x^T . dlogit. wg_t = wg transposed ([E,d], see hm_transpose_bf16);
+ * part = fp32 workspace of hm_router_bwd_part_elems(T,d,E) elements. */
+int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
+                  const float* dw, const void* x, const void* wg_t, int T, int d, int E, int k,
+                  void* dx, float* dlogit, void* dwg, float* part, void* stream);
+size_t hm_router_bwd_part_elems(int T, int d, int E);
+int hm_transpose_bf16(const void* in, int R, int C, void* out, void* stream);
+
+/* ---- K3 grouped expert GEMM (tcgen05 / TMEM / TMA) ----
+ * seg_offsets[E+1] (device) delimit each expert's rows of the activation buffers.
+ * GROUP_M modes: a = activations [rows, K]; b = per-expert weights ([E][N][K] or [E][K][N]).
+ * WGRAD: a = [rows, M], b = [rows, N], out = [E][M][N].
+ * max_ctas caps the persistent grid (capacity-weight emulation; <= 0 means all SMs). */
+int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_offsets, int E,
+                    int rows, int M, int N, int K, void* out, int ldo, void* out2, int ldo2,
+                    const void* aux, int ld_aux, int max_ctas, void* stream);
+
+/* SwiGLU expert FFN forward over permuted rows:
+ *   h[rows,2f]  = x_perm . w_ug[e]^T   (gate|up interleaved in 128-column blocks, saved for bwd)
+ *   act[rows,f] = silu(gate) * up
+ *   y_perm[rows,d] = act . w_d[e]^T
+ * w_ug: [E][2f][d] (rows 256*j .. +127 = gate f-cols 128*j.., rows +128 .. +255 = up), w_d: [E][d][f].
+ * Replaces: expert_duration (costmodel.py:28-37), i.e. the EXP_F / OFF_EXP_F tasks. */
+int hm_grouped_ffn_fwd(const void* x_perm, int rows, const int32_t* seg_offsets, int E,
+                       const void* w_ug, const void* w_d, int d, int f, void* h, void* act,
+                       void* y_perm, int max_ctas, void* stream);
+/* backward: dh = SwiGLU'(dy_perm . w_d[e]) (workspace [rows,2f]); dx_perm = dh . w_ug[e];
+ * dw_ug[e] = dh_e^T . x_e; dw_d[e] = dy_e^T . act_e. Replaces EXP_B / OFF_EXP_B. */
+int hm_grouped_ffn_bwd(const void* dy_perm, const void* x_perm, const void* h, const void* act,
+                       int rows, const int32_t* seg_offsets, int E, const void* w_ug,
+                       const void* w_d, int d, int f, void* dh, void* dx_perm, void* dw_ug,
+                       void* dw_d, int max_ctas, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HETERMOE_H_ */

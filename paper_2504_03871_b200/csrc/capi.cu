@@ -1,0 +1,417 @@
+// capi.cu — extern "C" entry points of libhetermoe_kernels.so (declared in include/hetermoe.h).
+//
+// Host-side responsibilities only: argument validation, TMA descriptor encoding
+// (cuTensorMapEncodeTiled through the runtime's driver entry point; no -lcuda), grid sizing
+// and launches on the caller's stream. No allocation, no synchronisation.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hetermoe.h"
+#include "grouped_gemm.cuh"
+#include "moe_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "%s: %s", what, cudaGetErrorString(e));
+  return 0;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---- TMA descriptor encoding -------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// bf16 tensor map with 128-byte swizzle. dims/strides innermost first; strides in bytes
+// for dims 1..rank-1.
+int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+             const uint64_t* strides_bytes, const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(HM_E_DRIVER, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base),
+                  reinterpret_cast<const cuuint64_t*>(dims),
+                  reinterpret_cast<const cuuint64_t*>(strides_bytes),
+                  reinterpret_cast<const cuuint32_t*>(box), estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HM_E_SHAPE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return 0;
+}
+
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
+int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
+                int max_ctas, cudaStream_t stream) {
+  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         hm::kGemmSmemBytes);
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attr: %s", cudaGetErrorString(e));
+    attr_set = true;
+  }
+  int grid = num_sms();
+  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
+  kern<<<grid, hm::kGemmThreads, hm::kGemmSmemBytes, stream>>>(ma, mb, p);
+  return check_launch("grouped_gemm");
+}
+
+}  // namespace
+
+extern "C" {
+
+int hm_abi_version(void) { return HM_ABI_VERSION; }
+const char* hm_last_error(void) { return g_last_error.c_str(); }
+int hm_num_sms(void) { return num_sms(); }
+
+// ---------------------------------------------------------------------------------------------
+size_t hm_router_chunk_elems(int T, int E) {
+  return static_cast<size_t>((T + hm::kChunk - 1) / hm::kChunk) * static_cast<size_t>(E);
+}
+
+int hm_router_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
+                   float* w, float* logits, int32_t* counts, int32_t* offsets,
+                   int32_t* chunk_base, void* stream) {
+  if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK || k > E)
+    return fail(HM_E_SHAPE, "router: unsupported shape T=%d d=%d E=%d k=%d", T, d, E, k);
+  if (!aligned16(x)) return fail(HM_E_ALIGN, "router: x not 16-byte aligned");
+  cudaStream_t st = S(stream);
+  const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
+  if (T == 0) {
+    cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, st);
+    cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), st);
+    return check_launch("router(empty)");
+  }
+  const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
+  const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(wg);
+  int eg = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
+  const size_t smem = static_cast<size_t>(d) * eg * 2;
+  if (smem > 200 * 1024) return fail(HM_E_SHAPE, "router: d*EG too large for shared memory");
+  const int ngroups = (E + eg - 1) / eg;
+  const int tt = (eg == 32) ? 2 : 4;
+  const int tok_per_iter = hm::kRouterWarps * tt;
+  int gx = (T + tok_per_iter - 1) / tok_per_iter;
+  const int cap = (2 * num_sms() + ngroups - 1) / ngroups;
+  if (gx > cap) gx = cap;
+  dim3 grid(gx, ngroups);
+  if (eg == 8) {
+    auto kern = hm::router_logits_kernel<8, 4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, T, d, E, logits);
+  } else if (eg == 16) {
+    auto kern = hm::router_logits_kernel<16, 4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, T, d, E, logits);
+  } else {
+    auto kern = hm::router_logits_kernel<32, 2>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, T, d, E, logits);
+  }
+  if (int rc = check_launch("router_logits")) return rc;
+  hm::router_topk_kernel<<<nchunk, 256, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+  if (int rc = check_launch("router_topk")) return rc;
+  hm::router_scan_kernel<<<1, 256, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
+  return check_launch("router_scan");
+}
+
+// ---------------------------------------------------------------------------------------------
+int hm_dispatch_permute(const void* x, const int32_t* idx, const int32_t* chunk_base, int T, int d,
+                        int E, int k, void* x_perm, int32_t* row_src, int32_t* row_of,
+                        void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK)
+    return fail(HM_E_SHAPE, "permute: unsupported shape T=%d d=%d E=%d k=%d", T, d, E, k);
+  if (!aligned16(x) || !aligned16(x_perm)) return fail(HM_E_ALIGN, "permute: x/x_perm alignment");
+  if (T == 0) return 0;
+  cudaStream_t st = S(stream);
+  const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
+  auto xb = static_cast<const __nv_bfloat16*>(x);
+  auto xp = static_cast<__nv_bfloat16*>(x_perm);
+#define HM_PERMUTE_CASE(V)                                                                      \
+  case V:                                                                                       \
+    hm::dispatch_permute_kernel<V><<<nchunk, 256, 0, st>>>(xb, idx, chunk_base, T, d, E, k, xp, \
+                                                            row_src, row_of);                   \
+    break;
+  if (d % 256 == 0 && d / 256 <= 16) {
+    switch (d / 256) {
+      HM_PERMUTE_CASE(1)
+      HM_PERMUTE_CASE(2)
+      HM_PERMUTE_CASE(4)
+      HM_PERMUTE_CASE(8)
+      HM_PERMUTE_CASE(16)
+      default:
+        hm::dispatch_permute_generic_kernel<<<nchunk, 256, 0, st>>>(xb, idx, chunk_base, T, d, E,
+                                                                    k, xp, row_src, row_of);
+    }
+  } else {
+    hm::dispatch_permute_generic_kernel<<<nchunk, 256, 0, st>>>(xb, idx, chunk_base, T, d, E, k,
+                                                                xp, row_src, row_of);
+  }
+#undef HM_PERMUTE_CASE
+  return check_launch("dispatch_permute");
+}
+
+#define HM_K_SWITCH(k, CALL)                                \
+  switch (k) {                                              \
+    case 1: { constexpr int K = 1; CALL; } break;           \
+    case 2: { constexpr int K = 2; CALL; } break;           \
+    case 3: { constexpr int K = 3; CALL; } break;           \
+    case 4: { constexpr int K = 4; CALL; } break;           \
+    case 5: { constexpr int K = 5; CALL; } break;           \
+    case 6: { constexpr int K = 6; CALL; } break;           \
+    case 7: { constexpr int K = 7; CALL; } break;           \
+    case 8: { constexpr int K = 8; CALL; } break;           \
+    default: return fail(HM_E_SHAPE, "unsupported k=%d", k); \
+  }
+
+static int row_grid(int T) {
+  const int warps = T;
+  int blocks = (warps + 7) / 8;
+  const int cap = num_sms() * 8;
+  return blocks < cap ? (blocks > 0 ? blocks : 1) : cap;
+}
+
+int hm_unpermute_sum(const void* dx_perm, const int32_t* row_of, int T, int d, int k, void* dx,
+                     void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0) return fail(HM_E_SHAPE, "unpermute: bad shape");
+  if (!aligned16(dx_perm) || !aligned16(dx)) return fail(HM_E_ALIGN, "unpermute: alignment");
+  if (T == 0) return 0;
+  auto in = static_cast<const __nv_bfloat16*>(dx_perm);
+  auto out = static_cast<__nv_bfloat16*>(dx);
+  HM_K_SWITCH(k, (hm::unpermute_sum_kernel<K><<<row_grid(T), 256, 0, S(stream)>>>(in, row_of, T, d, out)));
+  return check_launch("unpermute_sum");
+}
+
+int hm_combine(const void* y_perm, const int32_t* row_of, const float* w, int T, int d, int k,
+               void* y, void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0) return fail(HM_E_SHAPE, "combine: bad shape");
+  if (!aligned16(y_perm) || !aligned16(y)) return fail(HM_E_ALIGN, "combine: alignment");
+  if (T == 0) return 0;
+  auto in = static_cast<const __nv_bfloat16*>(y_perm);
+  auto out = static_cast<__nv_bfloat16*>(y);
+  HM_K_SWITCH(k, (hm::combine_kernel<K><<<row_grid(T), 256, 0, S(stream)>>>(in, row_of, w, T, d, out)));
+  return check_launch("combine");
+}
+
+int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, const float* w,
+                   int T, int d, int k, void* dy_perm, float* dw, void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0) return fail(HM_E_SHAPE, "combine_bwd: bad shape");
+  if (!aligned16(dy) || !aligned16(y_perm) || !aligned16(dy_perm))
+    return fail(HM_E_ALIGN, "combine_bwd: alignment");
+  if (T == 0) return 0;
+  auto g = static_cast<const __nv_bfloat16*>(dy);
+  auto yp = static_cast<const __nv_bfloat16*>(y_perm);
+  auto out = static_cast<__nv_bfloat16*>(dy_perm);
+  HM_K_SWITCH(k, (hm::combine_bwd_kernel<K><<<row_grid(T), 256, 0, S(stream)>>>(g, yp, row_of, w, T, d, out, dw)));
+  return check_launch("combine_bwd");
+}
+
+size_t hm_router_bwd_part_elems(int T, int d, int E) {
+  const int nsplit = 64;
+  (void)T;
+  return static_cast<size_t>(nsplit) * E * d;
+}
+
+int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
+                  const float* dw, const void* x, const void* wg_t, int T, int d, int E, int k,
+                  void* dx, float* dlogit, void* dwg, float* part, void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0 || E < 1 || E > 256) return fail(HM_E_SHAPE, "router_bwd: bad shape");
+  if (!aligned16(dx_perm) || !aligned16(dx) || !aligned16(wg_t))
+    return fail(HM_E_ALIGN, "router_bwd: alignment");
+  cudaStream_t st = S(stream);
+  if (T == 0) {
+    if (dwg) cudaMemsetAsync(dwg, 0, static_cast<size_t>(d) * E * 2, st);
+    return check_launch("router_bwd(empty)");
+  }
+  auto dp = static_cast<const __nv_bfloat16*>(dx_perm);
+  auto gt = static_cast<const __nv_bfloat16*>(wg_t);
+  auto out = static_cast<__nv_bfloat16*>(dx);
+  HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dlogit)));
+  if (int rc = check_launch("unpermute_router_bwd")) return rc;
+  if (dwg) {
+    if (!dlogit || !part) return fail(HM_E_ARG, "router_bwd: dwg needs dlogit and part");
+    const int nsplit = 64;
+    const int per = (T + nsplit - 1) / nsplit;
+    dim3 grid((d + 255) / 256, nsplit);
+    const size_t smem = static_cast<size_t>(E) * 256 * 4;
+    auto kern = hm::router_wgrad_partial_kernel;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, st>>>(static_cast<const __nv_bfloat16*>(x), idx, dlogit, T, d, E, k,
+                                  per, part);
+    if (int rc = check_launch("router_wgrad_partial")) return rc;
+    const long n = static_cast<long>(d) * E;
+    hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+        part, nsplit, d, E, static_cast<__nv_bfloat16*>(dwg));
+    return check_launch("router_wgrad_reduce");
+  }
+  return 0;
+}
+
+int hm_transpose_bf16(const void* in, int R, int C, void* out, void* stream) {
+  if (R <= 0 || C <= 0) return fail(HM_E_SHAPE, "transpose: bad shape");
+  dim3 grid((C + 31) / 32, (R + 31) / 32);
+  hm::transpose_bf16_kernel<<<grid, dim3(32, 8), 0, S(stream)>>>(
+      static_cast<const __nv_bfloat16*>(in), R, C, static_cast<__nv_bfloat16*>(out));
+  return check_launch("transpose_bf16");
+}
+
+// ---------------------------------------------------------------------------------------------
+int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_offsets, int E,
+                    int rows, int M, int N, int K, void* out, int ldo, void* out2, int ldo2,
+                    const void* aux, int ld_aux, int max_ctas, void* stream) {
+  if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "gemm: E=%d out of range", E);
+  if (rows < 0 || N <= 0 || N % 8 != 0) return fail(HM_E_SHAPE, "gemm: bad rows/N");
+  if (!aligned16(a) || !aligned16(b) || !aligned16(out)) return fail(HM_E_ALIGN, "gemm: alignment");
+  if (ldo % 8 != 0) return fail(HM_E_ALIGN, "gemm: ldo must be a multiple of 8");
+  cudaStream_t st = S(stream);
+  const bool wgrad = (mode == HM_GEMM_WGRAD);
+  if (!wgrad && (K <= 0 || K % 8 != 0)) return fail(HM_E_SHAPE, "gemm: K must be a positive multiple of 8");
+  if (wgrad && (M <= 0 || M % 8 != 0)) return fail(HM_E_SHAPE, "gemm: M must be a positive multiple of 8");
+  if (rows == 0 && !wgrad) return 0;
+
+  hm::GroupedGemmParams p{};
+  p.seg_offsets = seg_offsets;
+  p.E = E;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.ldo = ldo;
+  p.out2 = static_cast<__nv_bfloat16*>(out2);
+  p.ldo2 = ldo2;
+  p.aux = static_cast<const __nv_bfloat16*>(aux);
+  p.ld_aux = ld_aux;
+
+  CUtensorMap ma, mb;
+  const int rows_m = rows > 0 ? rows : 1;
+  if (!wgrad) {
+    {
+      uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows_m};
+      uint64_t str[1] = {(uint64_t)K * 2};
+      uint32_t box[2] = {64, 128};
+      if (int rc = make_map(&ma, a, 2, dims, str, box)) return rc;
+    }
+    const bool b_mn = (mode == HM_GEMM_BWD_DACT || mode == HM_GEMM_BWD_DX);
+    if (!b_mn) {
+      uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)E};
+      uint64_t str[2] = {(uint64_t)K * 2, (uint64_t)N * K * 2};
+      uint32_t box[3] = {64, 256, 1};
+      if (int rc = make_map(&mb, b, 3, dims, str, box)) return rc;
+    } else {
+      uint64_t dims[3] = {(uint64_t)N, (uint64_t)K, (uint64_t)E};
+      uint64_t str[2] = {(uint64_t)N * 2, (uint64_t)K * N * 2};
+      uint32_t box[3] = {64, 64, 1};
+      if (int rc = make_map(&mb, b, 3, dims, str, box)) return rc;
+    }
+    // raster: keep the larger operand outer so the smaller one is reused from L2
+    const double a_bytes = (double)rows / E * K;  // per-expert activation panel
+    const double b_bytes = (double)N * K;
+    p.n_fastest = (a_bytes > b_bytes) ? 1 : 0;
+  } else {
+    uint64_t dims_a[2] = {(uint64_t)M, (uint64_t)rows_m};
+    uint64_t str_a[1] = {(uint64_t)M * 2};
+    uint32_t box[2] = {64, 64};
+    if (int rc = make_map(&ma, a, 2, dims_a, str_a, box)) return rc;
+    uint64_t dims_b[2] = {(uint64_t)N, (uint64_t)rows_m};
+    uint64_t str_b[1] = {(uint64_t)N * 2};
+    if (int rc = make_map(&mb, b, 2, dims_b, str_b, box)) return rc;
+    p.n_fastest = (M >= N) ? 1 : 0;
+  }
+
+  switch (mode) {
+    case HM_GEMM_FWD_UPGATE:
+      if (N % 256 != 0 || !out2) return fail(HM_E_SHAPE, "upgate: N=2f must be a multiple of 256 and h given");
+      return launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD>(ma, mb, p, max_ctas, st);
+    case HM_GEMM_FWD_DOWN:
+      return launch_gemm<false, false, false, hm::EPI_STORE>(ma, mb, p, max_ctas, st);
+    case HM_GEMM_BWD_DACT:
+      if (N % 128 != 0 || !aux) return fail(HM_E_SHAPE, "dact: N=f must be a multiple of 128 and h given");
+      return launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD>(ma, mb, p, max_ctas, st);
+    case HM_GEMM_BWD_DX:
+      return launch_gemm<false, false, true, hm::EPI_STORE>(ma, mb, p, max_ctas, st);
+    case HM_GEMM_WGRAD:
+      return launch_gemm<true, true, true, hm::EPI_STORE>(ma, mb, p, max_ctas, st);
+    default:
+      return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
+  }
+}
+
+int hm_grouped_ffn_fwd(const void* x_perm, int rows, const int32_t* seg_offsets, int E,
+                       const void* w_ug, const void* w_d, int d, int f, void* h, void* act,
+                       void* y_perm, int max_ctas, void* stream) {
+  if (f % 128 != 0) return fail(HM_E_SHAPE, "ffn: f=%d must be a multiple of 128", f);
+  if (int rc = hm_grouped_gemm(HM_GEMM_FWD_UPGATE, x_perm, w_ug, seg_offsets, E, rows, 0, 2 * f, d,
+                               act, f, h, 2 * f, nullptr, 0, max_ctas, stream))
+    return rc;
+  return hm_grouped_gemm(HM_GEMM_FWD_DOWN, act, w_d, seg_offsets, E, rows, 0, d, f, y_perm, d,
+                         nullptr, 0, nullptr, 0, max_ctas, stream);
+}
+
+int hm_grouped_ffn_bwd(const void* dy_perm, const void* x_perm, const void* h, const void* act,
+                       int rows, const int32_t* seg_offsets, int E, const void* w_ug,
+                       const void* w_d, int d, int f, void* dh, void* dx_perm, void* dw_ug,
+                       void* dw_d, int max_ctas, void* stream) {
+  if (f % 128 != 0) return fail(HM_E_SHAPE, "ffn: f=%d must be a multiple of 128", f);
+  // dH = SwiGLU'(dY . W_d[e]) : K = d, N = f
+  if (int rc = hm_grouped_gemm(HM_GEMM_BWD_DACT, dy_perm, w_d, seg_offsets, E, rows, 0, f, d, dh,
+                               2 * f, nullptr, 0, h, 2 * f, max_ctas, stream))
+    return rc;
+  // dX = dH . W_ug[e] : K = 2f, N = d
+  if (int rc = hm_grouped_gemm(HM_GEMM_BWD_DX, dh, w_ug, seg_offsets, E, rows, 0, d, 2 * f, dx_perm,
+                               d, nullptr, 0, nullptr, 0, max_ctas, stream))
+    return rc;
+  // dW_ug[e] = dH_e^T . X_e : M = 2f, N = d
+  if (int rc = hm_grouped_gemm(HM_GEMM_WGRAD, dh, x_perm, seg_offsets, E, rows, 2 * f, d, 0, dw_ug,
+                               d, nullptr, 0, nullptr, 0, max_ctas, stream))
+    return rc;
+  // dW_d[e] = dY_e^T . act_e : M = d, N = f
+  return hm_grouped_gemm(HM_GEMM_WGRAD, dy_perm, act, seg_offsets, E, rows, d, f, 0, dw_d, f,
+                         nullptr, 0, nullptr, 0, max_ctas, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+// grouped_gemm.cuh — K3: persistent, warp-specialised grouped GEMM on tcgen05/TMEM fed by TMA.
+//
+// One kernel template covers every contraction of the SwiGLU expert FFN:
+//
+//   GROUP_M (rows of the activation buffer are grouped by expert, weights indexed by expert):
+//     fwd  up+gate : H[m_e, 2f]  = X[m_e, d]  · W_ug[e]^T   (W_ug[e] stored [2f, d], K-major)  EPI_SWIGLU_FWD
+//     fwd  down    : Y[m_e, d]   = A[m_e, f]  · W_d[e]^T    (W_d[e]  stored [d, f],  K-major)  EPI_STORE
+//     bwd  dgrad 1 : dA[m_e, f]  = dY[m_e, d] · W_d[e]      (W_d[e] as [K=d][N=f], MN-major)   EPI_SWIGLU_BWD
+//     bwd  dgrad 2 : dX[m_e, d]  = dH[m_e,2f] · W_ug[e]     (W_ug[e] as [K=2f][N=d], MN-major) EPI_STORE
+//   GROUP_K (the reduction runs over one expert's rows; variable K = m_e, possibly 0):
+//     bwd  wgrad   : dW_ug[e] = dH_e^T · X_e ,  dW_d[e] = dY_e^T · A_e   (both operands MN-major) EPI_STORE
+//
+// Tiles are 128 x 256 x 64 (UMMA M=128, N=256, K=16 x 4), 4-stage TMA ring (48 KB / stage),
+// two 256-column fp32 accumulators in TMEM so the epilogue of tile i overlaps the MMAs of i+1.
+// Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (lane 0 issues), warps 2..5 = epilogue
+// (warp w reads TMEM lanes 32*(w%4) .. +31, i.e. one accumulator row per thread).
+//
+// Tiles that straddle an expert boundary (GROUP_M) load a few rows of the next expert; those
+// rows are computed with the wrong weights and are never stored (row mask in the epilogue).
+// For GROUP_K the last K block of an expert would contract rows of the next expert, so the
+// MMA warp zero-fills those rows of the A tile in shared memory before issuing the MMAs.
+#pragma once
+
+#include "hm_common.cuh"
+
+namespace hm {
+
+enum EpilogueKind : int { EPI_STORE = 0, EPI_SWIGLU_FWD = 1, EPI_SWIGLU_BWD = 2 };
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBK = 64;
+constexpr int kStages = 4;
+constexpr int kATileBytes = kBM * kBK * 2;  // 16 KB
+constexpr int kBTileBytes = kBN * kBK * 2;  // 32 KB
+constexpr int kStageBytes = kATileBytes + kBTileBytes;
+constexpr int kMaxExperts = 256;
+constexpr int kGemmThreads = 192;
+constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
+constexpr int kGemmSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 4096 /*bookkeeping*/;
+
+struct GroupedGemmParams {
+  const int* seg_offsets;  // [E+1] row offsets of each expert's segment in the activation buffer
+  int E;
+  int M;   // GROUP_K: output rows per expert (weight rows). GROUP_M: unused.
+  int N;   // output columns of the GEMM
+  int K;   // GROUP_M: reduction length. GROUP_K: unused (per-expert m_e).
+  __nv_bfloat16* out;  // EPI_STORE: D;  SWIGLU_FWD: act [rows, N/2];  SWIGLU_BWD: dH [rows, 2N]
+  int ldo;
+  __nv_bfloat16* out2;  // SWIGLU_FWD: h = [gate|up] pre-activations [rows, N]
+  int ldo2;
+  const __nv_bfloat16* aux;  // SWIGLU_BWD: h saved by the forward [rows, 2N]
+  int ld_aux;
+  int n_fastest;  // raster: 1 = n-tile index varies fastest within an expert
+};
+
+struct GemmShared {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t tmem_full[2];
+  uint64_t tmem_empty[2];
+  uint32_t tmem_base;
+  int tile_prefix[kMaxExperts + 1];  // first global tile index of each expert
+  int seg[kMaxExperts + 1];          // copy of seg_offsets
+};
+
+struct TileCoord {
+  int e, mt, nt;
+};
+
+template <bool GROUP_K>
+HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_fixed, int ntiles,
+                             int n_fastest) {
+  // binary search: largest e with tile_prefix[e] <= tile
+  int lo = 0, hi = E - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (sh.tile_prefix[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  const int local = tile - sh.tile_prefix[lo];
+  int mtiles;
+  if (GROUP_K) mtiles = mtiles_fixed;
+  else mtiles = (sh.seg[lo + 1] - sh.seg[lo] + kBM - 1) / kBM;
+  TileCoord c;
+  c.e = lo;
+  if (n_fastest) { c.mt = local / ntiles; c.nt = local % ntiles; }
+  else { c.nt = local / mtiles; c.mt = local % mtiles; }
+  return c;
+}
+
+HM_DEV float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+// 32 consecutive fp32 accumulator columns of one row -> 32 bf16 (64 bytes) at dst
+HM_DEV void store_row32(__nv_bfloat16* dst, const float* v, int valid_cols) {
+  if (valid_cols >= 32) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w;
+      w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
+      w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
+      w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
+      w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
+      d4[q] = w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < valid_cols) dst[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, GroupedGemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  GemmShared& sh = *reinterpret_cast<GemmShared*>(tiles + kStages * kStageBytes);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int E = p.E;
+
+  // ---- per-CTA bookkeeping: expert segment table and tile prefix sums --------------------
+  const int ntiles = (p.N + kBN - 1) / kBN;
+  const int mtiles_fixed = GROUP_K ? (p.M + kBM - 1) / kBM : 0;
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) sh.seg[i] = p.seg_offsets[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      sh.tile_prefix[e] = acc;
+      const int me = sh.seg[e + 1] - sh.seg[e];
+      acc += (GROUP_K ? mtiles_fixed : (me + kBM - 1) / kBM) * ntiles;
+    }
+    sh.tile_prefix[E] = acc;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&sh.tmem_full[a], 1);
+      mbar_init(&sh.tmem_empty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&map_a);
+      tma_prefetch_desc(&map_b);
+    }
+  } else if (warp == 1) {
+    tmem_alloc(&sh.tmem_base, kTmemCols);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const int total_tiles = sh.tile_prefix[E];
+  const uint32_t tmem_base = sh.tmem_base;
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      const uint64_t pol_act = policy_evict_normal();
+      const uint64_t pol_w = policy_evict_normal();
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const TileCoord tc = decode_tile<GROUP_K>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+        const int seg0 = sh.seg[tc.e];
+        const int me = sh.seg[tc.e + 1] - seg0;
+        const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&sh.empty[s], ph ^ 1);
+          uint8_t* sa = tiles + s * kStageBytes;
+          uint8_t* sb = sa + kATileBytes;
+          mbar_arrive_expect_tx(&sh.full[s], kStageBytes);
+          if (!GROUP_K) {
+            // A: activation rows [seg0 + mt*128, +128), K-major box {64, 128}
+            tma_load_2d(sa, &map_a, &sh.full[s], kb * kBK, seg0 + tc.mt * kBM, pol_act);
+            if (!B_MN) {
+              // B: W[e] stored [N][K]; box {64, 256}
+              tma_load_3d(sb, &map_b, &sh.full[s], kb * kBK, tc.nt * kBN, tc.e, pol_w);
+            } else {
+              // B: W[e] stored [K][N]; four 64-wide N panels, box {64 (N), 64 (K)}
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                tma_load_3d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, kb * kBK,
+                            tc.e, pol_w);
+            }
+          } else {
+            // wgrad: both operands are [rows = K][cols] activations (MN-major), box {64, 64}
+            const int k0 = seg0 + kb * kBK;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              tma_load_2d(sa + q * 8192, &map_a, &sh.full[s], tc.mt * kBM + q * 64, k0, pol_w);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              tma_load_2d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, k0, pol_w);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    constexpr uint32_t idesc = make_idesc_bf16(kBM, kBN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+    uint32_t it = 0, tcount = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const TileCoord tc = decode_tile<GROUP_K>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+      const int seg0 = sh.seg[tc.e];
+      const int me = sh.seg[tc.e + 1] - seg0;
+      const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
+      if (nk == 0) continue;  // epilogue writes zeros for this tile without touching TMEM
+      const int acc = tcount & 1;
+      const uint32_t aph = (tcount >> 1) & 1;
+      mbar_wait(&sh.tmem_empty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * kBN;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % kStages;
+        const uint32_t ph = (it / kStages) & 1;
+        mbar_wait(&sh.full[s], ph);
+        tc_fence_after();
+        uint8_t* sa = tiles + s * kStageBytes;
+        uint8_t* sb = sa + kATileBytes;
+        if (GROUP_K && kb == nk - 1) {
+          const int rem = me - kb * kBK;  // valid K rows in this block (1..64)
+          if (rem < kBK) {
+            // zero K rows [rem, 64) of both 64-wide panels of the MN-major A tile
+            const int nrows = kBK - rem;
+            for (int i = lane; i < nrows * 2 * 8; i += 32) {
+              const int chunk = i & 7;
+              const int rr = rem + ((i >> 3) % nrows);
+              const int q = (i >> 3) / nrows;
+              uint4* dst = reinterpret_cast<uint4*>(sa + q * 8192 + (rr >> 3) * 1024 + (rr & 7) * 128) + chunk;
+              *dst = make_uint4(0u, 0u, 0u, 0u);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+          }
+        }
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sa);
+          const uint32_t b_addr = smem_u32(sb);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t adesc = A_MN ? make_sw128_desc(a_addr + kk * 2048, 8192, 1024)
+                                        : make_sw128_desc(a_addr + kk * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? make_sw128_desc(b_addr + kk * 2048, 8192, 1024)
+                                        : make_sw128_desc(b_addr + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&sh.empty[s]);
+          if (kb == nk - 1) umma_commit(&sh.tmem_full[acc]);
+        }
+        __syncwarp();
+      }
+      ++tcount;
+    }
+  } else {
+    // ======================= epilogue (warps 2..5) =======================
+    const int quad = warp & 3;
+    const int row_in_tile = quad * 32 + lane;
+    uint32_t tcount = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const TileCoord tc = decode_tile<GROUP_K>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+      const int seg0 = sh.seg[tc.e];
+      const int me = sh.seg[tc.e + 1] - seg0;
+      const int n0 = tc.nt * kBN;
+      const int ncols_valid = min(kBN, p.N - n0);
+      long grow;       // global output row
+      bool row_ok;
+      if (!GROUP_K) {
+        row_ok = tc.mt * kBM + row_in_tile < me;
+        grow = static_cast<long>(seg0) + tc.mt * kBM + row_in_tile;
+      } else {
+        row_ok = tc.mt * kBM + row_in_tile < p.M;
+        grow = static_cast<long>(tc.e) * p.M + tc.mt * kBM + row_in_tile;
+      }
+      if (GROUP_K && me == 0) {
+        // empty expert: its weight gradient is exactly zero
+        if (row_ok) {
+          float z[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) z[j] = 0.f;
+          for (int c = 0; c < ncols_valid; c += 32)
+            store_row32(p.out + grow * p.ldo + n0 + c, z, min(32, ncols_valid - c));
+        }
+        continue;
+      }
+      const int acc = tcount & 1;
+      const uint32_t aph = (tcount >> 1) & 1;
+      mbar_wait(&sh.tmem_full[acc], aph);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kBN;
+
+      if (EPI == EPI_STORE) {
+        for (int c = 0; c < kBN; c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c, r);
+          tmem_ld_wait();
+          if (row_ok && c < ncols_valid)
+            store_row32(p.out + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
+                        min(32, ncols_valid - c));
+        }
+      } else if (EPI == EPI_SWIGLU_FWD) {
+        // columns [0,128) = gate, [128,256) = up for f-columns [nt*128, +128)
+        const int f0 = tc.nt * (kBN / 2);
+        for (int c = 0; c < kBN / 2; c += 32) {
+          uint32_t rg[32], ru[32];
+          tmem_ld_32x32b_x32(t_row + c, rg);
+          tmem_ld_32x32b_x32(t_row + kBN / 2 + c, ru);
+          tmem_ld_wait();
+          if (row_ok) {
+            float* g = reinterpret_cast<float*>(rg);
+            float* u = reinterpret_cast<float*>(ru);
+            // saved pre-activations are the bf16-rounded accumulators; the activation is
+            // computed from the same rounded values so forward and backward agree exactly.
+            float gq[32], uq[32], a[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              gq[j] = __bfloat162float(__float2bfloat16_rn(g[j]));
+              uq[j] = __bfloat162float(__float2bfloat16_rn(u[j]));
+              a[j] = silu_f(gq[j]) * uq[j];
+            }
+            store_row32(p.out2 + grow * p.ldo2 + n0 + c, gq, 32);
+            store_row32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, uq, 32);
+            store_row32(p.out + grow * p.ldo + f0 + c, a, 32);
+          }
+        }
+      } else {  // EPI_SWIGLU_BWD: D = dA for f-columns [n0, n0+256)
+        for (int c = 0; c < kBN; c += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c, r);
+          tmem_ld_wait();
+          const int fcol = n0 + c;  // multiple of 32; a 32-chunk never crosses a 128 block
+          if (row_ok && c < ncols_valid) {
+            const int hcol = (fcol >> 7) * 256 + (fcol & 127);
+            const __nv_bfloat16* hg = p.aux + grow * p.ld_aux + hcol;
+            const __nv_bfloat16* hu = hg + 128;
+            const float* da = reinterpret_cast<float*>(r);
+            float dg[32], du[32];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 gv = *reinterpret_cast<const uint4*>(hg + q * 8);
+              uint4 uv = *reinterpret_cast<const uint4*>(hu + q * 8);
+              const uint16_t* gs = reinterpret_cast<const uint16_t*>(&gv);
+              const uint16_t* us = reinterpret_cast<const uint16_t*>(&uv);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float g = bf16_to_f32(gs[j]);
+                const float u = bf16_to_f32(us[j]);
+                const float sg = 1.0f / (1.0f + __expf(-g));
+                const float d = da[q * 8 + j];
+                du[q * 8 + j] = d * g * sg;
+                dg[q * 8 + j] = d * u * sg * (1.0f + g * (1.0f - sg));
+              }
+            }
+            store_row32(p.out + grow * p.ldo + hcol, dg, 32);
+            store_row32(p.out + grow * p.ldo + hcol + 128, du, 32);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.tmem_empty[acc]);
+      ++tcount;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, kTmemCols);
+  }
+}
+
+}  // namespace hm

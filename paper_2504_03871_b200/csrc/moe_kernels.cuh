@@ -1,0 +1,504 @@
+// moe_kernels.cuh — K1 router/top-k, K2 dispatch permute (+ unpermute), K4 combine (+ bwd).
+//
+// Semantics fixed by the CPU oracle (oracle/moe_oracle.py):
+//  * router logits l[t,e] = sum_i x[t,i] * Wg[i,e] in fp32 with a FIXED order: lane L of a warp
+//    accumulates i = 256*j + 8*L + q (j ascending, then q = 0..7) with fused multiply-adds
+//    (bf16*bf16 products are exact in fp32, so FMA == mul-then-add), then the 32 lane partials
+//    are combined by an xor butterfly (offsets 16, 8, 4, 2, 1). Indices, counts and the
+//    permutation therefore reproduce bit-for-bit on the CPU.
+//  * top-k: k largest logits, ties -> lower expert id; w = softmax over the k selected logits.
+//  * dispatch order: stable by (expert, token); a token appears at most once per expert.
+//    Tokens are processed in chunks of kChunk; chunk c's rows for expert e start at
+//    chunk_base[c][e] = offsets[e] + sum_{c'<c} count[c'][e].
+#pragma once
+
+#include "hm_common.cuh"
+
+namespace hm {
+
+constexpr int kChunk = 256;         // tokens per dispatch chunk (one permute CTA)
+constexpr int kMaxTopK = 8;
+constexpr int kRouterWarps = 8;
+
+// ------------------------------------------------------------------------------------------
+// K1a: router logits. grid = (token blocks, expert groups). EG experts per group staged in
+// shared memory as [d][EG] bf16. Each warp handles TT tokens at a time.
+template <int EG, int TT>
+__global__ void __launch_bounds__(kRouterWarps * 32)
+    router_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                         int T, int d, int E, float* __restrict__ logits) {
+  extern __shared__ __align__(16) uint8_t smem_r[];
+  __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(smem_r);  // [d][EG]
+  const int e0 = blockIdx.y * EG;
+  // stage Wg[:, e0:e0+EG]
+  for (int idx = threadIdx.x; idx < d * EG; idx += blockDim.x) {
+    const int i = idx / EG, e = idx % EG;
+    ws[idx] = (e0 + e < E) ? wg[static_cast<long>(i) * E + e0 + e] : __float2bfloat16(0.f);
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = d / 256;
+  const int tokens_per_block_iter = kRouterWarps * TT;
+  for (int t0 = blockIdx.x * tokens_per_block_iter + warp * TT; t0 < T;
+       t0 += gridDim.x * tokens_per_block_iter) {
+    float acc[TT][EG];
+#pragma unroll
+    for (int a = 0; a < TT; ++a)
+#pragma unroll
+      for (int e = 0; e < EG; ++e) acc[a][e] = 0.f;
+
+    for (int j = 0; j < nj; ++j) {
+      const int ibase = j * 256 + lane * 8;
+      uint4 xv[TT];
+#pragma unroll
+      for (int a = 0; a < TT; ++a) {
+        const int t = min(t0 + a, T - 1);
+        xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase));
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const __nv_bfloat16* wrow = ws + (ibase + q) * EG;
+        float wv[EG];
+#pragma unroll
+        for (int e = 0; e < EG; e += 8) {
+          uint4 w8 = *reinterpret_cast<const uint4*>(wrow + e);
+          const uint16_t* ws16 = reinterpret_cast<const uint16_t*>(&w8);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) wv[e + z] = bf16_to_f32(ws16[z]);
+        }
+#pragma unroll
+        for (int a = 0; a < TT; ++a) {
+          const float xf = bf16_to_f32(reinterpret_cast<const uint16_t*>(&xv[a])[q]);
+#pragma unroll
+          for (int e = 0; e < EG; ++e) acc[a][e] = __fmaf_rn(xf, wv[e], acc[a][e]);
+        }
+      }
+    }
+    // xor butterfly across lanes (fixed order 16, 8, 4, 2, 1)
+#pragma unroll
+    for (int a = 0; a < TT; ++a)
+#pragma unroll
+      for (int e = 0; e < EG; ++e) {
+        float v = acc[a][e];
+        v = v + __shfl_xor_sync(0xffffffffu, v, 16);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 8);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 4);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 2);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 1);
+        acc[a][e] = v;
+      }
+    // lane e writes expert e (EG <= 32)
+#pragma unroll
+    for (int a = 0; a < TT; ++a) {
+      const int t = t0 + a;
+      if (t < T) {
+#pragma unroll
+        for (int e = 0; e < EG; ++e)
+          if (lane == e && e0 + e < E) logits[static_cast<long>(t) * E + e0 + e] = acc[a][e];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K1b: top-k + softmax + per-chunk expert histogram. One CTA per chunk of kChunk tokens,
+// one warp per token (looping). E <= 256.
+__global__ void __launch_bounds__(256)
+    router_topk_kernel(const float* __restrict__ logits, int T, int E, int k,
+                       int32_t* __restrict__ idx, float* __restrict__ w,
+                       int32_t* __restrict__ chunk_counts /*[nchunk][E]*/) {
+  __shared__ int hist[256];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int tbeg = c * kChunk, tend = min(T, tbeg + kChunk);
+  constexpr int kPer = 8;  // values per lane (E <= 256)
+  for (int t = tbeg + warp; t < tend; t += 8) {
+    float v[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = q * 32 + lane;
+      v[q] = (e < E) ? logits[static_cast<long>(t) * E + e] : -INFINITY;
+    }
+    float sel_l[kMaxTopK];
+    int sel_e[kMaxTopK];
+    for (int s = 0; s < k; ++s) {
+      // lane-local best (ties -> lower id = lower q since e = q*32+lane ascends with q)
+      float bv = -INFINITY;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = q * 32 + lane;
+        if (e < E && (v[q] > bv || (v[q] == bv && e < be))) { bv = v[q]; be = e; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+      }
+      sel_l[s] = bv;
+      sel_e[s] = be;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q)
+        if (q * 32 + lane == be) v[q] = -INFINITY;
+    }
+    if (lane == 0) {
+      // softmax over the k selected logits (sel_l[0] is the max)
+      float ex[kMaxTopK];
+      float sum = 0.f;
+      for (int s = 0; s < k; ++s) { ex[s] = expf(sel_l[s] - sel_l[0]); sum += ex[s]; }
+      for (int s = 0; s < k; ++s) {
+        idx[static_cast<long>(t) * k + s] = sel_e[s];
+        w[static_cast<long>(t) * k + s] = ex[s] / sum;
+        atomicAdd(&hist[sel_e[s]], 1);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    chunk_counts[static_cast<long>(c) * E + e] = hist[e];
+}
+
+// ------------------------------------------------------------------------------------------
+// K1c: counts / offsets / chunk bases. Single CTA; thread e owns expert e.
+__global__ void __launch_bounds__(256)
+    router_scan_kernel(int32_t* __restrict__ chunk_counts /*in: counts, out: bases*/, int nchunk,
+                       int E, int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
+  __shared__ int tot[256];
+  __shared__ int off[257];
+  const int e = threadIdx.x;
+  int s = 0;
+  if (e < E)
+    for (int c = 0; c < nchunk; ++c) s += chunk_counts[static_cast<long>(c) * E + e];
+  tot[e] = (e < E) ? s : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int i = 0; i < E; ++i) { off[i] = a; a += tot[i]; }
+    off[E] = a;
+  }
+  __syncthreads();
+  if (e < E) {
+    counts[e] = tot[e];
+    offsets[e] = off[e];
+    int base = off[e];
+    for (int c = 0; c < nchunk; ++c) {
+      const int n = chunk_counts[static_cast<long>(c) * E + e];
+      chunk_counts[static_cast<long>(c) * E + e] = base;
+      base += n;
+    }
+  }
+  if (threadIdx.x == 0) offsets[E] = off[E];
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: dispatch permute. One CTA per chunk: (1) thread e walks the chunk's tokens in order and
+// assigns destination rows for expert e (stable), (2) warps copy token rows with 128-bit loads
+// and k 128-bit stores per 16-byte segment.
+template <int VPL>  // 16-byte vectors per lane per token row (d = VPL * 256)
+__global__ void __launch_bounds__(256)
+    dispatch_permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
+                            const int32_t* __restrict__ chunk_base, int T, int d, int E, int k,
+                            __nv_bfloat16* __restrict__ x_perm, int32_t* __restrict__ row_src,
+                            int32_t* __restrict__ row_of) {
+  __shared__ int s_idx[kChunk * kMaxTopK];
+  __shared__ int s_row[kChunk * kMaxTopK];
+  const int c = blockIdx.x;
+  const int tbeg = c * kChunk;
+  const int nt = min(kChunk, T - tbeg);
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) s_idx[i] = idx[static_cast<long>(tbeg) * k + i];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int r = chunk_base[static_cast<long>(c) * E + e];
+    for (int i = 0; i < nt * k; ++i)
+      if (s_idx[i] == e) s_row[i] = r++;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int r = s_row[i];
+    row_of[static_cast<long>(tbeg) * k + i] = r;
+    row_src[r] = tbeg + i / k;
+  }
+  // row copies
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int tt = warp; tt < nt; tt += 8) {
+    const long t = tbeg + tt;
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+    uint4 v[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) v[q] = __ldg(src + q * 32 + lane);
+    for (int s = 0; s < k; ++s) {
+      uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<long>(s_row[tt * k + s]) * d);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) dst[q * 32 + lane] = v[q];
+    }
+  }
+}
+
+// generic-d fallback of the row copy (d multiple of 8)
+__global__ void __launch_bounds__(256)
+    dispatch_permute_generic_kernel(const __nv_bfloat16* __restrict__ x,
+                                    const int32_t* __restrict__ idx,
+                                    const int32_t* __restrict__ chunk_base, int T, int d, int E,
+                                    int k, __nv_bfloat16* __restrict__ x_perm,
+                                    int32_t* __restrict__ row_src, int32_t* __restrict__ row_of) {
+  __shared__ int s_idx[kChunk * kMaxTopK];
+  __shared__ int s_row[kChunk * kMaxTopK];
+  const int c = blockIdx.x;
+  const int tbeg = c * kChunk;
+  const int nt = min(kChunk, T - tbeg);
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) s_idx[i] = idx[static_cast<long>(tbeg) * k + i];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int r = chunk_base[static_cast<long>(c) * E + e];
+    for (int i = 0; i < nt * k; ++i)
+      if (s_idx[i] == e) s_row[i] = r++;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int r = s_row[i];
+    row_of[static_cast<long>(tbeg) * k + i] = r;
+    row_src[r] = tbeg + i / k;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = d / 8;
+  for (int tt = warp; tt < nt; tt += 8) {
+    const long t = tbeg + tt;
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+    for (int q = lane; q < nv; q += 32) {
+      const uint4 v = __ldg(src + q);
+      for (int s = 0; s < k; ++s)
+        reinterpret_cast<uint4*>(x_perm + static_cast<long>(s_row[tt * k + s]) * d)[q] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K4: combine. y[t] = sum_s w[t,s] * y_perm[row_of[t,s]] (fp32 accumulate in slot order).
+// One warp per token; lane handles 8-element (16-byte) segments.
+template <int K>
+__global__ void __launch_bounds__(256)
+    combine_kernel(const __nv_bfloat16* __restrict__ y_perm, const int32_t* __restrict__ row_of,
+                   const float* __restrict__ w, int T, int d, __nv_bfloat16* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = d / 8;
+  for (int t = warp; t < T; t += nwarps) {
+    int rows[kMaxTopK];
+    float ws[kMaxTopK];
+    for (int s = 0; s < K; ++s) {
+      rows[s] = row_of[static_cast<long>(t) * K + s];
+      ws[s] = w[static_cast<long>(t) * K + s];
+    }
+    for (int q = lane; q < nv; q += 32) {
+      float acc[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+      uint4 v[kMaxTopK];
+      for (int s = 0; s < K; ++s)
+        v[s] = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q);
+      for (int s = 0; s < K; ++s) {
+        const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[s]);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(ws[s], bf16_to_f32(h[z]), acc[z]);
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      reinterpret_cast<uint4*>(y + static_cast<long>(t) * d)[q] = o;
+    }
+  }
+}
+
+// combine backward: dy_perm[row_of[t,s]] = w[t,s] * dy[t];  dw[t,s] = <dy[t], y_perm[row_of[t,s]]>
+template <int K>
+__global__ void __launch_bounds__(256)
+    combine_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ y_perm,
+                       const int32_t* __restrict__ row_of, const float* __restrict__ w, int T, int d, __nv_bfloat16* __restrict__ dy_perm, float* __restrict__ dw) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = d / 8;
+  for (int t = warp; t < T; t += nwarps) {
+    int rows[kMaxTopK];
+    float ws[kMaxTopK], dot[kMaxTopK];
+    for (int s = 0; s < K; ++s) {
+      rows[s] = row_of[static_cast<long>(t) * K + s];
+      ws[s] = w[static_cast<long>(t) * K + s];
+      dot[s] = 0.f;
+    }
+    for (int q = lane; q < nv; q += 32) {
+      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy + static_cast<long>(t) * d) + q);
+      const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g);
+      float gf[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) gf[z] = bf16_to_f32(gh[z]);
+      for (int s = 0; s < K; ++s) {
+        const uint4 yv = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q);
+        const uint16_t* yh = reinterpret_cast<const uint16_t*>(&yv);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) dot[s] = __fmaf_rn(gf[z], bf16_to_f32(yh[z]), dot[s]);
+        uint4 o;
+        o.x = pack_bf16x2(ws[s] * gf[0], ws[s] * gf[1]);
+        o.y = pack_bf16x2(ws[s] * gf[2], ws[s] * gf[3]);
+        o.z = pack_bf16x2(ws[s] * gf[4], ws[s] * gf[5]);
+        o.w = pack_bf16x2(ws[s] * gf[6], ws[s] * gf[7]);
+        reinterpret_cast<uint4*>(dy_perm + static_cast<long>(rows[s]) * d)[q] = o;
+      }
+    }
+    for (int s = 0; s < K; ++s) {
+      float v = dot[s];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) dw[static_cast<long>(t) * K + s] = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Dispatch backward fused with the router's input gradient:
+//   dlogit[t,s] = w[t,s] * (dw[t,s] - sum_j w[t,j] dw[t,j])        (softmax over the selected k)
+//   dx[t]       = sum_s dx_perm[row_of[t,s]] + sum_s dlogit[t,s] * Wg[:, idx[t,s]]
+// wg_t is Wg transposed ([E][d]). Also writes dlogit (for the router weight gradient).
+template <int K>
+__global__ void __launch_bounds__(256)
+    unpermute_router_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm,
+                                const int32_t* __restrict__ row_of, const int32_t* __restrict__ idx,
+                                const float* __restrict__ w, const float* __restrict__ dw,
+                                const __nv_bfloat16* __restrict__ wg_t, int T, int d,
+                                __nv_bfloat16* __restrict__ dx, float* __restrict__ dlogit) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = d / 8;
+  for (int t = warp; t < T; t += nwarps) {
+    int rows[kMaxTopK], ex[kMaxTopK];
+    float dl[kMaxTopK];
+    float wsum = 0.f;
+    for (int s = 0; s < K; ++s) {
+      rows[s] = row_of[static_cast<long>(t) * K + s];
+      ex[s] = idx[static_cast<long>(t) * K + s];
+      wsum += w[static_cast<long>(t) * K + s] * dw[static_cast<long>(t) * K + s];
+    }
+    for (int s = 0; s < K; ++s) {
+      const float ws = w[static_cast<long>(t) * K + s];
+      dl[s] = ws * (dw[static_cast<long>(t) * K + s] - wsum);
+      if (lane == 0 && dlogit) dlogit[static_cast<long>(t) * K + s] = dl[s];
+    }
+    for (int q = lane; q < nv; q += 32) {
+      float acc[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+      for (int s = 0; s < K; ++s) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(dx_perm + static_cast<long>(rows[s]) * d) + q);
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(wg_t + static_cast<long>(ex[s]) * d) + q);
+        const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v);
+        const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) {
+          acc[z] += bf16_to_f32(vh[z]);
+          acc[z] = __fmaf_rn(dl[s], bf16_to_f32(gh[z]), acc[z]);
+        }
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      reinterpret_cast<uint4*>(dx + static_cast<long>(t) * d)[q] = o;
+    }
+  }
+}
+
+// plain unpermute-sum: dx[t] = sum_s dx_perm[row_of[t,s]]
+template <int K>
+__global__ void __launch_bounds__(256)
+    unpermute_sum_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_of,
+                         int T, int d, __nv_bfloat16* __restrict__ dx) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = d / 8;
+  for (int t = warp; t < T; t += nwarps) {
+    int rows[kMaxTopK];
+    for (int s = 0; s < K; ++s) rows[s] = row_of[static_cast<long>(t) * K + s];
+    for (int q = lane; q < nv; q += 32) {
+      float acc[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+      for (int s = 0; s < K; ++s) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(dx_perm + static_cast<long>(rows[s]) * d) + q);
+        const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) acc[z] += bf16_to_f32(vh[z]);
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      reinterpret_cast<uint4*>(dx + static_cast<long>(t) * d)[q] = o;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Router weight gradient dWg[i,e] = sum_t x[t,i] * dlogit_dense[t,e] (only the k selected
+// experts are non-zero). grid = (d/256, nsplit); each CTA owns 256 columns and a token range,
+// accumulates per-expert sums in shared memory ([E][256] fp32), and writes a partial slab
+// part[split][e][i]. router_wgrad_reduce sums the slabs in split order (deterministic).
+__global__ void __launch_bounds__(256)
+    router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
+                                const float* __restrict__ dlogit, int T, int d, int E, int k,
+                                int tokens_per_split, float* __restrict__ part) {
+  extern __shared__ float accs[];  // [E][256]
+  const int col = blockIdx.x * 256 + threadIdx.x;
+  for (int e = 0; e < E; ++e) accs[e * 256 + threadIdx.x] = 0.f;
+  const int t0 = blockIdx.y * tokens_per_split;
+  const int t1 = min(T, t0 + tokens_per_split);
+  for (int t = t0; t < t1; ++t) {
+    const float xv = (col < d) ? __bfloat162float(x[static_cast<long>(t) * d + col]) : 0.f;
+    for (int s = 0; s < k; ++s) {
+      const int e = idx[static_cast<long>(t) * k + s];
+      const float g = dlogit[static_cast<long>(t) * k + s];
+      accs[e * 256 + threadIdx.x] = __fmaf_rn(xv, g, accs[e * 256 + threadIdx.x]);
+    }
+  }
+  if (col < d)
+    for (int e = 0; e < E; ++e)
+      part[(static_cast<long>(blockIdx.y) * E + e) * d + col] = accs[e * 256 + threadIdx.x];
+}
+
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nsplit, int d, int E,
+                                           __nv_bfloat16* __restrict__ dwg /*[d][E]*/) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(d) * E) return;
+  const int col = static_cast<int>(i / E), e = static_cast<int>(i % E);
+  float s = 0.f;
+  for (int p = 0; p < nsplit; ++p) s += part[(static_cast<long>(p) * E + e) * d + col];
+  dwg[i] = __float2bfloat16_rn(s);
+}
+
+// bf16 transpose [R][C] -> [C][R] (router weight layout helper)
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ in, int R, int C,
+                                      __nv_bfloat16* __restrict__ out) {
+  __shared__ __nv_bfloat16 tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + j, c = bx + threadIdx.x;
+    if (r < R && c < C) tile[j][threadIdx.x] = in[static_cast<long>(r) * C + c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int c = bx + j, r = by + threadIdx.x;
+    if (r < R && c < C) out[static_cast<long>(c) * R + r] = tile[threadIdx.x][j];
+  }
+}
+
+}  // namespace hm

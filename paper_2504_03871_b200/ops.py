@@ -1,0 +1,220 @@
+"""Tensor-level operators of the expert-layer hot path (router, dispatch, expert FFN, combine).
+
+Each function wraps one C-ABI entry point of ``libhetermoe_kernels.so`` and runs it on the
+current torch CUDA stream. There is no CPU fallback: inputs must be CUDA tensors and the
+native library must be present (``_native.NativeLibraryError`` otherwise).
+
+Reference anchors: the reference folds all of these into opaque task durations
+(router/permute/combine -> ATTN_F, ``/root/reference/pkg/src/zpsim/taskgraph.py:220-246``;
+expert FFN -> EXP_F, ``costmodel.py:28-37``); their semantics come from the paper
+(``PAPER.md:110,112,356,358``) and are pinned by ``oracle/moe_oracle.py``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native
+
+BLOCK_F = 128  # gate/up interleave block of the fused W_ug layout
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ValueError("hetermoe ops need contiguous CUDA tensors (no CPU fallback)")
+
+
+@dataclass
+class Routing:
+    """Result of the router: everything dispatch / combine need."""
+
+    idx: torch.Tensor  # [T, k] int32 expert ids, descending logit
+    w: torch.Tensor  # [T, k] fp32 gate weights (softmax over the k)
+    logits: torch.Tensor  # [T, E] fp32
+    counts: torch.Tensor  # [E] int32 tokens per expert
+    offsets: torch.Tensor  # [E+1] int32 exclusive prefix sum of counts
+    chunk_base: torch.Tensor  # [nchunk, E] int32 per-chunk row bases
+
+
+def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int) -> Routing:
+    """K1: fixed-order fp32 logits, top-k (ties -> lower id), softmax over the k, histogram."""
+    _require_cuda(x, wg)
+    lib = _native.load()
+    T, d = x.shape
+    E = wg.shape[1]
+    dev = x.device
+    idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+    w = torch.empty((T, k), dtype=torch.float32, device=dev)
+    logits = torch.empty((T, E), dtype=torch.float32, device=dev)
+    counts = torch.empty((E,), dtype=torch.int32, device=dev)
+    offsets = torch.empty((E + 1,), dtype=torch.int32, device=dev)
+    nce = lib.hm_router_chunk_elems(T, E)
+    chunk_base = torch.empty((max(nce, 1),), dtype=torch.int32, device=dev)
+    rc = lib.hm_router_topk(
+        _ptr(x), _ptr(wg), T, d, E, k, _ptr(idx), _ptr(w), _ptr(logits), _ptr(counts),
+        _ptr(offsets), _ptr(chunk_base), _stream(),
+    )
+    _native.check(rc, "hm_router_topk")
+    return Routing(idx, w, logits, counts, offsets, chunk_base)
+
+
+def dispatch_permute(x: torch.Tensor, r: Routing, out: torch.Tensor | None = None):
+    """K2: x[T,d] -> (x_perm[T*k,d] grouped by expert, row_src[T*k], row_of[T,k])."""
+    _require_cuda(x)
+    T, d = x.shape
+    k = r.idx.shape[1]
+    E = r.counts.shape[0]
+    dev = x.device
+    x_perm = out if out is not None else torch.empty((T * k, d), dtype=x.dtype, device=dev)
+    row_src = torch.empty((T * k,), dtype=torch.int32, device=dev)
+    row_of = torch.empty((T, k), dtype=torch.int32, device=dev)
+    rc = _native.load().hm_dispatch_permute(
+        _ptr(x), _ptr(r.idx), _ptr(r.chunk_base), T, d, E, k, _ptr(x_perm), _ptr(row_src),
+        _ptr(row_of), _stream(),
+    )
+    _native.check(rc, "hm_dispatch_permute")
+    return x_perm, row_src, row_of
+
+
+def unpermute_sum(dx_perm: torch.Tensor, row_of: torch.Tensor) -> torch.Tensor:
+    _require_cuda(dx_perm, row_of)
+    T, k = row_of.shape
+    d = dx_perm.shape[1]
+    dx = torch.empty((T, d), dtype=dx_perm.dtype, device=dx_perm.device)
+    rc = _native.load().hm_unpermute_sum(_ptr(dx_perm), _ptr(row_of), T, d, k, _ptr(dx), _stream())
+    _native.check(rc, "hm_unpermute_sum")
+    return dx
+
+
+def combine(y_perm: torch.Tensor, row_of: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """K4: y[t] = sum_s w[t,s] * y_perm[row_of[t,s]]."""
+    _require_cuda(y_perm, row_of, w)
+    T, k = row_of.shape
+    d = y_perm.shape[1]
+    y = torch.empty((T, d), dtype=y_perm.dtype, device=y_perm.device)
+    rc = _native.load().hm_combine(_ptr(y_perm), _ptr(row_of), _ptr(w), T, d, k, _ptr(y), _stream())
+    _native.check(rc, "hm_combine")
+    return y
+
+
+def combine_bwd(dy: torch.Tensor, y_perm: torch.Tensor, row_of: torch.Tensor, w: torch.Tensor):
+    _require_cuda(dy, y_perm, row_of, w)
+    T, k = row_of.shape
+    d = dy.shape[1]
+    dy_perm = torch.empty_like(y_perm)
+    dw = torch.empty((T, k), dtype=torch.float32, device=dy.device)
+    rc = _native.load().hm_combine_bwd(
+        _ptr(dy), _ptr(y_perm), _ptr(row_of), _ptr(w), T, d, k, _ptr(dy_perm), _ptr(dw), _stream()
+    )
+    _native.check(rc, "hm_combine_bwd")
+    return dy_perm, dw
+
+
+def transpose_bf16(a: torch.Tensor) -> torch.Tensor:
+    _require_cuda(a)
+    R, C = a.shape
+    out = torch.empty((C, R), dtype=a.dtype, device=a.device)
+    rc = _native.load().hm_transpose_bf16(_ptr(a), R, C, _ptr(out), _stream())
+    _native.check(rc, "hm_transpose_bf16")
+    return out
+
+
+def router_bwd(dx_perm, row_of, r: Routing, dw, x, wg_t, want_dwg: bool = True):
+    """dx = unpermute_sum(dx_perm) + dlogit . Wg^T ; dWg = x^T . dlogit."""
+    _require_cuda(dx_perm, row_of, dw, x, wg_t)
+    lib = _native.load()
+    T, k = row_of.shape
+    d = x.shape[1]
+    E = wg_t.shape[0]
+    dev = x.device
+    dx = torch.empty((T, d), dtype=x.dtype, device=dev)
+    dlogit = torch.empty((T, k), dtype=torch.float32, device=dev)
+    dwg = part = None
+    if want_dwg:
+        dwg = torch.empty((d, E), dtype=x.dtype, device=dev)
+        part = torch.empty((lib.hm_router_bwd_part_elems(T, d, E),), dtype=torch.float32, device=dev)
+    rc = lib.hm_router_bwd(
+        _ptr(dx_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(dw), _ptr(x), _ptr(wg_t), T, d, E,
+        k, _ptr(dx), _ptr(dlogit), _ptr(dwg), _ptr(part), _stream(),
+    )
+    _native.check(rc, "hm_router_bwd")
+    return dx, dlogit, dwg
+
+
+def grouped_gemm(mode: int, a, b, seg_offsets, E: int, rows: int, M: int, N: int, K: int, out,
+                 ldo: int, out2=None, ldo2: int = 0, aux=None, ld_aux: int = 0,
+                 max_ctas: int = 0) -> None:
+    rc = _native.load().hm_grouped_gemm(
+        mode, _ptr(a), _ptr(b), _ptr(seg_offsets), E, rows, M, N, K, _ptr(out), ldo, _ptr(out2),
+        ldo2, _ptr(aux), ld_aux, max_ctas, _stream(),
+    )
+    _native.check(rc, "hm_grouped_gemm")
+
+
+def grouped_ffn_fwd(x_perm, seg_offsets, w_ug, w_d, max_ctas: int = 0):
+    """K3 forward: returns (y_perm, h, act). w_ug [E,2f,d] interleaved, w_d [E,d,f]."""
+    _require_cuda(x_perm, seg_offsets, w_ug, w_d)
+    rows, d = x_perm.shape
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    dev = x_perm.device
+    h = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=dev)
+    act = torch.empty((rows, f), dtype=x_perm.dtype, device=dev)
+    y_perm = torch.empty((rows, d), dtype=x_perm.dtype, device=dev)
+    rc = _native.load().hm_grouped_ffn_fwd(
+        _ptr(x_perm), rows, _ptr(seg_offsets), E, _ptr(w_ug), _ptr(w_d), d, f, _ptr(h), _ptr(act),
+        _ptr(y_perm), max_ctas, _stream(),
+    )
+    _native.check(rc, "hm_grouped_ffn_fwd")
+    return y_perm, h, act
+
+
+def grouped_ffn_bwd(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: int = 0):
+    """K3 backward: returns (dx_perm, dw_ug, dw_d)."""
+    _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d)
+    rows, d = x_perm.shape
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    dev = x_perm.device
+    dh = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=dev)
+    dx_perm = torch.empty((rows, d), dtype=x_perm.dtype, device=dev)
+    dw_ug = torch.empty_like(w_ug)
+    dw_d = torch.empty_like(w_d)
+    rc = _native.load().hm_grouped_ffn_bwd(
+        _ptr(dy_perm), _ptr(x_perm), _ptr(h), _ptr(act), rows, _ptr(seg_offsets), E, _ptr(w_ug),
+        _ptr(w_d), d, f, _ptr(dh), _ptr(dx_perm), _ptr(dw_ug), _ptr(dw_d), max_ctas, _stream(),
+    )
+    _native.check(rc, "hm_grouped_ffn_bwd")
+    return dx_perm, dw_ug, dw_d
+
+
+# ---------------------------------------------------------------------------------------------
+# weight layout helpers (host side, any device)
+
+
+def interleave_gate_up(w_gate: torch.Tensor, w_up: torch.Tensor, block: int = BLOCK_F) -> torch.Tensor:
+    """[E,f,d] gate and up weights -> fused [E,2f,d] with 128-row gate/up blocks alternating."""
+    E, f, d = w_gate.shape
+    assert f % block == 0
+    g = w_gate.reshape(E, f // block, block, d)
+    u = w_up.reshape(E, f // block, block, d)
+    return torch.stack([g, u], dim=2).reshape(E, 2 * f, d).contiguous()
+
+
+def split_gate_up(w_ug: torch.Tensor, block: int = BLOCK_F):
+    """Inverse of interleave_gate_up."""
+    E, two_f, d = w_ug.shape
+    f = two_f // 2
+    v = w_ug.reshape(E, f // block, 2, block, d)
+    return v[:, :, 0].reshape(E, f, d), v[:, :, 1].reshape(E, f, d)

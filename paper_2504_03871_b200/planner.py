@@ -1,0 +1,58 @@
+"""Planner glue on the hot path: tokens/iteration, Algorithm-1 inputs, build+order+simulate.
+
+Drop-in for ``zpsim.planner`` lines 45-87 (``/root/reference/pkg/src/zpsim/planner.py``).
+The strategy comparison / sweep machinery of the reference is out of scope.
+"""
+
+from __future__ import annotations
+
+from fractions import Fraction
+from typing import Optional
+
+from . import costmodel, scheduler, simulator, taskgraph
+from .core import ExpertAssignment, Spec, TaskDurations
+
+
+def tokens_per_iteration(spec: Spec) -> int:
+    """Tokens (not top-k copies) per training iteration: s * seqs * M * R."""
+    md = spec.model
+    return md.seq_len * md.sequences_per_microbatch * spec.cluster.attention_gpus * md.microbatches
+
+
+def offload_inputs(spec: Spec, durations: TaskDurations,
+                   bounds: Optional[costmodel.MemoryBounds] = None) -> scheduler.OffloadPlanInputs:
+    b = bounds if bounds is not None else costmodel.memory_bounds(spec)
+    return scheduler.OffloadPlanInputs(
+        experts_per_layer=spec.model.experts_per_layer,
+        layers=spec.model.layers,
+        attention_gpus=spec.cluster.attention_gpus,
+        expert_gpus=spec.cluster.expert_gpus,
+        attn_fwd=Fraction(durations.attn_fwd),
+        single_expert_on_attn=Fraction(durations.single_expert_fwd_on_attn_gpu),
+        expert_layer_on_expert=Fraction(durations.expert_layer_fwd_on_expert_gpu),
+        n_min=b.n_min,
+        n_max=b.n_max,
+        squeeze_mode=spec.run.squeeze,
+    )
+
+
+def simulate_zp(spec: Spec, durations: TaskDurations, assignment: Optional[ExpertAssignment] = None,
+                mode: Optional[str] = None, include_backward: bool = True):
+    """Build, order and simulate one ZP instance; returns (graph, timeline)."""
+    graph = taskgraph.build_zp_graph(spec, durations, assignment=assignment, mode=mode,
+                                     include_backward=include_backward)
+    timeline = simulator.simulate(graph, scheduler.default_orders(graph))
+    problems = simulator.validate_timeline(graph, timeline)
+    if problems:
+        raise RuntimeError(f"simulated timeline invalid: {problems}")
+    return graph, timeline
+
+
+def plan_assignment(spec: Spec, durations: TaskDurations) -> ExpertAssignment:
+    """Explicit plan > Asym-EA (if enabled) > no offload (the reference CLI's resolution,
+    cli.py:93-106)."""
+    if spec.run.offload is not None:
+        return ExpertAssignment(spec.run.offload)
+    if spec.run.asym_ea:
+        return scheduler.asym_ea_offload(offload_inputs(spec, durations)).assignment
+    return ExpertAssignment.zeros(spec.model.layers)

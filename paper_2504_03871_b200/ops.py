@@ -20,6 +20,53 @@ from . import _native
 
 BLOCK_F = 128  # gate/up interleave block of the fused W_ug layout
 
+# number of native kernel launches issued through this module (bench.py's gpu_launches)
+LAUNCHES = [0]
+
+
+def _count(n: int) -> None:
+    LAUNCHES[0] += n
+
+
+class KernelTimer:
+    """Records CUDA events around every native call on the launching stream (bench.py uses it
+    over the timed region to get per-kernel device durations)."""
+
+    def __init__(self):
+        self.events = {}  # name -> list of (start, end) events
+
+    def begin(self, name: str):
+        s = torch.cuda.Event(enable_timing=True)
+        s.record()
+        return name, s
+
+    def end(self, tok) -> None:
+        name, s = tok
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.setdefault(name, []).append((s, e))
+
+    def summary(self) -> dict:
+        """name -> (launch count, total ms); call after synchronising."""
+        return {n: (len(v), sum(a.elapsed_time(b) for a, b in v)) for n, v in self.events.items()}
+
+
+_TIMER: list = [None]
+
+
+def set_timer(timer: "KernelTimer | None") -> None:
+    _TIMER[0] = timer
+
+
+def _begin(name: str):
+    t = _TIMER[0]
+    return t.begin(name) if t is not None else None
+
+
+def _end(tok) -> None:
+    if tok is not None:
+        _TIMER[0].end(tok)
+
 
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
@@ -61,11 +108,14 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int) -> Routing:
     offsets = torch.empty((E + 1,), dtype=torch.int32, device=dev)
     nce = lib.hm_router_chunk_elems(T, E)
     chunk_base = torch.empty((max(nce, 1),), dtype=torch.int32, device=dev)
+    _tk = _begin("router_topk")
     rc = lib.hm_router_topk(
         _ptr(x), _ptr(wg), T, d, E, k, _ptr(idx), _ptr(w), _ptr(logits), _ptr(counts),
         _ptr(offsets), _ptr(chunk_base), _stream(),
     )
+    _end(_tk)
     _native.check(rc, "hm_router_topk")
+    _count(3)
     return Routing(idx, w, logits, counts, offsets, chunk_base)
 
 
@@ -79,11 +129,14 @@ def dispatch_permute(x: torch.Tensor, r: Routing, out: torch.Tensor | None = Non
     x_perm = out if out is not None else torch.empty((T * k, d), dtype=x.dtype, device=dev)
     row_src = torch.empty((T * k,), dtype=torch.int32, device=dev)
     row_of = torch.empty((T, k), dtype=torch.int32, device=dev)
+    _tk = _begin("dispatch_permute")
     rc = _native.load().hm_dispatch_permute(
         _ptr(x), _ptr(r.idx), _ptr(r.chunk_base), T, d, E, k, _ptr(x_perm), _ptr(row_src),
         _ptr(row_of), _stream(),
     )
+    _end(_tk)
     _native.check(rc, "hm_dispatch_permute")
+    _count(1)
     return x_perm, row_src, row_of
 
 
@@ -92,8 +145,11 @@ def unpermute_sum(dx_perm: torch.Tensor, row_of: torch.Tensor) -> torch.Tensor:
     T, k = row_of.shape
     d = dx_perm.shape[1]
     dx = torch.empty((T, d), dtype=dx_perm.dtype, device=dx_perm.device)
+    _tk = _begin("unpermute_sum")
     rc = _native.load().hm_unpermute_sum(_ptr(dx_perm), _ptr(row_of), T, d, k, _ptr(dx), _stream())
+    _end(_tk)
     _native.check(rc, "hm_unpermute_sum")
+    _count(1)
     return dx
 
 
@@ -103,8 +159,11 @@ def combine(y_perm: torch.Tensor, row_of: torch.Tensor, w: torch.Tensor) -> torc
     T, k = row_of.shape
     d = y_perm.shape[1]
     y = torch.empty((T, d), dtype=y_perm.dtype, device=y_perm.device)
+    _tk = _begin("combine")
     rc = _native.load().hm_combine(_ptr(y_perm), _ptr(row_of), _ptr(w), T, d, k, _ptr(y), _stream())
+    _end(_tk)
     _native.check(rc, "hm_combine")
+    _count(1)
     return y
 
 
@@ -114,10 +173,13 @@ def combine_bwd(dy: torch.Tensor, y_perm: torch.Tensor, row_of: torch.Tensor, w:
     d = dy.shape[1]
     dy_perm = torch.empty_like(y_perm)
     dw = torch.empty((T, k), dtype=torch.float32, device=dy.device)
+    _tk = _begin("combine_bwd")
     rc = _native.load().hm_combine_bwd(
         _ptr(dy), _ptr(y_perm), _ptr(row_of), _ptr(w), T, d, k, _ptr(dy_perm), _ptr(dw), _stream()
     )
+    _end(_tk)
     _native.check(rc, "hm_combine_bwd")
+    _count(1)
     return dy_perm, dw
 
 
@@ -125,8 +187,11 @@ def transpose_bf16(a: torch.Tensor) -> torch.Tensor:
     _require_cuda(a)
     R, C = a.shape
     out = torch.empty((C, R), dtype=a.dtype, device=a.device)
+    _tk = _begin("transpose_bf16")
     rc = _native.load().hm_transpose_bf16(_ptr(a), R, C, _ptr(out), _stream())
+    _end(_tk)
     _native.check(rc, "hm_transpose_bf16")
+    _count(1)
     return out
 
 
@@ -144,26 +209,35 @@ def router_bwd(dx_perm, row_of, r: Routing, dw, x, wg_t, want_dwg: bool = True):
     if want_dwg:
         dwg = torch.empty((d, E), dtype=x.dtype, device=dev)
         part = torch.empty((lib.hm_router_bwd_part_elems(T, d, E),), dtype=torch.float32, device=dev)
+    _tk = _begin("router_bwd")
     rc = lib.hm_router_bwd(
         _ptr(dx_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(dw), _ptr(x), _ptr(wg_t), T, d, E,
         k, _ptr(dx), _ptr(dlogit), _ptr(dwg), _ptr(part), _stream(),
     )
+    _end(_tk)
     _native.check(rc, "hm_router_bwd")
+    _count(3 if want_dwg else 1)
     return dx, dlogit, dwg
 
 
 def grouped_gemm(mode: int, a, b, seg_offsets, E: int, rows: int, M: int, N: int, K: int, out,
                  ldo: int, out2=None, ldo2: int = 0, aux=None, ld_aux: int = 0,
-                 max_ctas: int = 0) -> None:
+                 max_ctas: int = 0, name: str = "grouped_gemm") -> None:
+    """One launch of the tcgen05 grouped GEMM (modes: _native.GEMM_*)."""
+    _tk = _begin(name)
     rc = _native.load().hm_grouped_gemm(
         mode, _ptr(a), _ptr(b), _ptr(seg_offsets), E, rows, M, N, K, _ptr(out), ldo, _ptr(out2),
         ldo2, _ptr(aux), ld_aux, max_ctas, _stream(),
     )
+    _end(_tk)
     _native.check(rc, "hm_grouped_gemm")
+    _count(1)
 
 
 def grouped_ffn_fwd(x_perm, seg_offsets, w_ug, w_d, max_ctas: int = 0):
-    """K3 forward: returns (y_perm, h, act). w_ug [E,2f,d] interleaved, w_d [E,d,f]."""
+    """K3 forward (same math as hm_grouped_ffn_fwd, one launch per GEMM so each is timed):
+    h = x_perm . w_ug[e]^T (gate|up), act = silu(gate)*up, y_perm = act . w_d[e]^T.
+    Returns (y_perm, h, act). w_ug [E,2f,d] interleaved, w_d [E,d,f]."""
     _require_cuda(x_perm, seg_offsets, w_ug, w_d)
     rows, d = x_perm.shape
     E, two_f, _ = w_ug.shape
@@ -172,16 +246,16 @@ def grouped_ffn_fwd(x_perm, seg_offsets, w_ug, w_d, max_ctas: int = 0):
     h = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=dev)
     act = torch.empty((rows, f), dtype=x_perm.dtype, device=dev)
     y_perm = torch.empty((rows, d), dtype=x_perm.dtype, device=dev)
-    rc = _native.load().hm_grouped_ffn_fwd(
-        _ptr(x_perm), rows, _ptr(seg_offsets), E, _ptr(w_ug), _ptr(w_d), d, f, _ptr(h), _ptr(act),
-        _ptr(y_perm), max_ctas, _stream(),
-    )
-    _native.check(rc, "hm_grouped_ffn_fwd")
+    grouped_gemm(_native.GEMM_FWD_UPGATE, x_perm, w_ug, seg_offsets, E, rows, 0, 2 * f, d, act, f,
+                 out2=h, ldo2=2 * f, max_ctas=max_ctas, name="gemm_fwd_upgate")
+    grouped_gemm(_native.GEMM_FWD_DOWN, act, w_d, seg_offsets, E, rows, 0, d, f, y_perm, d,
+                 max_ctas=max_ctas, name="gemm_fwd_down")
     return y_perm, h, act
 
 
 def grouped_ffn_bwd(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: int = 0):
-    """K3 backward: returns (dx_perm, dw_ug, dw_d)."""
+    """K3 backward: dh = SwiGLU'(dy_perm . w_d[e]); dx_perm = dh . w_ug[e];
+    dw_ug[e] = dh_e^T . x_e; dw_d[e] = dy_e^T . act_e. Returns (dx_perm, dw_ug, dw_d)."""
     _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d)
     rows, d = x_perm.shape
     E, two_f, _ = w_ug.shape
@@ -191,11 +265,14 @@ def grouped_ffn_bwd(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: i
     dx_perm = torch.empty((rows, d), dtype=x_perm.dtype, device=dev)
     dw_ug = torch.empty_like(w_ug)
     dw_d = torch.empty_like(w_d)
-    rc = _native.load().hm_grouped_ffn_bwd(
-        _ptr(dy_perm), _ptr(x_perm), _ptr(h), _ptr(act), rows, _ptr(seg_offsets), E, _ptr(w_ug),
-        _ptr(w_d), d, f, _ptr(dh), _ptr(dx_perm), _ptr(dw_ug), _ptr(dw_d), max_ctas, _stream(),
-    )
-    _native.check(rc, "hm_grouped_ffn_bwd")
+    grouped_gemm(_native.GEMM_BWD_DACT, dy_perm, w_d, seg_offsets, E, rows, 0, f, d, dh, 2 * f,
+                 aux=h, ld_aux=2 * f, max_ctas=max_ctas, name="gemm_bwd_dact")
+    grouped_gemm(_native.GEMM_BWD_DX, dh, w_ug, seg_offsets, E, rows, 0, d, 2 * f, dx_perm, d,
+                 max_ctas=max_ctas, name="gemm_bwd_dx")
+    grouped_gemm(_native.GEMM_WGRAD, dh, x_perm, seg_offsets, E, rows, 2 * f, d, 0, dw_ug, d,
+                 max_ctas=max_ctas, name="gemm_wgrad_ug")
+    grouped_gemm(_native.GEMM_WGRAD, dy_perm, act, seg_offsets, E, rows, d, f, 0, dw_d, f,
+                 max_ctas=max_ctas, name="gemm_wgrad_down")
     return dx_perm, dw_ug, dw_d
 
 

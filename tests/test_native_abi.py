@@ -1,0 +1,31 @@
+"""The C-ABI library loads on a CPU-only host and exports every entry point include/hetermoe.h
+declares (no compute call is made here)."""
+
+import os
+import re
+
+from paper_2504_03871_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "hetermoe.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(hm_\w+)\s*\(", src, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert _header_functions() == sorted(_native.SIGNATURES)
+
+
+def test_library_exports_all_symbols():
+    assert os.path.exists(_native.LIB_PATH), "build first: python -c 'import __graft_entry__ as g; g.build()'"
+    assert sorted(_native.exported_symbols()) == _header_functions()
+
+
+def test_pure_host_entry_points():
+    lib = _native.load()
+    assert lib.hm_abi_version() == 1
+    assert lib.hm_router_chunk_elems(4096, 8) == 16 * 8
+    assert lib.hm_router_chunk_elems(1, 64) == 64
+    assert lib.hm_router_bwd_part_elems(16384, 4096, 8) == 64 * 8 * 4096

@@ -1,0 +1,101 @@
+"""CPU checks of the tensor-path oracle (no GPU): the restated semantics and the aggregate
+token accounting the reference pins (costmodel.py:59-79 B; taskgraph.py:560-575 conservation)."""
+
+from fractions import Fraction
+
+import numpy as np
+import torch
+
+from oracle import moe_oracle as orc
+from paper_2504_03871_b200 import ExpertAssignment, token_flow, workload_shape
+from paper_2504_03871_b200.configs import C1, LayerConfig, make_inputs, with_tokens, zipf_bias
+from paper_2504_03871_b200.ops import interleave_gate_up, split_gate_up
+
+
+def test_fixed_order_logits_close_to_exact_matmul():
+    inp = make_inputs(with_tokens(C1, 300), seed=3)
+    lg = orc.router_logits(inp.x.float().numpy(), inp.wg.float().numpy())
+    exact = (inp.x.double() @ inp.wg.double()).numpy()
+    assert lg.dtype == np.float32
+    assert np.abs(lg - exact).max() < 1e-4
+
+
+def test_fixed_order_is_the_documented_lane_butterfly():
+    # brute-force restatement for one token: lane partials in (j, q) order, then xor butterfly
+    rng = np.random.default_rng(0)
+    d, E = 512, 4
+    x = torch.tensor(rng.standard_normal((1, d)), dtype=torch.float32).bfloat16().float().numpy()
+    w = torch.tensor(rng.standard_normal((d, E)), dtype=torch.float32).bfloat16().float().numpy()
+    lanes = np.zeros((32, E), dtype=np.float32)
+    for lane in range(32):
+        for j in range(d // 256):
+            for q in range(8):
+                i = 256 * j + 8 * lane + q
+                lanes[lane] = (lanes[lane] + np.float32(x[0, i]) * w[i]).astype(np.float32)
+    for off in (16, 8, 4, 2, 1):
+        lanes = (lanes + lanes[np.arange(32) ^ off]).astype(np.float32)
+    assert np.array_equal(lanes[0], orc.router_logits(x, w)[0])
+
+
+def test_topk_ties_go_to_lower_expert_and_softmax_normalises():
+    logits = np.array([[1.0, 3.0, 3.0, 0.5], [2.0, 2.0, 2.0, 2.0]], dtype=np.float32)
+    idx, w = orc.topk_softmax(logits, 2)
+    assert idx.tolist() == [[1, 2], [0, 1]]
+    assert np.allclose(w.sum(1), 1.0) and np.allclose(w, 0.5)
+
+
+def test_permutation_is_stable_by_expert_then_token():
+    idx = np.array([[2, 0], [0, 1], [2, 1], [0, 2]], dtype=np.int32)
+    row_src, row_of = orc.permutation(idx, 3)
+    assert row_src.tolist() == [0, 1, 3, 1, 2, 0, 2, 3]
+    for t in range(4):
+        for s in range(2):
+            assert row_src[row_of[t, s]] == t
+
+
+def test_counts_conserve_routed_tokens_like_the_reference():
+    # zpsim prices B = s*seqs*M*k/N tokens per expert GPU (costmodel.py:59-73); with M = N = 1
+    # the oracle's routed copies must total exactly T*k = B, and no copy is dropped (dropless)
+    cfg = LayerConfig("acct", E=8, k=2, d=256, f=128, T=1024)
+    inp = make_inputs(cfg, seed=4)
+    r = orc.route(inp.x.float().numpy(), inp.wg.float().numpy(), cfg.k)
+    from paper_2504_03871_b200 import GpuClass, HardwareProfile, ModelSpec, RunOptions, Spec, ZpGroupSpec
+
+    g = GpuClass("b200", 10**12, expert_coeff=Fraction(1))
+    spec = Spec(ZpGroupSpec(1, 1, g, g, 10**12, 2 * cfg.d), ModelSpec(1, cfg.E, cfg.k, cfg.d, cfg.T, 1, 1, 0, 0),
+                HardwareProfile(g, g), RunOptions())
+    assert int(r.counts.sum()) == workload_shape(spec).tokens_per_expert_gpu == cfg.T * cfg.k
+    flow = token_flow(spec, ExpertAssignment((0,)), 1)
+    assert flow["entering_dispatch"] == int(r.offsets[-1]) == flow["leaving_combine"]
+
+
+def test_zipf_bias_skews_loads():
+    cfg = LayerConfig("skew", E=8, k=2, d=256, f=128, T=2048)
+    flat = orc.route(*(t.float().numpy() for t in (make_inputs(cfg, 5).x, make_inputs(cfg, 5).wg)), cfg.k)
+    inp = make_inputs(cfg, 5, expert_bias=zipf_bias(cfg.E, 1.5))
+    sk = orc.route(inp.x.float().numpy(), inp.wg.float().numpy(), cfg.k)
+    assert sk.counts.max() / sk.counts.mean() > flat.counts.max() / flat.counts.mean()
+
+
+def test_gate_up_interleave_roundtrip():
+    g = torch.randn(3, 256, 64)
+    u = torch.randn(3, 256, 64)
+    ug = interleave_gate_up(g, u)
+    assert torch.equal(ug[:, 0:128], g[:, 0:128]) and torch.equal(ug[:, 128:256], u[:, 0:128])
+    g2, u2 = split_gate_up(ug)
+    assert torch.equal(g2, g) and torch.equal(u2, u)
+
+
+def test_oracle_layer_gradients_match_finite_differences():
+    cfg = LayerConfig("fd", E=4, k=2, d=256, f=128, T=8)
+    inp = make_inputs(cfg, seed=9)
+    w_ug = interleave_gate_up(inp.w_gate, inp.w_up)
+    out = orc.moe_layer(inp.x, inp.wg, w_ug, inp.w_down, cfg.k, dy=inp.dy)
+    # directional derivative along a random direction in x (routing fixed)
+    v = torch.randn(cfg.T, cfg.d) * 1e-2
+    r = out["routing"]
+    yp = orc.moe_layer(inp.x.float() + v, inp.wg, w_ug, inp.w_down, cfg.k, routing=r)["y"]
+    ym = orc.moe_layer(inp.x.float() - v, inp.wg, w_ug, inp.w_down, cfg.k, routing=r)["y"]
+    fd = ((yp - ym) * inp.dy.float()).sum() / 2
+    an = (out["dx"] * v).sum()
+    assert abs(fd - an) / abs(an) < 1e-2

@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/hetermoe.h"
@@ -85,21 +86,46 @@ int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
   return 0;
 }
 
-template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
                 int max_ctas, cudaStream_t stream) {
-  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI>;
+  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI, CTAS>;
+  constexpr int smem = hm::TileCfg<CTAS>::kSmemBytes;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         hm::kGemmSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attr: %s", cudaGetErrorString(e));
     attr_set = true;
   }
   int grid = num_sms();
   if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  kern<<<grid, hm::kGemmThreads, hm::kGemmSmemBytes, stream>>>(ma, mb, p);
+  grid = (grid / CTAS) * CTAS;
+  if (grid < CTAS) grid = CTAS;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(hm::kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CTAS;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "grouped_gemm launch: %s", cudaGetErrorString(e));
   return check_launch("grouped_gemm");
+}
+
+// CTA-pair (cta_group::2) tiles for the GROUP_M GEMMs unless HM_GEMM_CTAS=1
+int gemm_ctas() {
+  static int v = 0;
+  if (v == 0) {
+    const char* s = getenv("HM_GEMM_CTAS");
+    v = (s && atoi(s) == 1) ? 1 : 2;
+  }
+  return v;
 }
 
 }  // namespace
@@ -329,6 +355,7 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
 
   CUtensorMap ma, mb;
   const int rows_m = rows > 0 ? rows : 1;
+  const int ctas = wgrad ? 1 : gemm_ctas();
   if (!wgrad) {
     {
       uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows_m};
@@ -340,7 +367,7 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
     if (!b_mn) {
       uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)E};
       uint64_t str[2] = {(uint64_t)K * 2, (uint64_t)N * K * 2};
-      uint32_t box[3] = {64, 256, 1};
+      uint32_t box[3] = {64, (uint32_t)(256 / ctas), 1};
       if (int rc = make_map(&mb, b, 3, dims, str, box)) return rc;
     } else {
       uint64_t dims[3] = {(uint64_t)N, (uint64_t)K, (uint64_t)E};
@@ -366,16 +393,20 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
   switch (mode) {
     case HM_GEMM_FWD_UPGATE:
       if (N % 256 != 0 || !out2) return fail(HM_E_SHAPE, "upgate: N=2f must be a multiple of 256 and h given");
-      return launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 2>(ma, mb, p, max_ctas, st)
+                       : launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 1>(ma, mb, p, max_ctas, st);
     case HM_GEMM_FWD_DOWN:
-      return launch_gemm<false, false, false, hm::EPI_STORE>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
+                       : launch_gemm<false, false, false, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
     case HM_GEMM_BWD_DACT:
       if (N % 128 != 0 || !aux) return fail(HM_E_SHAPE, "dact: N=f must be a multiple of 128 and h given");
-      return launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 2>(ma, mb, p, max_ctas, st)
+                       : launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 1>(ma, mb, p, max_ctas, st);
     case HM_GEMM_BWD_DX:
-      return launch_gemm<false, false, true, hm::EPI_STORE>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
+                       : launch_gemm<false, false, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
     case HM_GEMM_WGRAD:
-      return launch_gemm<true, true, true, hm::EPI_STORE>(ma, mb, p, max_ctas, st);
+      return launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
     default:
       return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
   }

@@ -27,17 +27,29 @@ namespace hm {
 
 enum EpilogueKind : int { EPI_STORE = 0, EPI_SWIGLU_FWD = 1, EPI_SWIGLU_BWD = 2 };
 
-constexpr int kBM = 128;
-constexpr int kBN = 256;
-constexpr int kBK = 64;
-constexpr int kStages = 4;
+constexpr int kBM = 128;  // accumulator rows per CTA (TMEM lanes)
+constexpr int kBN = 256;  // accumulator columns (UMMA N)
+constexpr int kBK = 64;   // K per pipeline stage (one 128-byte swizzle atom of bf16)
 constexpr int kATileBytes = kBM * kBK * 2;  // 16 KB
-constexpr int kBTileBytes = kBN * kBK * 2;  // 32 KB
-constexpr int kStageBytes = kATileBytes + kBTileBytes;
+constexpr int kMaxStages = 8;
 constexpr int kMaxExperts = 256;
 constexpr int kGemmThreads = 192;
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
-constexpr int kGemmSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 4096 /*bookkeeping*/;
+
+// CTAS = 1: one CTA computes a 128 x 256 tile (UMMA M=128, cta_group::1).
+// CTAS = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (UMMA M=256):
+//           each CTA stages its own 128 rows of A and half (128 columns) of B, the leader CTA
+//           issues the MMAs, each CTA's TMEM receives its 128 accumulator rows.
+template <int CTAS>
+struct TileCfg {
+  static constexpr int kTileM = kBM * CTAS;           // output rows per (cluster) tile
+  static constexpr int kBRows = kBN / CTAS;           // B rows (N) staged per CTA
+  static constexpr int kBTileBytes = kBRows * kBK * 2;
+  static constexpr int kStageBytes = kATileBytes + kBTileBytes;
+  static constexpr int kStages = CTAS == 1 ? 4 : 6;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 4096 /*bookkeeping*/;
+};
+constexpr int kGemmSmemBytes = TileCfg<1>::kSmemBytes;
 
 struct GroupedGemmParams {
   const int* seg_offsets;  // [E+1] row offsets of each expert's segment in the activation buffer
@@ -55,8 +67,8 @@ struct GroupedGemmParams {
 };
 
 struct GemmShared {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
   uint64_t tmem_full[2];
   uint64_t tmem_empty[2];
   uint32_t tmem_base;
@@ -68,7 +80,7 @@ struct TileCoord {
   int e, mt, nt;
 };
 
-template <bool GROUP_K>
+template <bool GROUP_K, int TILE_M>
 HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_fixed, int ntiles,
                              int n_fastest) {
   // binary search: largest e with tile_prefix[e] <= tile
@@ -80,7 +92,7 @@ HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_f
   const int local = tile - sh.tile_prefix[lo];
   int mtiles;
   if (GROUP_K) mtiles = mtiles_fixed;
-  else mtiles = (sh.seg[lo + 1] - sh.seg[lo] + kBM - 1) / kBM;
+  else mtiles = (sh.seg[lo + 1] - sh.seg[lo] + TILE_M - 1) / TILE_M;
   TileCoord c;
   c.e = lo;
   if (n_fastest) { c.mt = local / ntiles; c.nt = local % ntiles; }
@@ -110,10 +122,15 @@ HM_DEV void store_row32(__nv_bfloat16* dst, const float* v, int valid_cols) {
   }
 }
 
-template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GroupedGemmParams p) {
+  using Cfg = TileCfg<CTAS>;
+  static_assert(!(GROUP_K && CTAS == 2), "wgrad runs on single-CTA tiles");
+  constexpr int kStages = Cfg::kStages;
+  constexpr int kStageBytes = Cfg::kStageBytes;
+  constexpr int kTileM = Cfg::kTileM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   GemmShared& sh = *reinterpret_cast<GemmShared*>(tiles + kStages * kStageBytes);
@@ -121,10 +138,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int E = p.E;
+  const uint32_t rank = (CTAS == 2) ? cluster_ctarank() : 0u;
+  const bool leader = (rank == 0);
+  const int tile0 = (CTAS == 2) ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int tile_step = (CTAS == 2) ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
 
   // ---- per-CTA bookkeeping: expert segment table and tile prefix sums --------------------
   const int ntiles = (p.N + kBN - 1) / kBN;
-  const int mtiles_fixed = GROUP_K ? (p.M + kBM - 1) / kBM : 0;
+  const int mtiles_fixed = GROUP_K ? (p.M + kTileM - 1) / kTileM : 0;
   for (int i = threadIdx.x; i <= E; i += blockDim.x) sh.seg[i] = p.seg_offsets[i];
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -132,7 +153,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int e = 0; e < E; ++e) {
       sh.tile_prefix[e] = acc;
       const int me = sh.seg[e + 1] - sh.seg[e];
-      acc += (GROUP_K ? mtiles_fixed : (me + kBM - 1) / kBM) * ntiles;
+      acc += (GROUP_K ? mtiles_fixed : (me + kTileM - 1) / kTileM) * ntiles;
     }
     sh.tile_prefix[E] = acc;
     for (int s = 0; s < kStages; ++s) {
@@ -141,7 +162,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&sh.tmem_full[a], 1);
-      mbar_init(&sh.tmem_empty[a], 4);
+      mbar_init(&sh.tmem_empty[a], 4 * CTAS);
     }
     fence_barrier_init();
   }
@@ -151,23 +172,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tma_prefetch_desc(&map_b);
     }
   } else if (warp == 1) {
-    tmem_alloc(&sh.tmem_base, kTmemCols);
+    if (CTAS == 2) tmem_alloc_pair(&sh.tmem_base, kTmemCols);
+    else tmem_alloc(&sh.tmem_base, kTmemCols);
   }
   tc_fence_before();
-  __syncthreads();
+  if (CTAS == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
 
   const int total_tiles = sh.tile_prefix[E];
   const uint32_t tmem_base = sh.tmem_base;
 
   if (warp == 0) {
-    // ======================= TMA producer =======================
+    // ======================= TMA producer (both CTAs of a pair) =======================
     if (lane == 0) {
-      const uint64_t pol_act = policy_evict_normal();
-      const uint64_t pol_w = policy_evict_normal();
+      const uint64_t pol = policy_evict_normal();
       uint32_t it = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const TileCoord tc = decode_tile<GROUP_K>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+      for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+        const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
         const int seg0 = sh.seg[tc.e];
         const int me = sh.seg[tc.e + 1] - seg0;
         const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
@@ -177,96 +198,120 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&sh.empty[s], ph ^ 1);
           uint8_t* sa = tiles + s * kStageBytes;
           uint8_t* sb = sa + kATileBytes;
-          mbar_arrive_expect_tx(&sh.full[s], kStageBytes);
-          if (!GROUP_K) {
-            // A: activation rows [seg0 + mt*128, +128), K-major box {64, 128}
-            tma_load_2d(sa, &map_a, &sh.full[s], kb * kBK, seg0 + tc.mt * kBM, pol_act);
-            if (!B_MN) {
-              // B: W[e] stored [N][K]; box {64, 256}
-              tma_load_3d(sb, &map_b, &sh.full[s], kb * kBK, tc.nt * kBN, tc.e, pol_w);
+          if (CTAS == 1) {
+            mbar_arrive_expect_tx(&sh.full[s], kStageBytes);
+            if (!GROUP_K) {
+              // A: activation rows [seg0 + mt*128, +128), K-major box {64, 128}
+              tma_load_2d(sa, &map_a, &sh.full[s], kb * kBK, seg0 + tc.mt * kTileM, pol);
+              if (!B_MN) {
+                // B: W[e] stored [N][K]; box {64, 256}
+                tma_load_3d(sb, &map_b, &sh.full[s], kb * kBK, tc.nt * kBN, tc.e, pol);
+              } else {
+                // B: W[e] stored [K][N]; four 64-wide N panels, box {64 (N), 64 (K)}
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  tma_load_3d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, kb * kBK,
+                              tc.e, pol);
+              }
             } else {
-              // B: W[e] stored [K][N]; four 64-wide N panels, box {64 (N), 64 (K)}
+              // wgrad: both operands are [rows = K][cols] activations (MN-major), box {64, 64}
+              const int k0 = seg0 + kb * kBK;
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+                tma_load_2d(sa + q * 8192, &map_a, &sh.full[s], tc.mt * kTileM + q * 64, k0, pol);
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                tma_load_3d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, kb * kBK,
-                            tc.e, pol_w);
+                tma_load_2d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, k0, pol);
             }
           } else {
-            // wgrad: both operands are [rows = K][cols] activations (MN-major), box {64, 64}
-            const int k0 = seg0 + kb * kBK;
+            // CTA pair: every load completes on the leader's full barrier, which the leader
+            // arms with both CTAs' bytes.
+            const uint32_t lbar = mapa_shared(&sh.full[s], 0);
+            if (leader) mbar_arrive_expect_tx(&sh.full[s], 2 * kStageBytes);
+            tma_load_2d_pair(sa, &map_a, lbar, kb * kBK, seg0 + tc.mt * kTileM + rank * kBM, pol);
+            const int n0 = tc.nt * kBN + rank * Cfg::kBRows;
+            if (!B_MN) {
+              tma_load_3d_pair(sb, &map_b, lbar, kb * kBK, n0, tc.e, pol);
+            } else {
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
-              tma_load_2d(sa + q * 8192, &map_a, &sh.full[s], tc.mt * kBM + q * 64, k0, pol_w);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              tma_load_2d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, k0, pol_w);
+              for (int q = 0; q < Cfg::kBRows / 64; ++q)
+                tma_load_3d_pair(sb + q * 8192, &map_b, lbar, n0 + q * 64, kb * kBK, tc.e, pol);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ======================= MMA issuer =======================
-    constexpr uint32_t idesc = make_idesc_bf16(kBM, kBN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
+    // ======================= MMA issuer (leader CTA) =======================
+    constexpr uint32_t idesc = make_idesc_bf16(kTileM, kBN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
     uint32_t it = 0, tcount = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const TileCoord tc = decode_tile<GROUP_K>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
-      const int seg0 = sh.seg[tc.e];
-      const int me = sh.seg[tc.e + 1] - seg0;
-      const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
-      if (nk == 0) continue;  // epilogue writes zeros for this tile without touching TMEM
-      const int acc = tcount & 1;
-      const uint32_t aph = (tcount >> 1) & 1;
-      mbar_wait(&sh.tmem_empty[acc], aph ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * kBN;
-      for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
-        mbar_wait(&sh.full[s], ph);
+    if (leader) {
+      for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+        const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+        const int seg0 = sh.seg[tc.e];
+        const int me = sh.seg[tc.e + 1] - seg0;
+        const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
+        if (nk == 0) continue;  // epilogue writes zeros for this tile without touching TMEM
+        const int acc = tcount & 1;
+        const uint32_t aph = (tcount >> 1) & 1;
+        mbar_wait(&sh.tmem_empty[acc], aph ^ 1);
         tc_fence_after();
-        uint8_t* sa = tiles + s * kStageBytes;
-        uint8_t* sb = sa + kATileBytes;
-        if (GROUP_K && kb == nk - 1) {
-          const int rem = me - kb * kBK;  // valid K rows in this block (1..64)
-          if (rem < kBK) {
-            // zero K rows [rem, 64) of both 64-wide panels of the MN-major A tile
-            const int nrows = kBK - rem;
-            for (int i = lane; i < nrows * 2 * 8; i += 32) {
-              const int chunk = i & 7;
-              const int rr = rem + ((i >> 3) % nrows);
-              const int q = (i >> 3) / nrows;
-              uint4* dst = reinterpret_cast<uint4*>(sa + q * 8192 + (rr >> 3) * 1024 + (rr & 7) * 128) + chunk;
-              *dst = make_uint4(0u, 0u, 0u, 0u);
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          const uint32_t ph = (it / kStages) & 1;
+          mbar_wait(&sh.full[s], ph);
+          tc_fence_after();
+          uint8_t* sa = tiles + s * kStageBytes;
+          uint8_t* sb = sa + kATileBytes;
+          if (GROUP_K && kb == nk - 1) {
+            const int rem = me - kb * kBK;  // valid K rows in this block (1..64)
+            if (rem < kBK) {
+              // zero K rows [rem, 64) of both 64-wide panels of the MN-major A tile
+              const int nrows = kBK - rem;
+              for (int i = lane; i < nrows * 2 * 8; i += 32) {
+                const int chunk = i & 7;
+                const int rr = rem + ((i >> 3) % nrows);
+                const int q = (i >> 3) / nrows;
+                uint4* dst = reinterpret_cast<uint4*>(sa + q * 8192 + (rr >> 3) * 1024 + (rr & 7) * 128) + chunk;
+                *dst = make_uint4(0u, 0u, 0u, 0u);
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
             }
-            fence_proxy_async_smem();
-            __syncwarp();
           }
-        }
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(sa);
-          const uint32_t b_addr = smem_u32(sb);
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sa);
+            const uint32_t b_addr = smem_u32(sb);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t adesc = A_MN ? make_sw128_desc(a_addr + kk * 2048, 8192, 1024)
-                                        : make_sw128_desc(a_addr + kk * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? make_sw128_desc(b_addr + kk * 2048, 8192, 1024)
-                                        : make_sw128_desc(b_addr + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t adesc = A_MN ? make_sw128_desc(a_addr + kk * 2048, 8192, 1024)
+                                          : make_sw128_desc(a_addr + kk * 32, 16, 1024);
+              const uint64_t bdesc = B_MN ? make_sw128_desc(b_addr + kk * 2048, 8192, 1024)
+                                          : make_sw128_desc(b_addr + kk * 32, 16, 1024);
+              if (CTAS == 2) umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+              else umma_bf16(d_tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+            }
+            if (CTAS == 2) {
+              umma_commit_pair(&sh.empty[s], 0x3);
+              if (kb == nk - 1) umma_commit_pair(&sh.tmem_full[acc], 0x3);
+            } else {
+              umma_commit(&sh.empty[s]);
+              if (kb == nk - 1) umma_commit(&sh.tmem_full[acc]);
+            }
           }
-          umma_commit(&sh.empty[s]);
-          if (kb == nk - 1) umma_commit(&sh.tmem_full[acc]);
+          __syncwarp();
         }
-        __syncwarp();
+        ++tcount;
       }
-      ++tcount;
     }
   } else {
     // ======================= epilogue (warps 2..5) =======================
     const int quad = warp & 3;
-    const int row_in_tile = quad * 32 + lane;
+    const int row_in_tile = static_cast<int>(rank) * kBM + quad * 32 + lane;
     uint32_t tcount = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const TileCoord tc = decode_tile<GROUP_K>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+    for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+      const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
       const int seg0 = sh.seg[tc.e];
       const int me = sh.seg[tc.e + 1] - seg0;
       const int n0 = tc.nt * kBN;
@@ -274,11 +319,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       long grow;       // global output row
       bool row_ok;
       if (!GROUP_K) {
-        row_ok = tc.mt * kBM + row_in_tile < me;
-        grow = static_cast<long>(seg0) + tc.mt * kBM + row_in_tile;
+        row_ok = tc.mt * kTileM + row_in_tile < me;
+        grow = static_cast<long>(seg0) + tc.mt * kTileM + row_in_tile;
       } else {
-        row_ok = tc.mt * kBM + row_in_tile < p.M;
-        grow = static_cast<long>(tc.e) * p.M + tc.mt * kBM + row_in_tile;
+        row_ok = tc.mt * kTileM + row_in_tile < p.M;
+        grow = static_cast<long>(tc.e) * p.M + tc.mt * kTileM + row_in_tile;
       }
       if (GROUP_K && me == 0) {
         // empty expert: its weight gradient is exactly zero
@@ -366,16 +411,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sh.tmem_empty[acc]);
+      if (lane == 0) {
+        if (CTAS == 2) mbar_arrive_cluster(mapa_shared(&sh.tmem_empty[acc], 0));
+        else mbar_arrive(&sh.tmem_empty[acc]);
+      }
       ++tcount;
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CTAS == 2) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    if (CTAS == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+    else tmem_dealloc(tmem_base, kTmemCols);
   }
 }
 

@@ -12,8 +12,9 @@
 //
 // Tiles are 128 x 256 x 64 (UMMA M=128, N=256, K=16 x 4), 4-stage TMA ring (48 KB / stage),
 // two 256-column fp32 accumulators in TMEM so the epilogue of tile i overlaps the MMAs of i+1.
-// Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (lane 0 issues), warps 2..5 = epilogue
-// (warp w reads TMEM lanes 32*(w%4) .. +31, i.e. one accumulator row per thread).
+// Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (lane 0 issues), warps 2..9 = epilogue
+// (warp w reads TMEM lanes 32*(w%4) .. +31, one accumulator row per thread, and columns
+// [128*h, 128*h+128) with h = (w-2)/4).
 //
 // Tiles that straddle an expert boundary (GROUP_M) load a few rows of the next expert; those
 // rows are computed with the wrong weights and are never stored (row mask in the epilogue).
@@ -33,7 +34,8 @@ constexpr int kBK = 64;   // K per pipeline stage (one 128-byte swizzle atom of 
 constexpr int kATileBytes = kBM * kBK * 2;  // 16 KB
 constexpr int kMaxStages = 8;
 constexpr int kMaxExperts = 256;
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;     // two warps per TMEM lane quadrant, each owns 128 columns
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 
 // CTAS = 1: one CTA computes a 128 x 256 tile (UMMA M=128, cta_group::1).
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&sh.tmem_full[a], 1);
-      mbar_init(&sh.tmem_empty[a], 4 * CTAS);
+      mbar_init(&sh.tmem_empty[a], kEpiWarps * CTAS);
     }
     fence_barrier_init();
   }
@@ -306,8 +308,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ======================= epilogue (warps 2..5) =======================
+    // ======================= epilogue (warps 2..9) =======================
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;  // column half of the 256-wide accumulator
     const int row_in_tile = static_cast<int>(rank) * kBM + quad * 32 + lane;
     uint32_t tcount = 0;
     for (int tile = tile0; tile < total_tiles; tile += tile_step) {
@@ -331,81 +334,120 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           float z[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) z[j] = 0.f;
-          for (int c = 0; c < ncols_valid; c += 32)
+          for (int c = half * 128; c < min(ncols_valid, half * 128 + 128); c += 32)
             store_row32(p.out + grow * p.ldo + n0 + c, z, min(32, ncols_valid - c));
         }
         continue;
       }
       const int acc = tcount & 1;
       const uint32_t aph = (tcount >> 1) & 1;
-      mbar_wait(&sh.tmem_full[acc], aph);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kBN;
 
-      if (EPI == EPI_STORE) {
-        for (int c = 0; c < kBN; c += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + c, r);
-          tmem_ld_wait();
-          if (row_ok && c < ncols_valid)
-            store_row32(p.out + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
-                        min(32, ncols_valid - c));
-        }
-      } else if (EPI == EPI_SWIGLU_FWD) {
-        // columns [0,128) = gate, [128,256) = up for f-columns [nt*128, +128)
-        const int f0 = tc.nt * (kBN / 2);
-        for (int c = 0; c < kBN / 2; c += 32) {
-          uint32_t rg[32], ru[32];
-          tmem_ld_32x32b_x32(t_row + c, rg);
-          tmem_ld_32x32b_x32(t_row + kBN / 2 + c, ru);
-          tmem_ld_wait();
-          if (row_ok) {
-            float* g = reinterpret_cast<float*>(rg);
-            float* u = reinterpret_cast<float*>(ru);
-            // saved pre-activations are the bf16-rounded accumulators; the activation is
-            // computed from the same rounded values so forward and backward agree exactly.
-            float gq[32], uq[32], a[32];
+      if (EPI == EPI_SWIGLU_BWD) {
+        // dA for f-columns [n0 + 128*half, +128); the saved gate/up pre-activations are
+        // prefetched one 32-column chunk ahead (the first before the accumulator is ready).
+        const int cbeg = half * 128;
+        const bool live = row_ok && cbeg < ncols_valid;
+        auto hptr = [&](int c) {
+          const int fcol = n0 + c;  // multiple of 32; a 32-chunk never crosses a 128 block
+          return p.aux + grow * p.ld_aux + (fcol >> 7) * 256 + (fcol & 127);
+        };
+        uint4 gcur[4], ucur[4], gnxt[4], unxt[4];
+        if (live) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              gq[j] = __bfloat162float(__float2bfloat16_rn(g[j]));
-              uq[j] = __bfloat162float(__float2bfloat16_rn(u[j]));
-              a[j] = silu_f(gq[j]) * uq[j];
-            }
-            store_row32(p.out2 + grow * p.ldo2 + n0 + c, gq, 32);
-            store_row32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, uq, 32);
-            store_row32(p.out + grow * p.ldo + f0 + c, a, 32);
+          for (int q = 0; q < 4; ++q) {
+            gcur[q] = *reinterpret_cast<const uint4*>(hptr(cbeg) + q * 8);
+            ucur[q] = *reinterpret_cast<const uint4*>(hptr(cbeg) + 128 + q * 8);
           }
         }
-      } else {  // EPI_SWIGLU_BWD: D = dA for f-columns [n0, n0+256)
-        for (int c = 0; c < kBN; c += 32) {
+        mbar_wait(&sh.tmem_full[acc], aph);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kBN;
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) {
+          const int c = cbeg + 32 * i;
+          const bool ok = row_ok && c < ncols_valid;
+          if (i < 3 && row_ok && c + 32 < ncols_valid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              gnxt[q] = *reinterpret_cast<const uint4*>(hptr(c + 32) + q * 8);
+              unxt[q] = *reinterpret_cast<const uint4*>(hptr(c + 32) + 128 + q * 8);
+            }
+          }
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_row + c, r);
           tmem_ld_wait();
-          const int fcol = n0 + c;  // multiple of 32; a 32-chunk never crosses a 128 block
-          if (row_ok && c < ncols_valid) {
-            const int hcol = (fcol >> 7) * 256 + (fcol & 127);
-            const __nv_bfloat16* hg = p.aux + grow * p.ld_aux + hcol;
-            const __nv_bfloat16* hu = hg + 128;
+          if (ok) {
             const float* da = reinterpret_cast<float*>(r);
-            float dg[32], du[32];
+            const int fcol = n0 + c;
+            __nv_bfloat16* dgp = p.out + grow * p.ldo + (fcol >> 7) * 256 + (fcol & 127);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              uint4 gv = *reinterpret_cast<const uint4*>(hg + q * 8);
-              uint4 uv = *reinterpret_cast<const uint4*>(hu + q * 8);
-              const uint16_t* gs = reinterpret_cast<const uint16_t*>(&gv);
-              const uint16_t* us = reinterpret_cast<const uint16_t*>(&uv);
+              const uint16_t* gs = reinterpret_cast<const uint16_t*>(&gcur[q]);
+              const uint16_t* us = reinterpret_cast<const uint16_t*>(&ucur[q]);
+              float dg[8], du[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const float g = bf16_to_f32(gs[j]);
                 const float u = bf16_to_f32(us[j]);
                 const float sg = 1.0f / (1.0f + __expf(-g));
                 const float d = da[q * 8 + j];
-                du[q * 8 + j] = d * g * sg;
-                dg[q * 8 + j] = d * u * sg * (1.0f + g * (1.0f - sg));
+                du[j] = d * g * sg;
+                dg[j] = d * u * sg * (1.0f + g * (1.0f - sg));
               }
+              uint4 wg, wu;
+              wg.x = pack_bf16x2(dg[0], dg[1]); wg.y = pack_bf16x2(dg[2], dg[3]);
+              wg.z = pack_bf16x2(dg[4], dg[5]); wg.w = pack_bf16x2(dg[6], dg[7]);
+              wu.x = pack_bf16x2(du[0], du[1]); wu.y = pack_bf16x2(du[2], du[3]);
+              wu.z = pack_bf16x2(du[4], du[5]); wu.w = pack_bf16x2(du[6], du[7]);
+              reinterpret_cast<uint4*>(dgp)[q] = wg;
+              reinterpret_cast<uint4*>(dgp + 128)[q] = wu;
             }
-            store_row32(p.out + grow * p.ldo + hcol, dg, 32);
-            store_row32(p.out + grow * p.ldo + hcol + 128, du, 32);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { gcur[q] = gnxt[q]; ucur[q] = unxt[q]; }
+        }
+      } else {
+        mbar_wait(&sh.tmem_full[acc], aph);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kBN;
+        if (EPI == EPI_STORE) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c = half * 128 + 32 * i;
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(t_row + c, r);
+            tmem_ld_wait();
+            if (row_ok && c < ncols_valid)
+              store_row32(p.out + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
+                          min(32, ncols_valid - c));
+          }
+        } else {  // EPI_SWIGLU_FWD
+          // columns [0,128) = gate, [128,256) = up for f-columns [nt*128, +128); this warp
+          // takes the gate/up chunk pairs c = 64*half, 64*half + 32
+          const int f0 = tc.nt * (kBN / 2);
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int c = half * 64 + 32 * i;
+            uint32_t rg[32], ru[32];
+            tmem_ld_32x32b_x32(t_row + c, rg);
+            tmem_ld_32x32b_x32(t_row + kBN / 2 + c, ru);
+            tmem_ld_wait();
+            if (row_ok) {
+              float* g = reinterpret_cast<float*>(rg);
+              float* u = reinterpret_cast<float*>(ru);
+              // saved pre-activations are the bf16-rounded accumulators; the activation is
+              // computed from the same rounded values so forward and backward agree exactly.
+              float gq[32], uq[32], a[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                gq[j] = __bfloat162float(__float2bfloat16_rn(g[j]));
+                uq[j] = __bfloat162float(__float2bfloat16_rn(u[j]));
+                a[j] = silu_f(gq[j]) * uq[j];
+              }
+              store_row32(p.out2 + grow * p.ldo2 + n0 + c, gq, 32);
+              store_row32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, uq, 32);
+              store_row32(p.out + grow * p.ldo + f0 + c, a, 32);
+            }
           }
         }
       }

@@ -40,7 +40,8 @@ extern "C" {
 #define HM_GEMM_FWD_DOWN 1   /* out = A[rows,K] . B[e][N][K]^T                                 */
 #define HM_GEMM_BWD_DACT 2   /* dH = SwiGLU'(A[rows,K] . B[e][K][N], h)              (N = f)  */
 #define HM_GEMM_BWD_DX 3     /* out = A[rows,K] . B[e][K][N]                                   */
-#define HM_GEMM_WGRAD 4      /* out[e][M][N] = A[seg_e, M]^T . B[seg_e, N]                     */
+#define HM_GEMM_WGRAD 4      /* out[e][M][N] = A[seg_e, M]^T . B[seg_e, N]   (bf16 out)          */
+#define HM_GEMM_WGRAD_ACC 5  /* out[e][M][N] += A[seg_e, M]^T . B[seg_e, N]  (fp32 out, accumulate) */
 
 int hm_abi_version(void);
 const char* hm_last_error(void);
@@ -89,11 +90,13 @@ int hm_transpose_bf16(const void* in, int R, int C, void* out, void* stream);
 /* ---- K3 grouped expert GEMM (tcgen05 / TMEM / TMA) ----
  * seg_offsets[E+1] (device) delimit each expert's rows of the activation buffers.
  * GROUP_M modes: a = activations [rows, K]; b = per-expert weights ([E][N][K] or [E][K][N]).
- * WGRAD: a = [rows, M], b = [rows, N], out = [E][M][N].
+ * WGRAD(_ACC): a = [rows, M], b = [rows, N], out = [E][M][N]; needs a 128-byte aligned device
+ * workspace of hm_grouped_gemm_workspace_bytes(mode, E) bytes (per-expert TMA views).
  * max_ctas caps the persistent grid (capacity-weight emulation; <= 0 means all SMs). */
 int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_offsets, int E,
                     int rows, int M, int N, int K, void* out, int ldo, void* out2, int ldo2,
-                    const void* aux, int ld_aux, int max_ctas, void* stream);
+                    const void* aux, int ld_aux, void* workspace, int max_ctas, void* stream);
+size_t hm_grouped_gemm_workspace_bytes(int mode, int E);
 
 /* SwiGLU expert FFN forward over permuted rows:
  *   h[rows,2f]  = x_perm . w_ug[e]^T   (gate|up interleaved in 128-column blocks, saved for bwd)
@@ -105,11 +108,12 @@ int hm_grouped_ffn_fwd(const void* x_perm, int rows, const int32_t* seg_offsets,
                        const void* w_ug, const void* w_d, int d, int f, void* h, void* act,
                        void* y_perm, int max_ctas, void* stream);
 /* backward: dh = SwiGLU'(dy_perm . w_d[e]) (workspace [rows,2f]); dx_perm = dh . w_ug[e];
- * dw_ug[e] = dh_e^T . x_e; dw_d[e] = dy_e^T . act_e. Replaces EXP_B / OFF_EXP_B. */
+ * dw_ug[e] = dh_e^T . x_e; dw_d[e] = dy_e^T . act_e. workspace: 2 * hm_grouped_gemm_workspace_bytes(
+ * HM_GEMM_WGRAD, E) bytes, 128-byte aligned. Replaces EXP_B / OFF_EXP_B. */
 int hm_grouped_ffn_bwd(const void* dy_perm, const void* x_perm, const void* h, const void* act,
                        int rows, const int32_t* seg_offsets, int E, const void* w_ug,
                        const void* w_d, int d, int f, void* dh, void* dx_perm, void* dw_ug,
-                       void* dw_d, int max_ctas, void* stream);
+                       void* dw_d, void* workspace, int max_ctas, void* stream);
 
 #ifdef __cplusplus
 }

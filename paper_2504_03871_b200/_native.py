@@ -20,6 +20,7 @@ GEMM_FWD_DOWN = 1
 GEMM_BWD_DACT = 2
 GEMM_BWD_DX = 3
 GEMM_WGRAD = 4
+GEMM_WGRAD_ACC = 5
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -39,9 +40,10 @@ SIGNATURES = {
     "hm_router_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "hm_router_bwd_part_elems": (ctypes.c_size_t, [_I, _I, _I]),
     "hm_transpose_bf16": (_I, [_P, _I, _I, _P, _P]),
-    "hm_grouped_gemm": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _I, _P]),
+    "hm_grouped_gemm": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P]),
+    "hm_grouped_gemm_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
     "hm_grouped_ffn_fwd": (_I, [_P, _I, _P, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P]),
-    "hm_grouped_ffn_bwd": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _P, _I, _I, _P, _P, _P, _P, _I, _P]),
+    "hm_grouped_ffn_bwd": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P]),
 }
 
 

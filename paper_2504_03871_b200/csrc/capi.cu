@@ -327,15 +327,21 @@ int hm_transpose_bf16(const void* in, int R, int C, void* out, void* stream) {
 }
 
 // ---------------------------------------------------------------------------------------------
+size_t hm_grouped_gemm_workspace_bytes(int mode, int E) {
+  return (mode == HM_GEMM_WGRAD || mode == HM_GEMM_WGRAD_ACC) ? static_cast<size_t>(2 * E) * sizeof(CUtensorMap) : 0;
+}
+
 int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_offsets, int E,
                     int rows, int M, int N, int K, void* out, int ldo, void* out2, int ldo2,
-                    const void* aux, int ld_aux, int max_ctas, void* stream) {
+                    const void* aux, int ld_aux, void* workspace, int max_ctas, void* stream) {
   if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "gemm: E=%d out of range", E);
   if (rows < 0 || N <= 0 || N % 8 != 0) return fail(HM_E_SHAPE, "gemm: bad rows/N");
   if (!aligned16(a) || !aligned16(b) || !aligned16(out)) return fail(HM_E_ALIGN, "gemm: alignment");
   if (ldo % 8 != 0) return fail(HM_E_ALIGN, "gemm: ldo must be a multiple of 8");
   cudaStream_t st = S(stream);
-  const bool wgrad = (mode == HM_GEMM_WGRAD);
+  const bool wgrad = (mode == HM_GEMM_WGRAD || mode == HM_GEMM_WGRAD_ACC);
+  if (wgrad && (workspace == nullptr || (reinterpret_cast<uintptr_t>(workspace) & 127u)))
+    return fail(HM_E_ARG, "gemm: wgrad needs a 128-byte aligned workspace of hm_grouped_gemm_workspace_bytes()");
   if (!wgrad && (K <= 0 || K % 8 != 0)) return fail(HM_E_SHAPE, "gemm: K must be a positive multiple of 8");
   if (wgrad && (M <= 0 || M % 8 != 0)) return fail(HM_E_SHAPE, "gemm: M must be a positive multiple of 8");
   if (rows == 0 && !wgrad) return 0;
@@ -347,6 +353,7 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
   p.N = N;
   p.K = K;
   p.out = static_cast<__nv_bfloat16*>(out);
+  p.out_f32 = static_cast<float*>(out);
   p.ldo = ldo;
   p.out2 = static_cast<__nv_bfloat16*>(out2);
   p.ldo2 = ldo2;
@@ -355,7 +362,7 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
 
   CUtensorMap ma, mb;
   const int rows_m = rows > 0 ? rows : 1;
-  const int ctas = wgrad ? 1 : gemm_ctas();
+  const int ctas = gemm_ctas();
   if (!wgrad) {
     {
       uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows_m};
@@ -388,6 +395,13 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
     uint64_t str_b[1] = {(uint64_t)N * 2};
     if (int rc = make_map(&mb, b, 2, dims_b, str_b, box)) return rc;
     p.n_fastest = (M >= N) ? 1 : 0;
+    // per-expert views (device side, no host sync on the expert sizes)
+    CUtensorMap* maps = static_cast<CUtensorMap*>(workspace);
+    hm::build_expert_maps_kernel<<<(E + 127) / 128, 128, 0, st>>>(
+        ma, mb, seg_offsets, E, static_cast<const uint8_t*>(a), static_cast<long>(M) * 2,
+        static_cast<const uint8_t*>(b), static_cast<long>(N) * 2, maps);
+    if (int rc = check_launch("build_expert_maps")) return rc;
+    p.expert_maps = maps;
   }
 
   switch (mode) {
@@ -406,7 +420,11 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
       return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
                        : launch_gemm<false, false, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
     case HM_GEMM_WGRAD:
-      return launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
+                       : launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
+    case HM_GEMM_WGRAD_ACC:
+      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_ACC_F32, 2>(ma, mb, p, max_ctas, st)
+                       : launch_gemm<true, true, true, hm::EPI_ACC_F32, 1>(ma, mb, p, max_ctas, st);
     default:
       return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
   }
@@ -417,32 +435,35 @@ int hm_grouped_ffn_fwd(const void* x_perm, int rows, const int32_t* seg_offsets,
                        void* y_perm, int max_ctas, void* stream) {
   if (f % 128 != 0) return fail(HM_E_SHAPE, "ffn: f=%d must be a multiple of 128", f);
   if (int rc = hm_grouped_gemm(HM_GEMM_FWD_UPGATE, x_perm, w_ug, seg_offsets, E, rows, 0, 2 * f, d,
-                               act, f, h, 2 * f, nullptr, 0, max_ctas, stream))
+                               act, f, h, 2 * f, nullptr, 0, nullptr, max_ctas, stream))
     return rc;
   return hm_grouped_gemm(HM_GEMM_FWD_DOWN, act, w_d, seg_offsets, E, rows, 0, d, f, y_perm, d,
-                         nullptr, 0, nullptr, 0, max_ctas, stream);
+                         nullptr, 0, nullptr, 0, nullptr, max_ctas, stream);
 }
 
 int hm_grouped_ffn_bwd(const void* dy_perm, const void* x_perm, const void* h, const void* act,
                        int rows, const int32_t* seg_offsets, int E, const void* w_ug,
                        const void* w_d, int d, int f, void* dh, void* dx_perm, void* dw_ug,
-                       void* dw_d, int max_ctas, void* stream) {
+                       void* dw_d, void* workspace, int max_ctas, void* stream) {
   if (f % 128 != 0) return fail(HM_E_SHAPE, "ffn: f=%d must be a multiple of 128", f);
   // dH = SwiGLU'(dY . W_d[e]) : K = d, N = f
   if (int rc = hm_grouped_gemm(HM_GEMM_BWD_DACT, dy_perm, w_d, seg_offsets, E, rows, 0, f, d, dh,
-                               2 * f, nullptr, 0, h, 2 * f, max_ctas, stream))
+                               2 * f, nullptr, 0, h, 2 * f, nullptr, max_ctas, stream))
     return rc;
   // dX = dH . W_ug[e] : K = 2f, N = d
   if (int rc = hm_grouped_gemm(HM_GEMM_BWD_DX, dh, w_ug, seg_offsets, E, rows, 0, d, 2 * f, dx_perm,
-                               d, nullptr, 0, nullptr, 0, max_ctas, stream))
+                               d, nullptr, 0, nullptr, 0, nullptr, max_ctas, stream))
     return rc;
   // dW_ug[e] = dH_e^T . X_e : M = 2f, N = d
   if (int rc = hm_grouped_gemm(HM_GEMM_WGRAD, dh, x_perm, seg_offsets, E, rows, 2 * f, d, 0, dw_ug,
-                               d, nullptr, 0, nullptr, 0, max_ctas, stream))
+                               d, nullptr, 0, nullptr, 0, workspace, max_ctas, stream))
     return rc;
-  // dW_d[e] = dY_e^T . act_e : M = d, N = f
+  // dW_d[e] = dY_e^T . act_e : M = d, N = f  (second half of the workspace: the first call's
+  // maps may still be in use by its kernel)
   return hm_grouped_gemm(HM_GEMM_WGRAD, dy_perm, act, seg_offsets, E, rows, d, f, 0, dw_d, f,
-                         nullptr, 0, nullptr, 0, max_ctas, stream);
+                         nullptr, 0, nullptr, 0,
+                         static_cast<uint8_t*>(workspace) + hm_grouped_gemm_workspace_bytes(HM_GEMM_WGRAD, E),
+                         max_ctas, stream);
 }
 
 }  // extern "C"

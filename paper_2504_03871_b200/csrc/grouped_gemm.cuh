@@ -18,15 +18,15 @@
 //
 // Tiles that straddle an expert boundary (GROUP_M) load a few rows of the next expert; those
 // rows are computed with the wrong weights and are never stored (row mask in the epilogue).
-// For GROUP_K the last K block of an expert would contract rows of the next expert, so the
-// MMA warp zero-fills those rows of the A tile in shared memory before issuing the MMAs.
+// For GROUP_K the K loop runs over one expert's rows through per-expert TMA views
+// (build_expert_maps_kernel), so rows past the expert's end arrive as zeros.
 #pragma once
 
 #include "hm_common.cuh"
 
 namespace hm {
 
-enum EpilogueKind : int { EPI_STORE = 0, EPI_SWIGLU_FWD = 1, EPI_SWIGLU_BWD = 2 };
+enum EpilogueKind : int { EPI_STORE = 0, EPI_SWIGLU_FWD = 1, EPI_SWIGLU_BWD = 2, EPI_ACC_F32 = 3 };
 
 constexpr int kBM = 128;  // accumulator rows per CTA (TMEM lanes)
 constexpr int kBN = 256;  // accumulator columns (UMMA N)
@@ -66,7 +66,53 @@ struct GroupedGemmParams {
   const __nv_bfloat16* aux;  // SWIGLU_BWD: h saved by the forward [rows, 2N]
   int ld_aux;
   int n_fastest;  // raster: 1 = n-tile index varies fastest within an expert
+  const CUtensorMap* expert_maps;  // GROUP_K: per-expert TMA views, [2e] = A rows, [2e+1] = B rows
+  float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
 };
+
+// out[0..31] += v[0..31] (fp32), masked to valid_cols
+HM_DEV void acc_row32(float* dst, const float* v, int valid_cols) {
+  if (valid_cols >= 32) {
+    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 o = d4[q];
+      o.x += v[q * 4 + 0]; o.y += v[q * 4 + 1]; o.z += v[q * 4 + 2]; o.w += v[q * 4 + 3];
+      d4[q] = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < valid_cols) dst[j] += v[j];
+  }
+}
+
+// Per-expert TMA views for the variable-K weight gradient: copies of the whole-buffer maps
+// whose base address is moved to the expert's first row and whose row extent is m_e, so TMA
+// zero-fills every row past the expert's end (no contraction over a neighbour's rows).
+__global__ void build_expert_maps_kernel(const __grid_constant__ CUtensorMap tmpl_a,
+                                         const __grid_constant__ CUtensorMap tmpl_b,
+                                         const int* __restrict__ seg_offsets, int E,
+                                         const uint8_t* base_a, long row_bytes_a,
+                                         const uint8_t* base_b, long row_bytes_b,
+                                         CUtensorMap* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int s0 = seg_offsets[e];
+  const int me = seg_offsets[e + 1] - s0;
+  const uint32_t rows = me > 0 ? static_cast<uint32_t>(me) : 1u;
+  const uint4* ta = reinterpret_cast<const uint4*>(&tmpl_a);
+  const uint4* tb = reinterpret_cast<const uint4*>(&tmpl_b);
+  uint4* oa = reinterpret_cast<uint4*>(out + 2 * e);
+  uint4* ob = reinterpret_cast<uint4*>(out + 2 * e + 1);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { oa[i] = ta[i]; ob[i] = tb[i]; }
+  tensormap_set_address(out + 2 * e, base_a + static_cast<long>(s0) * row_bytes_a);
+  tensormap_set_dim(out + 2 * e, 1, rows);
+  tensormap_set_address(out + 2 * e + 1, base_b + static_cast<long>(s0) * row_bytes_b);
+  tensormap_set_dim(out + 2 * e + 1, 1, rows);
+  tensormap_release();
+}
 
 struct GemmShared {
   uint64_t full[kMaxStages];
@@ -129,7 +175,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GroupedGemmParams p) {
   using Cfg = TileCfg<CTAS>;
-  static_assert(!(GROUP_K && CTAS == 2), "wgrad runs on single-CTA tiles");
   constexpr int kStages = Cfg::kStages;
   constexpr int kStageBytes = Cfg::kStageBytes;
   constexpr int kTileM = Cfg::kTileM;
@@ -189,56 +234,63 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       const uint64_t pol = policy_evict_normal();
       uint32_t it = 0;
+      int mapped_e = -1;
       for (int tile = tile0; tile < total_tiles; tile += tile_step) {
         const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
         const int seg0 = sh.seg[tc.e];
         const int me = sh.seg[tc.e + 1] - seg0;
         const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
+        const CUtensorMap* mA = &map_a;
+        const CUtensorMap* mB = &map_b;
+        if (GROUP_K) {
+          mA = p.expert_maps + 2 * tc.e;
+          mB = mA + 1;
+          if (nk > 0 && tc.e != mapped_e) {
+            tensormap_acquire(mA);
+            tensormap_acquire(mB);
+            mapped_e = tc.e;
+          }
+        }
+        // this CTA's share of the tile: A rows (M) and B rows (N)
+        const int m0 = tc.mt * kTileM + static_cast<int>(rank) * kBM;
+        const int n0 = tc.nt * kBN + static_cast<int>(rank) * Cfg::kBRows;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
           mbar_wait(&sh.empty[s], ph ^ 1);
           uint8_t* sa = tiles + s * kStageBytes;
           uint8_t* sb = sa + kATileBytes;
+          uint32_t bar;
           if (CTAS == 1) {
             mbar_arrive_expect_tx(&sh.full[s], kStageBytes);
-            if (!GROUP_K) {
-              // A: activation rows [seg0 + mt*128, +128), K-major box {64, 128}
-              tma_load_2d(sa, &map_a, &sh.full[s], kb * kBK, seg0 + tc.mt * kTileM, pol);
-              if (!B_MN) {
-                // B: W[e] stored [N][K]; box {64, 256}
-                tma_load_3d(sb, &map_b, &sh.full[s], kb * kBK, tc.nt * kBN, tc.e, pol);
-              } else {
-                // B: W[e] stored [K][N]; four 64-wide N panels, box {64 (N), 64 (K)}
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  tma_load_3d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, kb * kBK,
-                              tc.e, pol);
-              }
-            } else {
-              // wgrad: both operands are [rows = K][cols] activations (MN-major), box {64, 64}
-              const int k0 = seg0 + kb * kBK;
-#pragma unroll
-              for (int q = 0; q < 2; ++q)
-                tma_load_2d(sa + q * 8192, &map_a, &sh.full[s], tc.mt * kTileM + q * 64, k0, pol);
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                tma_load_2d(sb + q * 8192, &map_b, &sh.full[s], tc.nt * kBN + q * 64, k0, pol);
-            }
+            bar = smem_u32(&sh.full[s]);
           } else {
             // CTA pair: every load completes on the leader's full barrier, which the leader
             // arms with both CTAs' bytes.
-            const uint32_t lbar = mapa_shared(&sh.full[s], 0);
+            bar = mapa_shared(&sh.full[s], 0);
             if (leader) mbar_arrive_expect_tx(&sh.full[s], 2 * kStageBytes);
-            tma_load_2d_pair(sa, &map_a, lbar, kb * kBK, seg0 + tc.mt * kTileM + rank * kBM, pol);
-            const int n0 = tc.nt * kBN + rank * Cfg::kBRows;
+          }
+          if (!GROUP_K) {
+            // A: activation rows [seg0 + m0, +128), K-major box {64, 128}
+            tma_load_2d_any<CTAS>(sa, mA, bar, kb * kBK, seg0 + m0, pol);
             if (!B_MN) {
-              tma_load_3d_pair(sb, &map_b, lbar, kb * kBK, n0, tc.e, pol);
+              // B: W[e] stored [N][K]; box {64, kBRows}
+              tma_load_3d_any<CTAS>(sb, mB, bar, kb * kBK, n0, tc.e, pol);
             } else {
+              // B: W[e] stored [K][N]; 64-wide N panels, box {64 (N), 64 (K)}
 #pragma unroll
               for (int q = 0; q < Cfg::kBRows / 64; ++q)
-                tma_load_3d_pair(sb + q * 8192, &map_b, lbar, n0 + q * 64, kb * kBK, tc.e, pol);
+                tma_load_3d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, tc.e, pol);
             }
+          } else {
+            // wgrad: both operands are the expert's [rows = K][cols] activations (MN-major),
+            // box {64, 64}; rows past the expert's end are zero-filled by TMA
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              tma_load_2d_any<CTAS>(sa + q * 8192, mA, bar, m0 + q * 64, kb * kBK, pol);
+#pragma unroll
+            for (int q = 0; q < Cfg::kBRows / 64; ++q)
+              tma_load_2d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, pol);
           }
         }
       }
@@ -266,22 +318,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           uint8_t* sa = tiles + s * kStageBytes;
           uint8_t* sb = sa + kATileBytes;
-          if (GROUP_K && kb == nk - 1) {
-            const int rem = me - kb * kBK;  // valid K rows in this block (1..64)
-            if (rem < kBK) {
-              // zero K rows [rem, 64) of both 64-wide panels of the MN-major A tile
-              const int nrows = kBK - rem;
-              for (int i = lane; i < nrows * 2 * 8; i += 32) {
-                const int chunk = i & 7;
-                const int rr = rem + ((i >> 3) % nrows);
-                const int q = (i >> 3) / nrows;
-                uint4* dst = reinterpret_cast<uint4*>(sa + q * 8192 + (rr >> 3) * 1024 + (rr & 7) * 128) + chunk;
-                *dst = make_uint4(0u, 0u, 0u, 0u);
-              }
-              fence_proxy_async_smem();
-              __syncwarp();
-            }
-          }
           if (lane == 0) {
             const uint32_t a_addr = smem_u32(sa);
             const uint32_t b_addr = smem_u32(sb);
@@ -329,8 +365,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         grow = static_cast<long>(tc.e) * p.M + tc.mt * kTileM + row_in_tile;
       }
       if (GROUP_K && me == 0) {
-        // empty expert: its weight gradient is exactly zero
-        if (row_ok) {
+        // empty expert: its weight gradient is exactly zero (nothing to add when accumulating)
+        if (row_ok && EPI != EPI_ACC_F32) {
           float z[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) z[j] = 0.f;
@@ -410,16 +446,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&sh.tmem_full[acc], aph);
         tc_fence_after();
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16) + acc * kBN;
-        if (EPI == EPI_STORE) {
+        if (EPI == EPI_STORE || EPI == EPI_ACC_F32) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int c = half * 128 + 32 * i;
             uint32_t r[32];
             tmem_ld_32x32b_x32(t_row + c, r);
             tmem_ld_wait();
-            if (row_ok && c < ncols_valid)
-              store_row32(p.out + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
+            if (row_ok && c < ncols_valid) {
+              if (EPI == EPI_STORE)
+                store_row32(p.out + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
+                            min(32, ncols_valid - c));
+              else
+                acc_row32(p.out_f32 + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
                           min(32, ncols_valid - c));
+            }
           }
         } else {  // EPI_SWIGLU_FWD
           // columns [0,128) = gate, [128,256) = up for f-columns [nt*128, +128); this warp

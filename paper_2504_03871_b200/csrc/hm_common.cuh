@@ -323,3 +323,71 @@ HM_DEV void umma_commit_pair(uint64_t* bar, uint16_t cta_mask) {
 }
 
 }  // namespace hm
+
+// ---------------------------------------------------------------------------------------------
+// device-side tensor-map editing (per-expert TMA views for the variable-K weight gradient)
+
+namespace hm {
+
+HM_DEV void tensormap_set_address(CUtensorMap* map, const void* addr) {
+  asm volatile("tensormap.replace.tile.global_address.global.b1024.b64 [%0], %1;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "l"(reinterpret_cast<uint64_t>(addr))
+               : "memory");
+}
+
+// ordinal `dim` of the global shape (0 = innermost)
+HM_DEV void tensormap_set_dim(CUtensorMap* map, int dim, uint32_t extent) {
+  if (dim == 1)
+    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 1, %1;" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(extent)
+                 : "memory");
+  else
+    asm volatile("tensormap.replace.tile.global_dim.global.b1024.b32 [%0], 0, %1;" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(extent)
+                 : "memory");
+}
+
+HM_DEV void tensormap_release() {
+  asm volatile("fence.proxy.tensormap::generic.release.gpu;" ::: "memory");
+}
+
+HM_DEV void tensormap_acquire(const CUtensorMap* map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                   reinterpret_cast<uint64_t>(map))
+               : "memory");
+}
+
+}  // namespace hm
+
+namespace hm {
+// TMA loads addressed by a 32-bit shared::cta / shared::cluster barrier address.
+template <int CTAS>
+HM_DEV void tma_load_2d_any(void* smem_dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
+                            int32_t c1, uint64_t hint) {
+  if (CTAS == 2) {
+    tma_load_2d_pair(smem_dst, map, bar, c0, c1, hint);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(hint)
+        : "memory");
+  }
+}
+template <int CTAS>
+HM_DEV void tma_load_3d_any(void* smem_dst, const CUtensorMap* map, uint32_t bar, int32_t c0,
+                            int32_t c1, int32_t c2, uint64_t hint) {
+  if (CTAS == 2) {
+    tma_load_3d_pair(smem_dst, map, bar, c0, c1, c2, hint);
+  } else {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(hint)
+        : "memory");
+  }
+}
+}  // namespace hm

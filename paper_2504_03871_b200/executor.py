@@ -1,0 +1,501 @@
+"""Zebra-parallel (ZP) executor: runs a ``TaskGraph`` on real devices and returns a MEASURED
+``Timeline`` — the B200 replacement for the reference's timing model
+``simulate(graph, orders)`` (``/root/reference/pkg/src/zpsim/simulator.py:33``).
+
+One process per GPU. Ranks ``[0, M)`` are attention ranks, ``[M, M+N)`` expert ranks
+(``ZpGroupSpec``, ``core.py:70-79``). Each rank owns three CUDA streams — compute, dispatch,
+combine (``PAPER.md:198``) — and two NCCL communicators, one per comm lane, so dispatch and
+combine transfers overlap compute and each other. Every task of the graph is issued in ONE
+global order (the simulated start order of the graph under ``default_orders``), so each
+communicator sees its collectives in the same order on every rank (``comm_order``,
+``scheduler.py:110-140``). Cross-lane edges of the DAG become CUDA events.
+
+What each task kind does here:
+  ATTN_F(l,j)   combine(l-1) + residual, attention block, router, dispatch permute
+  DISP_F(l,j)   expert-count all-gather, then NCCL send/recv of the permuted rows to the
+                experts' owners (expert ranks, or attention ranks for Asym-EA offloaded experts)
+  EXP_F / OFF_EXP_F   grouped SwiGLU FFN over the received rows (expert-major layout)
+  COMB_F(l,j)   expert outputs back to their senders
+  DISP_B(l,j)   (l = L: final combine + loss gradient + combine-bwd, the zp-full turnaround)
+                send of dY rows
+  EXP_B / OFF_EXP_B   grouped FFN backward; expert weight grads accumulate in fp32
+  COMB_B(l,j)   dX rows back
+  ATTN_B(l,j)   router backward + unpermute-sum, residual, attention backward, combine-bwd(l-1)
+
+Expert placement per layer follows the Asym-EA assignment (``expert_owners``): each expert
+rank gives its last o_l local experts to the attention ranks, dealt in (expert rank, local
+id) order in blocks of o_l*N/M, which reproduces ``offload_scaling``'s shares exactly
+(``taskgraph.py:178-194``).
+
+The tensor work goes through a backend object. ``NativeBackend`` (this file) is the product
+path: native sm_100a kernels + torch CUDA streams/events. There is no implicit CPU fallback;
+the CPU/gloo tests inject their own backend explicitly.
+"""
+
+from __future__ import annotations
+
+import contextlib
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from .core import ExpertAssignment
+from .scheduler import default_orders
+from .simulator import MeasuredTimeline, simulate
+from .taskgraph import TaskGraph, TaskKind
+
+K = TaskKind
+
+
+# ---------------------------------------------------------------------------------------------
+# placement
+
+
+def expert_owners(E: int, M: int, N: int, offload: int) -> list:
+    """Owner rank of every expert of one layer. Base: expert rank M+i owns experts
+    [i*E/N, (i+1)*E/N). With offload o, the last o local experts of each expert rank move to
+    the attention ranks, dealt in (expert rank, local id) order, o*N/M per attention rank."""
+    per = E // N
+    owners = [M + e // per for e in range(E)]
+    if offload:
+        moved = [i * per + loc for i in range(N) for loc in range(per - offload, per)]
+        block = offload * N // M
+        if block * M != offload * N or block < 1:
+            raise ValueError(f"offload {offload} does not split evenly over {M} attention ranks")
+        for idx, e in enumerate(moved):
+            owners[e] = idx // block
+    return owners
+
+
+@dataclass(frozen=True)
+class ZpLayerShape:
+    """Tensor shape of one MoE transformer layer as executed."""
+
+    E: int
+    k: int
+    d: int
+    f: int
+    tokens_per_mb: int  # tokens per micro-batch per attention rank
+    heads: int = 0  # attention heads (0 = d // 128)
+    attention: bool = True  # include the attention block (False: identity + residual)
+
+
+# ---------------------------------------------------------------------------------------------
+# backends
+
+
+class NativeBackend:
+    """Product backend: sm_100a kernels (``ops``) on three CUDA streams of one device."""
+
+    def __init__(self, device, max_ctas: int = 0):
+        from . import ops  # requires the built extension; fails loudly otherwise
+
+        self.ops = ops
+        self.device = torch.device(device)
+        self.max_ctas = max_ctas
+        self.streams = {lane: torch.cuda.Stream(self.device) for lane in ("compute", "dispatch", "combine")}
+        self.dtype = torch.bfloat16
+
+    # streams / events
+    def on(self, lane: str):
+        return torch.cuda.stream(self.streams[lane])
+
+    def mark(self):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def wait(self, ev) -> None:
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+
+    def host_wait(self, ev) -> None:
+        ev.synchronize()
+
+    def elapsed_ns(self, a, b) -> int:
+        return int(round(a.elapsed_time(b) * 1e6))
+
+    def synchronize(self) -> None:
+        torch.cuda.synchronize(self.device)
+
+    # tensor ops
+    def router(self, u, wg, k):
+        r = self.ops.router_topk(u, wg, k)
+        return r
+
+    def permute(self, u, r):
+        x_perm, _row_src, row_of = self.ops.dispatch_permute(u, r)
+        return x_perm, row_of
+
+    def counts(self, r):
+        return r.counts
+
+    def combine(self, y_perm, row_of, r):
+        return self.ops.combine(y_perm, row_of, r.w)
+
+    def combine_bwd(self, dy, y_perm, row_of, r):
+        return self.ops.combine_bwd(dy, y_perm, row_of, r.w)
+
+    def router_bwd(self, dx_perm, row_of, r, dw, u, wg_t):
+        dx, _dl, dwg = self.ops.router_bwd(dx_perm, row_of, r, dw, u, wg_t, want_dwg=True)
+        return dx, dwg
+
+    def transpose(self, w):
+        return self.ops.transpose_bf16(w)
+
+    def ffn_fwd(self, x, seg, w_ug, w_d):
+        return self.ops.grouped_ffn_fwd(x, seg, w_ug, w_d, self.max_ctas)
+
+    def ffn_bwd_acc(self, dy, x, h, act, seg, w_ug, w_d, gw_ug, gw_d):
+        return self.ops.grouped_ffn_bwd_acc(dy, x, h, act, seg, w_ug, w_d, gw_ug, gw_d, self.max_ctas)
+
+    def tensor(self, shape, dtype=None):
+        return torch.empty(shape, dtype=dtype or self.dtype, device=self.device)
+
+    def seg_tensor(self, offsets):
+        return torch.tensor(offsets, dtype=torch.int32, device=self.device)
+
+
+# ---------------------------------------------------------------------------------------------
+# per-rank model state
+
+
+def attention_block(h, wqkv, wo, heads: int):
+    """u = h + Attn(h): fused QKV projection, causal SDPA, output projection (torch/cuBLAS/
+    flash attention; not one of the four hot-path kernels)."""
+    T, d = h.shape
+    hd = d // heads
+    qkv = (h @ wqkv).view(T, 3, heads, hd).permute(1, 2, 0, 3)
+    o = torch.nn.functional.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True)
+    return h + o.permute(1, 0, 2).reshape(T, d) @ wo
+
+
+@dataclass
+class RankState:
+    """Parameters (and fp32 gradient accumulators) resident on one rank."""
+
+    owners: list  # per layer: owner rank of each expert
+    own: list  # per layer: sorted expert ids owned by this rank
+    w_ug: dict = field(default_factory=dict)  # layer -> [E_own, 2f, d]
+    w_d: dict = field(default_factory=dict)
+    gw_ug: dict = field(default_factory=dict)  # fp32 accumulators
+    gw_d: dict = field(default_factory=dict)
+    wg: dict = field(default_factory=dict)  # attention ranks: router [d, E]
+    gwg: dict = field(default_factory=dict)
+    wqkv: dict = field(default_factory=dict)
+    wo: dict = field(default_factory=dict)
+
+
+class ZpExecutor:
+    """Executes one ZP training iteration per ``run()`` on this rank."""
+
+    def __init__(self, graph: TaskGraph, shape: ZpLayerShape, M: int, N: int, rank: int,
+                 backend, disp_group=None, comb_group=None, seed: int = 0,
+                 durations_hint: Optional[dict] = None):
+        if graph.mode != "zp-full":
+            raise ValueError("the executor runs zp-full graphs (layer-L experts + loss turnaround)")
+        if shape.E % N:
+            raise ValueError("N must divide E")
+        self.g, self.s, self.M, self.N, self.rank = graph, shape, M, N, rank
+        self.W = M + N
+        self.be = backend
+        self.disp_group, self.comb_group = disp_group, comb_group
+        self.is_attn = rank < M
+        self.L, self.R = graph.layers, graph.microbatches
+        self.heads = shape.heads or max(1, shape.d // 128)
+        self.orders = default_orders(graph)
+        self.issue_order = self._issue_order()
+        owners = [expert_owners(shape.E, M, N, o) for o in graph.assignment.offload]
+        own = [sorted(e for e in range(shape.E) if ow[e] == rank) for ow in owners]
+        self.st = RankState(owners=owners, own=own)
+        self._init_params(seed)
+
+    # ------------------------------------------------------------------ setup
+    def _issue_order(self):
+        tl = simulate(self.g, self.orders)
+        return sorted(self.g.tasks, key=lambda t: (tl.starts[t.id], t.id))
+
+    def _init_params(self, seed: int) -> None:
+        s, be, st = self.s, self.be, self.st
+        gen = torch.Generator().manual_seed(seed)
+
+        def rand(shape, std):
+            # parameters are generated on the CPU from one global seed so every rank agrees
+            return (torch.randn(shape, generator=gen) * std).to(be.dtype)
+
+        for l in range(1, self.L + 1):
+            wqkv = rand((s.d, 3 * s.d), s.d ** -0.5)
+            wo = rand((s.d, s.d), s.d ** -0.5)
+            wg = rand((s.d, s.E), s.d ** -0.5)
+            w_ug_all = rand((s.E, 2 * s.f, s.d), s.d ** -0.5)
+            w_d_all = rand((s.E, s.d, s.f), s.f ** -0.5)
+            if self.is_attn:
+                st.wqkv[l] = wqkv.to(be.device).requires_grad_()
+                st.wo[l] = wo.to(be.device).requires_grad_()
+                st.wg[l] = wg.to(be.device)
+                st.gwg[l] = torch.zeros((s.d, s.E), dtype=torch.float32, device=be.device)
+            own = st.own[l - 1]
+            if own:
+                idx = torch.tensor(own)
+                st.w_ug[l] = w_ug_all[idx].contiguous().to(be.device)
+                st.w_d[l] = w_d_all[idx].contiguous().to(be.device)
+                st.gw_ug[l] = torch.zeros(st.w_ug[l].shape, dtype=torch.float32, device=be.device)
+                st.gw_d[l] = torch.zeros(st.w_d[l].shape, dtype=torch.float32, device=be.device)
+        # synthetic inputs / output gradient per micro-batch (attention ranks)
+        self.inputs, self.out_grads = {}, {}
+        if self.is_attn:
+            g2 = torch.Generator().manual_seed(seed * 7919 + 17 + self.rank)
+            for j in range(1, self.R + 1):
+                self.inputs[j] = torch.randn((s.tokens_per_mb, s.d), generator=g2).to(be.dtype).to(be.device)
+                self.out_grads[j] = torch.randn((s.tokens_per_mb, s.d), generator=g2).to(be.dtype).to(be.device)
+
+    # ------------------------------------------------------------------ helpers
+    def _ev(self, key):
+        return self.events.get(key)
+
+    def _recv_layout(self, l: int, counts_all):
+        """Expert-major receive layout on this rank for layer l: for each owned expert, the rows
+        of every attention rank in rank order. Returns (segment offsets per owned expert,
+        {(a, e): (recv_off, rows)})."""
+        seg = [0]
+        pos = {}
+        off = 0
+        for e in self.st.own[l - 1]:
+            for a in range(self.M):
+                c = counts_all[a][e]
+                pos[(a, e)] = (off, c)
+                off += c
+            seg.append(off)
+        return seg, pos
+
+    def _send_offsets(self, counts_row):
+        off, acc = [], 0
+        for c in counts_row:
+            off.append(acc)
+            acc += c
+        return off
+
+    def _exchange(self, l, j, buf_send, buf_recv, forward: bool, group):
+        """One all-to-all of rows between attention ranks and owners.
+
+        forward=True: attention rank a sends rows of expert e (its permuted buffer) to
+        owner[e]; owners receive expert-major. forward=False: the reverse."""
+        owners = self.st.owners[l - 1]
+        counts_all = self.counts[(l, j)]
+        ops_ = []
+        me = self.rank
+        for e in range(self.s.E):
+            o = owners[e]
+            for a in range(self.M):
+                c = counts_all[a][e]
+                if c == 0:
+                    continue
+                s_off = self.send_off[(l, j, a)][e]
+                if o == me:
+                    r_off, _ = self.recv_pos[(l, j)][(a, e)]
+                if forward:
+                    if a == me and o == me:
+                        buf_recv[r_off:r_off + c].copy_(buf_send[s_off:s_off + c])
+                    elif a == me:
+                        ops_.append(dist.P2POp(dist.isend, buf_send[s_off:s_off + c], o, group=group))
+                    elif o == me:
+                        ops_.append(dist.P2POp(dist.irecv, buf_recv[r_off:r_off + c], a, group=group))
+                else:
+                    if a == me and o == me:
+                        buf_recv[s_off:s_off + c].copy_(buf_send[r_off:r_off + c])
+                    elif o == me:
+                        ops_.append(dist.P2POp(dist.isend, buf_send[r_off:r_off + c], a, group=group))
+                    elif a == me:
+                        ops_.append(dist.P2POp(dist.irecv, buf_recv[s_off:s_off + c], o, group=group))
+        if ops_:
+            for w in dist.batch_isend_irecv(ops_):
+                w.wait()
+
+    # ------------------------------------------------------------------ task handlers
+    def _attn_f(self, l, j):
+        s, st, be = self.s, self.st, self.be
+        if l == 1:
+            h = self.inputs[j].detach().requires_grad_()
+        else:
+            y = be.combine(self.y_perm[(l - 1, j)], self.row_of[(l - 1, j)], self.route[(l - 1, j)])
+            h = (self.u[(l - 1, j)].detach() + y).requires_grad_()
+        self.h_in[(l, j)] = h
+        with torch.enable_grad():
+            u = attention_block(h, st.wqkv[l], st.wo[l], self.heads) if s.attention else h * 1
+        self.u[(l, j)] = u
+        ud = u.detach()
+        r = be.router(ud, st.wg[l], s.k)
+        x_perm, row_of = be.permute(ud, r)
+        self.route[(l, j)], self.row_of[(l, j)], self.x_perm[(l, j)] = r, row_of, x_perm
+        self.my_counts[(l, j)] = be.counts(r)
+
+    def _disp_f(self, l, j):
+        s, be = self.s, self.be
+        mine = self.my_counts.get((l, j))
+        if mine is None:
+            mine = be.tensor((s.E,), torch.int32).zero_()
+        gathered = [be.tensor((s.E,), torch.int32) for _ in range(self.W)]
+        dist.all_gather(gathered, mine.to(torch.int32), group=self.disp_group)
+        allc = torch.stack(gathered).cpu()  # the one host sync per (layer, micro-batch)
+        counts_all = [[int(v) for v in allc[a].tolist()] for a in range(self.M)]
+        self.counts[(l, j)] = counts_all
+        for a in range(self.M):
+            self.send_off[(l, j, a)] = self._send_offsets(counts_all[a])
+        seg, pos = self._recv_layout(l, counts_all)
+        self.recv_pos[(l, j)] = pos
+        self.seg[(l, j)] = seg
+        rows = seg[-1]
+        self.x_recv[(l, j)] = x_recv = be.tensor((max(rows, 1), s.d))
+        self._exchange(l, j, self.x_perm.get((l, j)), x_recv, True, self.disp_group)
+
+    def _exp_f(self, l, j):
+        st, be = self.st, self.be
+        seg = self.seg[(l, j)]
+        self.seg_t[(l, j)] = seg_t = be.seg_tensor(seg)
+        x = self.x_recv[(l, j)][: max(seg[-1], 1)]
+        y, h, act = be.ffn_fwd(x, seg_t, st.w_ug[l], st.w_d[l])
+        self.y_recv[(l, j)], self.h_save[(l, j)], self.act[(l, j)] = y, h, act
+
+    def _comb_f(self, l, j):
+        s, be = self.s, self.be
+        if self.is_attn:
+            self.y_perm[(l, j)] = be.tensor((s.tokens_per_mb * s.k, s.d))
+        self._exchange(l, j, self.y_recv.get((l, j)), self.y_perm.get((l, j)), False, self.comb_group)
+
+    def _disp_b(self, l, j):
+        s, be = self.s, self.be
+        if self.is_attn and l == self.L:
+            # zp-full loss turnaround on the attention device: final combine, loss gradient,
+            # combine backward (the reference prices this attention-side work at 0 ns).
+            r = self.route[(l, j)]
+            dh = self.out_grads[j]
+            self.dh_next[(l, j)] = dh
+            dy_perm, dw = be.combine_bwd(dh, self.y_perm[(l, j)], self.row_of[(l, j)], r)
+            self.dy_perm[(l, j)], self.dw[(l, j)] = dy_perm, dw
+        rows = self.seg[(l, j)][-1]
+        self.dy_recv[(l, j)] = dy_recv = be.tensor((max(rows, 1), s.d))
+        self._exchange(l, j, self.dy_perm.get((l, j)), dy_recv, True, self.disp_group)
+
+    def _exp_b(self, l, j):
+        st, be = self.st, self.be
+        seg = self.seg[(l, j)]
+        n = max(seg[-1], 1)
+        dx = be.ffn_bwd_acc(self.dy_recv[(l, j)][:n], self.x_recv[(l, j)][:n], self.h_save[(l, j)],
+                            self.act[(l, j)], self.seg_t[(l, j)], st.w_ug[l], st.w_d[l],
+                            st.gw_ug[l], st.gw_d[l])
+        self.dx_recv[(l, j)] = dx
+
+    def _comb_b(self, l, j):
+        s, be = self.s, self.be
+        if self.is_attn:
+            self.dx_perm[(l, j)] = be.tensor((s.tokens_per_mb * s.k, s.d))
+        self._exchange(l, j, self.dx_recv.get((l, j)), self.dx_perm.get((l, j)), False, self.comb_group)
+
+    def _attn_b(self, l, j):
+        st, be = self.st, self.be
+        r = self.route[(l, j)]
+        u = self.u[(l, j)]
+        if l not in self.wg_t:
+            self.wg_t[l] = be.transpose(st.wg[l])
+        dmoe, dwg = be.router_bwd(self.dx_perm[(l, j)], self.row_of[(l, j)], r, self.dw[(l, j)],
+                                  u.detach(), self.wg_t[l])
+        st.gwg[l] += dwg.float()
+        du = self.dh_next[(l, j)] + dmoe
+        h = self.h_in[(l, j)]
+        with torch.enable_grad():
+            torch.autograd.backward(u, du)
+        dh = h.grad
+        if l > 1:
+            self.dh_next[(l - 1, j)] = dh
+            dy_perm, dw = be.combine_bwd(dh, self.y_perm[(l - 1, j)], self.row_of[(l - 1, j)],
+                                         self.route[(l - 1, j)])
+            self.dy_perm[(l - 1, j)], self.dw[(l - 1, j)] = dy_perm, dw
+        # free the layer's activations early
+        self.u.pop((l, j), None)
+        self.h_in.pop((l, j), None)
+
+    _HANDLERS = {
+        K.ATTN_F: ("_attn_f", "compute", "attn"),
+        K.DISP_F: ("_disp_f", "dispatch", "all"),
+        K.EXP_F: ("_exp_f", "compute", "exp"),
+        K.OFF_EXP_F: ("_exp_f", "compute", "attn"),
+        K.COMB_F: ("_comb_f", "combine", "all"),
+        K.DISP_B: ("_disp_b", "dispatch", "all"),
+        K.EXP_B: ("_exp_b", "compute", "exp"),
+        K.OFF_EXP_B: ("_exp_b", "compute", "attn"),
+        K.COMB_B: ("_comb_b", "combine", "all"),
+        K.ATTN_B: ("_attn_b", "compute", "attn"),
+    }
+
+    def _participates(self, task) -> bool:
+        _, _, who = self._HANDLERS[task.kind]
+        if who == "all":
+            return True
+        if task.kind in (K.OFF_EXP_F, K.OFF_EXP_B):
+            return self.is_attn and bool(self.st.own[task.layer - 1])
+        return (who == "attn") == self.is_attn
+
+    # ------------------------------------------------------------------ iteration
+    def run(self) -> dict:
+        """One forward+backward iteration. Returns {task_id: (start_ns, end_ns)} measured on
+        this rank (relative to the iteration start event), for the tasks it took part in."""
+        self.events, marks = {}, {}
+        for name in ("u", "h_in", "route", "row_of", "x_perm", "my_counts", "counts", "send_off",
+                     "recv_pos", "seg", "seg_t", "x_recv", "y_recv", "h_save", "act", "y_perm",
+                     "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm"):
+            setattr(self, name, {})
+        self.wg_t = {}
+        for gdict in (self.st.gw_ug, self.st.gw_d, self.st.gwg):
+            for t in gdict.values():
+                t.zero_()
+        be = self.be
+        be.synchronize()
+        if dist.is_initialized():
+            dist.barrier(group=self.disp_group)  # common time origin (up to launch skew)
+        with be.on("compute"):
+            t0 = be.mark()
+        preds = {t.id: list(self.g.predecessors(t.id)) for t in self.g.tasks}
+        for task in self.issue_order:
+            if not self._participates(task):
+                continue
+            meth, lane, _ = self._HANDLERS[task.kind]
+            with be.on(lane):
+                for p in preds[task.id]:
+                    be.wait(self.events.get(p))
+                start = be.mark()
+                getattr(self, meth)(task.layer, task.microbatch)
+                end = be.mark()
+            self.events[task.id] = end
+            marks[task.id] = (start, end)
+        be.synchronize()
+        out = {tid: (be.elapsed_ns(t0, a), be.elapsed_ns(t0, b)) for tid, (a, b) in marks.items()}
+        return out
+
+
+def merge_rank_intervals(graph: TaskGraph, per_rank: list, M: int) -> Timeline:
+    """Timeline of the representative devices (the reference's one-device-per-role model,
+    ``taskgraph.py:6-7``): a task's interval on its home role spans the earliest start and the
+    latest end over that role's ranks."""
+    starts, ends = {}, {}
+    for t in graph.tasks:
+        ranks = range(0, M) if t.device == "attn" else range(M, len(per_rank))
+        iv = [per_rank[r][t.id] for r in ranks if t.id in per_rank[r]]
+        if not iv:  # e.g. a comm task whose home role had nothing to send
+            iv = [per_rank[r][t.id] for r in range(len(per_rank)) if t.id in per_rank[r]]
+        starts[t.id] = min(a for a, _ in iv)
+        ends[t.id] = max(b for _, b in iv)
+    orders = default_orders(graph)
+    return MeasuredTimeline(starts, ends, max(ends.values(), default=0),
+                            {k: list(v) for k, v in orders.items()}, per_rank=list(per_rank))
+
+
+def execute(graph: TaskGraph, executor: ZpExecutor, world_group=None) -> MeasuredTimeline:
+    """Run one iteration on every rank and return the measured Timeline (all ranks)."""
+    local = executor.run()
+    W = executor.W
+    gathered = [None] * W
+    dist.all_gather_object(gathered, local, group=world_group)
+    return merge_rank_intervals(graph, gathered, executor.M)

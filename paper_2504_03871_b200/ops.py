@@ -223,11 +223,19 @@ def router_bwd(dx_perm, row_of, r: Routing, dw, x, wg_t, want_dwg: bool = True):
 def grouped_gemm(mode: int, a, b, seg_offsets, E: int, rows: int, M: int, N: int, K: int, out,
                  ldo: int, out2=None, ldo2: int = 0, aux=None, ld_aux: int = 0,
                  max_ctas: int = 0, name: str = "grouped_gemm") -> None:
-    """One launch of the tcgen05 grouped GEMM (modes: _native.GEMM_*)."""
+    """One launch of the tcgen05 grouped GEMM (modes: _native.GEMM_*). The WGRAD modes get a
+    small device workspace for their per-expert TMA views."""
+    lib = _native.load()
+    ws = None
+    nbytes = lib.hm_grouped_gemm_workspace_bytes(mode, E)
+    if nbytes:
+        ws = torch.empty((nbytes + 128,), dtype=torch.uint8, device=a.device)
+        off = (-ws.data_ptr()) % 128
+        ws = ws[off:off + nbytes]
     _tk = _begin(name)
-    rc = _native.load().hm_grouped_gemm(
+    rc = lib.hm_grouped_gemm(
         mode, _ptr(a), _ptr(b), _ptr(seg_offsets), E, rows, M, N, K, _ptr(out), ldo, _ptr(out2),
-        ldo2, _ptr(aux), ld_aux, max_ctas, _stream(),
+        ldo2, _ptr(aux), ld_aux, _ptr(ws), max_ctas, _stream(),
     )
     _end(_tk)
     _native.check(rc, "hm_grouped_gemm")
@@ -274,6 +282,28 @@ def grouped_ffn_bwd(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: i
     grouped_gemm(_native.GEMM_WGRAD, dy_perm, act, seg_offsets, E, rows, d, f, 0, dw_d, f,
                  max_ctas=max_ctas, name="gemm_wgrad_down")
     return dx_perm, dw_ug, dw_d
+
+
+def grouped_ffn_bwd_acc(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, gw_ug, gw_d,
+                        max_ctas: int = 0):
+    """Backward with fp32 weight-gradient ACCUMULATION (gw_ug [E,2f,d], gw_d [E,d,f] fp32 +=),
+    used when gradients accumulate over micro-batches. Returns dx_perm."""
+    _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, gw_ug, gw_d)
+    rows, d = x_perm.shape
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    dev = x_perm.device
+    dh = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=dev)
+    dx_perm = torch.empty((rows, d), dtype=x_perm.dtype, device=dev)
+    grouped_gemm(_native.GEMM_BWD_DACT, dy_perm, w_d, seg_offsets, E, rows, 0, f, d, dh, 2 * f,
+                 aux=h, ld_aux=2 * f, max_ctas=max_ctas, name="gemm_bwd_dact")
+    grouped_gemm(_native.GEMM_BWD_DX, dh, w_ug, seg_offsets, E, rows, 0, d, 2 * f, dx_perm, d,
+                 max_ctas=max_ctas, name="gemm_bwd_dx")
+    grouped_gemm(_native.GEMM_WGRAD_ACC, dh, x_perm, seg_offsets, E, rows, 2 * f, d, 0, gw_ug, d,
+                 max_ctas=max_ctas, name="gemm_wgrad_ug")
+    grouped_gemm(_native.GEMM_WGRAD_ACC, dy_perm, act, seg_offsets, E, rows, d, f, 0, gw_d, f,
+                 max_ctas=max_ctas, name="gemm_wgrad_down")
+    return dx_perm
 
 
 # ---------------------------------------------------------------------------------------------

@@ -56,3 +56,21 @@ def plan_assignment(spec: Spec, durations: TaskDurations) -> ExpertAssignment:
     if spec.run.asym_ea:
         return scheduler.asym_ea_offload(offload_inputs(spec, durations)).assignment
     return ExpertAssignment.zeros(spec.model.layers)
+
+
+def make_zp_spec(M: int, N: int, layers: int, microbatches: int, experts: int, top_k: int,
+                 tokens_per_mb: int, hidden: int, attn_fwd_ns: int, expert_layer_fwd_ns: int,
+                 single_expert_fwd_ns: int, dispatch_ns: int = 0, combine_ns: int = 0,
+                 gamma=Fraction(2), asym_ea: bool = False, squeeze: str = "verbatim",
+                 expert_mem: int = 0, attn_capacity: int = 10**12, exp_capacity: int = 10**12) -> Spec:
+    """Spec with a duration table (measured B200 times enter here, costmodel.py:88-104)."""
+    from .core import GpuClass, HardwareProfile, ModelSpec, RunOptions, ZpGroupSpec
+
+    a = GpuClass("b200-attention", attn_capacity)
+    e = GpuClass("b200-expert", exp_capacity)
+    prof = HardwareProfile(a, e, {"attn_fwd": int(attn_fwd_ns), "single_expert_fwd": int(single_expert_fwd_ns)},
+                           {"expert_layer_fwd": int(expert_layer_fwd_ns)},
+                           {"dispatch": int(dispatch_ns), "combine": int(combine_ns)})
+    model = ModelSpec(layers, experts, top_k, hidden, tokens_per_mb, microbatches, 1, expert_mem, 0)
+    return Spec(ZpGroupSpec(M, N, a, e, 900 * 10**9, 2 * hidden), model, prof,
+                RunOptions(mode="zp-full", gamma=Fraction(gamma), asym_ea=asym_ea, squeeze=squeeze))

@@ -1,0 +1,174 @@
+"""Multi-process (gloo, CPU) tests of the ZP executor's host logic: placement, stream-order
+walk, count exchange and the attention<->expert send/recv choreography, against a
+single-process fp32 reference of the same L-layer MoE stack."""
+
+import os
+import socket
+import sys
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _build(M, N, L, R, E, k, T, d, f, offload):
+    from paper_2504_03871_b200 import ExpertAssignment, build_zp_graph, derive_task_durations
+    from paper_2504_03871_b200.planner import make_zp_spec
+
+    spec = make_zp_spec(M, N, L, R, E, k, T, d, attn_fwd_ns=3000, expert_layer_fwd_ns=4000,
+                        single_expert_fwd_ns=3000, dispatch_ns=100, combine_ns=100)
+    dur = derive_task_durations(spec)
+    return build_zp_graph(spec, dur, ExpertAssignment(tuple(offload)), mode="zp-full")
+
+
+def _worker(rank, W, M, N, args, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=W)
+    try:
+        from cpu_backend import CpuBackend
+        from paper_2504_03871_b200.executor import ZpExecutor, ZpLayerShape, execute
+        from paper_2504_03871_b200 import validate_timeline
+        from paper_2504_03871_b200.simulator import validate_measured_timeline
+
+        L, R, E, k, T, d, f, offload, attention = args
+        g = _build(M, N, L, R, E, k, T, d, f, offload)
+        shape = ZpLayerShape(E, k, d, f, T, heads=2, attention=attention)
+        disp = dist.new_group(list(range(W)))
+        comb = dist.new_group(list(range(W)))
+        ex = ZpExecutor(g, shape, M, N, rank, CpuBackend(), disp, comb, seed=3)
+        tl = execute(g, ex)
+        out = {
+            "rank": rank,
+            "own": ex.st.own,
+            "gw_ug": {l: v.clone() for l, v in ex.st.gw_ug.items()},
+            "gw_d": {l: v.clone() for l, v in ex.st.gw_d.items()},
+            "gwg": {l: v.clone() for l, v in ex.st.gwg.items()},
+            "gwqkv": {l: ex.st.wqkv[l].grad.clone() for l in ex.st.wqkv if ex.st.wqkv[l].grad is not None},
+            "measured_violations": validate_measured_timeline(g, tl) if rank == 0 else None,
+            "makespan": tl.makespan,
+        }
+        q.put(out)
+    except Exception as exc:  # report instead of hanging the parent
+        import traceback
+
+        q.put({"rank": rank, "error": traceback.format_exc()})
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _reference(M, N, args):
+    """Single-process fp32 reference of the whole iteration (all attention ranks' batches)."""
+    sys.path.insert(0, HERE)
+    from cpu_backend import CpuBackend
+    from paper_2504_03871_b200.executor import attention_block
+
+    L, R, E, k, T, d, f, offload, attention = args
+    be = CpuBackend()
+    gen = torch.Generator().manual_seed(3)
+    rand = lambda shape, std: (torch.randn(shape, generator=gen) * std)  # noqa: E731
+    P = []
+    for _ in range(L):
+        P.append(dict(wqkv=rand((d, 3 * d), d ** -0.5).requires_grad_(), wo=rand((d, d), d ** -0.5).requires_grad_(),
+                      wg=rand((d, E), d ** -0.5).requires_grad_(), w_ug=rand((E, 2 * f, d), d ** -0.5).requires_grad_(),
+                      w_d=rand((E, d, f), f ** -0.5).requires_grad_()))
+    for a in range(M):
+        g2 = torch.Generator().manual_seed(3 * 7919 + 17 + a)
+        for _ in range(R):
+            x = torch.randn((T, d), generator=g2)
+            gout = torch.randn((T, d), generator=g2)
+            h = x
+            for l in range(L):
+                p = P[l]
+                u = attention_block(h, p["wqkv"], p["wo"], 2) if attention else h * 1
+                with torch.no_grad():
+                    r = be.router(u, p["wg"], k)
+                logits = u @ p["wg"]
+                w = torch.softmax(torch.gather(logits, 1, r.idx.long()), 1)
+                wgt, wut = CpuBackend._split(p["w_ug"])
+                y = torch.zeros_like(u)
+                for s in range(k):
+                    for e in range(E):
+                        m = r.idx[:, s].long() == e
+                        if m.any():
+                            ue = u[m]
+                            ye = (torch.nn.functional.silu(ue @ wgt[e].t()) * (ue @ wut[e].t())) @ p["w_d"][e].t()
+                            y = y.index_add(0, m.nonzero()[:, 0], w[m, s:s + 1] * ye)
+                h = u + y
+            (h * gout).sum().backward()
+    return P
+
+
+def _close(a, b, tol=1e-4):
+    err = (torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(b)).item()
+    assert err < tol, f"relative error {err:.3e}"
+
+
+@pytest.mark.parametrize("M,N,offload,attention", [
+    (1, 1, (0, 0), True),
+    (1, 1, (0, 2), False),
+    (2, 2, (1, 0), True),
+    (1, 2, (0, 1), False),
+])
+def test_executor_matches_single_process_reference(M, N, offload, attention):
+    L, R, E, k, T, d, f = 2, 2, 4, 2, 16, 256, 128
+    args = (L, R, E, k, T, d, f, list(offload), attention)
+    W = M + N
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, W, M, N, args, port, q)) for r in range(W)]
+    for p in procs:
+        p.start()
+    outs = []
+    for _ in range(W):
+        o = q.get(timeout=240)
+        assert "error" not in o, o.get("error")
+        outs.append(o)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    outs.sort(key=lambda o: o["rank"])
+    P = _reference(M, N, args)
+    assert outs[0]["measured_violations"] == []
+    for l in range(1, L + 1):
+        p = P[l - 1]
+        wgt, wut = None, None
+        g_ug = torch.zeros_like(p["w_ug"])
+        g_d = torch.zeros_like(p["w_d"])
+        for o in outs:
+            own = o["own"][l - 1]
+            if own:
+                g_ug[own] += o["gw_ug"][l]
+                g_d[own] += o["gw_d"][l]
+        _close(g_ug, p["w_ug"].grad)
+        _close(g_d, p["w_d"].grad)
+        gwg = sum(o["gwg"][l] for o in outs if l in o["gwg"])
+        _close(gwg, p["wg"].grad)
+        if attention:
+            gq = sum(o["gwqkv"][l] for o in outs if l in o["gwqkv"])
+            _close(gq, p["wqkv"].grad)
+
+
+def test_expert_owners_reproduce_offload_shares():
+    from paper_2504_03871_b200.executor import expert_owners
+
+    assert expert_owners(8, 4, 4, 0) == [4, 4, 5, 5, 6, 6, 7, 7]
+    assert expert_owners(8, 4, 4, 1) == [4, 0, 5, 1, 6, 2, 7, 3]
+    assert expert_owners(8, 2, 4, 1) == [2, 0, 3, 0, 4, 1, 5, 1]
+    # M=4, N=2 (n2 = 2): each expert rank gives 2, each attention rank gets 1
+    assert expert_owners(8, 4, 2, 2) == [4, 4, 0, 1, 5, 5, 2, 3]

@@ -137,6 +137,18 @@ def test_grouped_ffn_vs_fp32(segs, df):
     assert orc.rel_err(dg, wgr.grad) < TOL_W
     assert orc.rel_err(du, wur.grad) < TOL_W
     assert orc.rel_err(dw_d, wdr.grad) < TOL_W
+    # fp32 accumulation variant: two accumulations of the same micro-batch = 2x the gradient
+    gw_ug = torch.zeros(w_ug.shape, dtype=torch.float32, device="cuda")
+    gw_d = torch.zeros(w_down.shape, dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        dx2 = ops.grouped_ffn_bwd_acc(dy.cuda(), x_perm.cuda(), h, act, seg, w_ug.cuda(),
+                                      w_down.cuda(), gw_ug, gw_d)
+    torch.cuda.synchronize()
+    assert torch.equal(dx2.cpu(), dx.cpu())
+    ag, au = ops.split_gate_up(gw_ug.cpu())
+    assert orc.rel_err(ag, 2 * wgr.grad) < TOL_W
+    assert orc.rel_err(au, 2 * wur.grad) < TOL_W
+    assert orc.rel_err(gw_d, 2 * wdr.grad) < TOL_W
 
 
 @pytest.mark.parametrize("cfg", [with_tokens(C1, 1024), LayerConfig("c3ish", 16, 4, 512, 384, 700)],

@@ -67,6 +67,65 @@ def router_logits(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
     return acc[:, 0, :].copy()
 
 
+_CLIB = None
+
+
+def _clib():
+    """oracle/librouter_ref.so (C restatement, built by `make -C oracle`), or None."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librouter_ref.so")
+        if os.path.exists(p):
+            lib = ctypes.CDLL(p)
+            P, I = ctypes.c_void_p, ctypes.c_int
+            lib.hm_ref_router_logits.argtypes = [P, P, I, I, I, P]
+            lib.hm_ref_topk_softmax.argtypes = [P, I, I, I, P, P]
+            lib.hm_ref_permutation.argtypes = [P, I, I, I, P, P, P, P]
+            _CLIB = lib
+        else:
+            _CLIB = False
+    return _CLIB or None
+
+
+def router_logits_c(x_bf16: torch.Tensor, wg_bf16: torch.Tensor) -> np.ndarray:
+    """Same fixed-order logits as ``router_logits`` from the C restatement (fast, any size)."""
+    lib = _clib()
+    if lib is None:
+        return router_logits(x_bf16.float().numpy(), wg_bf16.float().numpy())
+    x = x_bf16.contiguous().view(torch.int16).numpy()
+    w = wg_bf16.contiguous().view(torch.int16).numpy()
+    T, d = x.shape
+    E = w.shape[1]
+    out = np.empty((T, E), dtype=np.float32)
+    lib.hm_ref_router_logits(x.ctypes.data, w.ctypes.data, T, d, E, out.ctypes.data)
+    return out
+
+
+def route_c(x_bf16: torch.Tensor, wg_bf16: torch.Tensor, k: int) -> "RoutingRef":
+    """``route`` with the C restatement doing the heavy loops (for full-size parity checks)."""
+    logits = router_logits_c(x_bf16, wg_bf16)
+    lib = _clib()
+    T, E = logits.shape
+    if lib is None:
+        idx, w = topk_softmax(logits, k)
+        counts, offsets = counts_offsets(idx, E)
+        row_src, row_of = permutation(idx, E)
+        return RoutingRef(logits, idx, w, counts, offsets, row_src, row_of)
+    idx = np.empty((T, k), dtype=np.int32)
+    w = np.empty((T, k), dtype=np.float32)
+    lib.hm_ref_topk_softmax(logits.ctypes.data, T, E, k, idx.ctypes.data, w.ctypes.data)
+    counts = np.empty(E, dtype=np.int32)
+    offsets = np.empty(E + 1, dtype=np.int32)
+    row_src = np.empty(T * k, dtype=np.int32)
+    row_of = np.empty((T, k), dtype=np.int32)
+    lib.hm_ref_permutation(idx.ctypes.data, T, k, E, counts.ctypes.data, offsets.ctypes.data,
+                           row_src.ctypes.data, row_of.ctypes.data)
+    return RoutingRef(logits, idx, w, counts, offsets, row_src, row_of)
+
+
 def topk_softmax(logits: np.ndarray, k: int):
     """Top-k with ties -> lower expert id; w = softmax over the selected logits (fp32)."""
     T, E = logits.shape

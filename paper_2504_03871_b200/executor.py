@@ -168,9 +168,9 @@ def attention_block(h, wqkv, wo, heads: int):
     flash attention; not one of the four hot-path kernels)."""
     T, d = h.shape
     hd = d // heads
-    qkv = (h @ wqkv).view(T, 3, heads, hd).permute(1, 2, 0, 3)
+    qkv = (h @ wqkv).view(1, T, 3, heads, hd).permute(2, 0, 3, 1, 4)  # [3, 1, H, T, hd]
     o = torch.nn.functional.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True)
-    return h + o.permute(1, 0, 2).reshape(T, d) @ wo
+    return h + o[0].permute(1, 0, 2).reshape(T, d) @ wo
 
 
 @dataclass

@@ -99,3 +99,20 @@ def test_oracle_layer_gradients_match_finite_differences():
     fd = ((yp - ym) * inp.dy.float()).sum() / 2
     an = (out["dx"] * v).sum()
     assert abs(fd - an) / abs(an) < 1e-2
+
+
+def test_c_restatement_matches_numpy_oracle():
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", os.path.join(root, "oracle")], check=True, capture_output=True)
+    assert orc._clib() is not None
+    for cfg in (LayerConfig("c", 8, 2, 512, 128, 333), LayerConfig("c3", 64, 6, 1024, 128, 200)):
+        inp = make_inputs(cfg, seed=12)
+        a = orc.route(inp.x.float().numpy(), inp.wg.float().numpy(), cfg.k)
+        b = orc.route_c(inp.x, inp.wg, cfg.k)
+        assert np.array_equal(a.logits.view(np.uint32), b.logits.view(np.uint32))
+        for f in ("idx", "counts", "offsets", "row_src", "row_of"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+        assert np.abs(a.w - b.w).max() < 1e-6

@@ -4,6 +4,7 @@
 // (cuTensorMapEncodeTiled through the runtime's driver entry point; no -lcuda), grid sizing
 // and launches on the caller's stream. No allocation, no synchronisation.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -27,8 +28,20 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("HM_DEBUG_SYNC");
+    v = (s && atoi(s) != 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// HM_DEBUG_SYNC=1: synchronise the device after every launch so a fault is attributed to the
+// kernel that caused it (debugging only; the default path never synchronises)
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug_sync()) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(static_cast<int>(e), "%s: %s", what, cudaGetErrorString(e));
   return 0;
 }

@@ -220,11 +220,12 @@ class ZpExecutor:
 
     def _init_params(self, seed: int) -> None:
         s, be, st = self.s, self.be, self.st
-        gen = torch.Generator().manual_seed(seed)
+        # parameters come from one global seed, generated on the backend's device type, so
+        # every rank draws the identical sequence and keeps its own slice
+        gen = torch.Generator(device=be.device).manual_seed(seed)
 
         def rand(shape, std):
-            # parameters are generated on the CPU from one global seed so every rank agrees
-            return (torch.randn(shape, generator=gen) * std).to(be.dtype)
+            return (torch.randn(shape, generator=gen, device=be.device) * std).to(be.dtype)
 
         for l in range(1, self.L + 1):
             wqkv = rand((s.d, 3 * s.d), s.d ** -0.5)
@@ -239,7 +240,7 @@ class ZpExecutor:
                 st.gwg[l] = torch.zeros((s.d, s.E), dtype=torch.float32, device=be.device)
             own = st.own[l - 1]
             if own:
-                idx = torch.tensor(own)
+                idx = torch.tensor(own, device=be.device)
                 st.w_ug[l] = w_ug_all[idx].contiguous().to(be.device)
                 st.w_d[l] = w_d_all[idx].contiguous().to(be.device)
                 st.gw_ug[l] = torch.zeros(st.w_ug[l].shape, dtype=torch.float32, device=be.device)
@@ -247,10 +248,10 @@ class ZpExecutor:
         # synthetic inputs / output gradient per micro-batch (attention ranks)
         self.inputs, self.out_grads = {}, {}
         if self.is_attn:
-            g2 = torch.Generator().manual_seed(seed * 7919 + 17 + self.rank)
+            g2 = torch.Generator(device=be.device).manual_seed(seed * 7919 + 17 + self.rank)
             for j in range(1, self.R + 1):
-                self.inputs[j] = torch.randn((s.tokens_per_mb, s.d), generator=g2).to(be.dtype).to(be.device)
-                self.out_grads[j] = torch.randn((s.tokens_per_mb, s.d), generator=g2).to(be.dtype).to(be.device)
+                self.inputs[j] = torch.randn((s.tokens_per_mb, s.d), generator=g2, device=be.device).to(be.dtype)
+                self.out_grads[j] = torch.randn((s.tokens_per_mb, s.d), generator=g2, device=be.device).to(be.dtype)
 
     # ------------------------------------------------------------------ helpers
     def _ev(self, key):

@@ -48,13 +48,21 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
 #pragma unroll
       for (int e = 0; e < EG; ++e) acc[a][e] = 0.f;
 
+    // x rows are streamed with one 16-byte load per token per j, prefetched one j ahead
+    uint4 xv[TT], xn[TT];
+#pragma unroll
+    for (int a = 0; a < TT; ++a) {
+      const int t = min(t0 + a, T - 1);
+      xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + lane * 8));
+    }
     for (int j = 0; j < nj; ++j) {
       const int ibase = j * 256 + lane * 8;
-      uint4 xv[TT];
+      if (j + 1 < nj) {
 #pragma unroll
-      for (int a = 0; a < TT; ++a) {
-        const int t = min(t0 + a, T - 1);
-        xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase));
+        for (int a = 0; a < TT; ++a) {
+          const int t = min(t0 + a, T - 1);
+          xn[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase + 256));
+        }
       }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -74,6 +82,8 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
           for (int e = 0; e < EG; ++e) acc[a][e] = __fmaf_rn(xf, wv[e], acc[a][e]);
         }
       }
+#pragma unroll
+      for (int a = 0; a < TT; ++a) xv[a] = xn[a];
     }
     // xor butterfly across lanes (fixed order 16, 8, 4, 2, 1)
 #pragma unroll
@@ -104,7 +114,7 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
 // ------------------------------------------------------------------------------------------
 // K1b: top-k + softmax + per-chunk expert histogram. One CTA per chunk of kChunk tokens,
 // one warp per token (looping). E <= 256.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     router_topk_kernel(const float* __restrict__ logits, int T, int E, int k,
                        int32_t* __restrict__ idx, float* __restrict__ w,
                        int32_t* __restrict__ chunk_counts /*[nchunk][E]*/) {
@@ -115,7 +125,8 @@ __global__ void __launch_bounds__(256)
   const int c = blockIdx.x;
   const int tbeg = c * kChunk, tend = min(T, tbeg + kChunk);
   constexpr int kPer = 8;  // values per lane (E <= 256)
-  for (int t = tbeg + warp; t < tend; t += 8) {
+  const int nwarps = blockDim.x >> 5;
+  for (int t = tbeg + warp; t < tend; t += nwarps) {
     float v[kPer];
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -138,6 +149,12 @@ __global__ void __launch_bounds__(256)
         const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
         const int oe = __shfl_xor_sync(0xffffffffu, be, off);
         if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+      }
+      if (be == 0x7fffffff) {
+        // every remaining logit is NaN: take the lowest unselected expert so indices stay valid
+        be = 0;
+        for (int p = 0; p < s; ++p)
+          if (sel_e[p] == be) { ++be; p = -1; }
       }
       sel_l[s] = bv;
       sel_e[s] = be;
@@ -194,6 +211,25 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x == 0) offsets[E] = off[E];
 }
 
+// Stable destination rows of one chunk: warp w handles experts w, w+8, ...; for each expert it
+// scans the chunk's (token, slot) entries 32 at a time with a ballot, so entry i of expert e
+// gets row base[e] + #(earlier entries of e). Tokens hold distinct experts, so entry order ==
+// token order within an expert.
+HM_DEV void assign_rows_ballot(const int* s_idx, int* s_row, const int32_t* base, int n, int E) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  for (int e = warp; e < E; e += nwarps) {
+    int r = base[e];
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const int i = i0 + lane;
+      const bool hit = (i < n) && (s_idx[i] == e);
+      const uint32_t m = __ballot_sync(0xffffffffu, hit);
+      if (hit) s_row[i] = r + __popc(m & ((1u << lane) - 1u));
+      r += __popc(m);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // K2: dispatch permute. One CTA per chunk: (1) thread e walks the chunk's tokens in order and
 // assigns destination rows for expert e (stable), (2) warps copy token rows with 128-bit loads
@@ -211,11 +247,7 @@ __global__ void __launch_bounds__(256)
   const int nt = min(kChunk, T - tbeg);
   for (int i = threadIdx.x; i < nt * k; i += blockDim.x) s_idx[i] = idx[static_cast<long>(tbeg) * k + i];
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int r = chunk_base[static_cast<long>(c) * E + e];
-    for (int i = 0; i < nt * k; ++i)
-      if (s_idx[i] == e) s_row[i] = r++;
-  }
+  assign_rows_ballot(s_idx, s_row, chunk_base + static_cast<long>(c) * E, nt * k, E);
   __syncthreads();
   for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
     const int r = s_row[i];
@@ -252,11 +284,7 @@ __global__ void __launch_bounds__(256)
   const int nt = min(kChunk, T - tbeg);
   for (int i = threadIdx.x; i < nt * k; i += blockDim.x) s_idx[i] = idx[static_cast<long>(tbeg) * k + i];
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int r = chunk_base[static_cast<long>(c) * E + e];
-    for (int i = 0; i < nt * k; ++i)
-      if (s_idx[i] == e) s_row[i] = r++;
-  }
+  assign_rows_ballot(s_idx, s_row, chunk_base + static_cast<long>(c) * E, nt * k, E);
   __syncthreads();
   for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
     const int r = s_row[i];

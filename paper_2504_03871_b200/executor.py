@@ -36,6 +36,7 @@ from __future__ import annotations
 
 import contextlib
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -439,6 +440,19 @@ class ZpExecutor:
             return self.is_attn and bool(self.st.own[task.layer - 1])
         return (who == "attn") == self.is_attn
 
+    def _debug_check(self, task) -> None:
+        """HM_ZP_DEBUG=1: synchronise after every task and check its outputs are finite."""
+        self.be.synchronize()
+        key = (task.layer, task.microbatch)
+        for name in ("u", "x_perm", "x_recv", "y_recv", "y_perm", "dy_perm", "dy_recv", "dx_recv", "dx_perm"):
+            t = getattr(self, name).get(key)
+            if t is not None and t.numel() and not bool(torch.isfinite(t.float()).all()):
+                raise FloatingPointError(f"rank {self.rank}: non-finite {name} after {task.kind.value} "
+                                         f"L{task.layer} M{task.microbatch}")
+        r = self.route.get(key)
+        if r is not None and (int(r.idx.min()) < 0 or int(r.idx.max()) >= self.s.E):
+            raise IndexError(f"rank {self.rank}: router index out of range at L{task.layer} M{task.microbatch}")
+
     # ------------------------------------------------------------------ iteration
     def run(self) -> dict:
         """One forward+backward iteration. Returns {task_id: (start_ns, end_ns)} measured on
@@ -459,6 +473,7 @@ class ZpExecutor:
         with be.on("compute"):
             t0 = be.mark()
         preds = {t.id: list(self.g.predecessors(t.id)) for t in self.g.tasks}
+        debug = os.environ.get("HM_ZP_DEBUG") == "1"
         for task in self.issue_order:
             if not self._participates(task):
                 continue
@@ -469,6 +484,8 @@ class ZpExecutor:
                 start = be.mark()
                 getattr(self, meth)(task.layer, task.microbatch)
                 end = be.mark()
+            if debug:
+                self._debug_check(task)
             self.events[task.id] = end
             marks[task.id] = (start, end)
         be.synchronize()

@@ -164,12 +164,16 @@ class NativeBackend:
 # per-rank model state
 
 
+def rms_norm(x):
+    return torch.nn.functional.rms_norm(x, (x.shape[-1],), eps=1e-6)
+
+
 def attention_block(h, wqkv, wo, heads: int):
-    """u = h + Attn(h): fused QKV projection, causal SDPA, output projection (torch/cuBLAS/
-    flash attention; not one of the four hot-path kernels)."""
+    """u = h + Attn(RMSNorm(h)): fused QKV projection, causal SDPA, output projection (torch /
+    cuBLAS / flash attention; not one of the four hot-path kernels). Pre-norm, as in Mixtral."""
     T, d = h.shape
     hd = d // heads
-    qkv = (h @ wqkv).view(1, T, 3, heads, hd).permute(2, 0, 3, 1, 4)  # [3, 1, H, T, hd]
+    qkv = (rms_norm(h) @ wqkv).view(1, T, 3, heads, hd).permute(2, 0, 3, 1, 4)  # [3, 1, H, T, hd]
     o = torch.nn.functional.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True)
     return h + o[0].permute(1, 0, 2).reshape(T, d) @ wo
 
@@ -327,10 +331,12 @@ class ZpExecutor:
         self.h_in[(l, j)] = h
         with torch.enable_grad():
             u = attention_block(h, st.wqkv[l], st.wo[l], self.heads) if s.attention else h * 1
+            z = rms_norm(u)  # pre-norm MoE input
         self.u[(l, j)] = u
-        ud = u.detach()
-        r = be.router(ud, st.wg[l], s.k)
-        x_perm, row_of = be.permute(ud, r)
+        self.z[(l, j)] = z
+        zd = z.detach()
+        r = be.router(zd, st.wg[l], s.k)
+        x_perm, row_of = be.permute(zd, r)
         self.route[(l, j)], self.row_of[(l, j)], self.x_perm[(l, j)] = r, row_of, x_perm
         self.my_counts[(l, j)] = be.counts(r)
 
@@ -399,16 +405,16 @@ class ZpExecutor:
     def _attn_b(self, l, j):
         st, be = self.st, self.be
         r = self.route[(l, j)]
-        u = self.u[(l, j)]
+        u, z = self.u[(l, j)], self.z[(l, j)]
         if l not in self.wg_t:
             self.wg_t[l] = be.transpose(st.wg[l])
-        dmoe, dwg = be.router_bwd(self.dx_perm[(l, j)], self.row_of[(l, j)], r, self.dw[(l, j)],
-                                  u.detach(), self.wg_t[l])
+        dz, dwg = be.router_bwd(self.dx_perm[(l, j)], self.row_of[(l, j)], r, self.dw[(l, j)],
+                                z.detach(), self.wg_t[l])
         st.gwg[l] += dwg.float()
-        du = self.dh_next[(l, j)] + dmoe
         h = self.h_in[(l, j)]
         with torch.enable_grad():
-            torch.autograd.backward(u, du)
+            # residual path (dh_next into u) + MoE path (dz through the pre-norm)
+            torch.autograd.backward([u, z], [self.dh_next[(l, j)], dz.to(z.dtype)])
         dh = h.grad
         if l > 1:
             self.dh_next[(l - 1, j)] = dh
@@ -417,6 +423,7 @@ class ZpExecutor:
             self.dy_perm[(l - 1, j)], self.dw[(l - 1, j)] = dy_perm, dw
         # free the layer's activations early
         self.u.pop((l, j), None)
+        self.z.pop((l, j), None)
         self.h_in.pop((l, j), None)
 
     _HANDLERS = {
@@ -458,7 +465,7 @@ class ZpExecutor:
         """One forward+backward iteration. Returns {task_id: (start_ns, end_ns)} measured on
         this rank (relative to the iteration start event), for the tasks it took part in."""
         self.events, marks = {}, {}
-        for name in ("u", "h_in", "route", "row_of", "x_perm", "my_counts", "counts", "send_off",
+        for name in ("u", "z", "h_in", "route", "row_of", "x_perm", "my_counts", "counts", "send_off",
                      "recv_pos", "seg", "seg_t", "x_recv", "y_recv", "h_save", "act", "y_perm",
                      "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm"):
             setattr(self, name, {})

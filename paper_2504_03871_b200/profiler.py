@@ -36,7 +36,7 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
                       device="cuda", seed: int = 0) -> dict:
     """Duration table (ns) for ``planner.make_zp_spec`` measured with the native kernels."""
     from . import ops
-    from .executor import attention_block
+    from .executor import attention_block, rms_norm
 
     dev = torch.device(device)
     g = torch.Generator(device=dev).manual_seed(seed)
@@ -51,8 +51,9 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
 
     def attn_step():
         u = attention_block(x, wqkv, wo, heads) if shape.attention else x
-        r = ops.router_topk(u, wg, k)
-        ops.dispatch_permute(u, r)
+        z = rms_norm(u)
+        r = ops.router_topk(z, wg, k)
+        ops.dispatch_permute(z, r)
 
     attn_ms = _time_ms(attn_step)
 

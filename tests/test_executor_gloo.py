@@ -75,7 +75,7 @@ def _reference(M, N, args):
     """Single-process fp32 reference of the whole iteration (all attention ranks' batches)."""
     sys.path.insert(0, HERE)
     from cpu_backend import CpuBackend
-    from paper_2504_03871_b200.executor import attention_block
+    from paper_2504_03871_b200.executor import attention_block, rms_norm
 
     L, R, E, k, T, d, f, offload, attention = args
     be = CpuBackend()
@@ -95,9 +95,10 @@ def _reference(M, N, args):
             for l in range(L):
                 p = P[l]
                 u = attention_block(h, p["wqkv"], p["wo"], 2) if attention else h * 1
+                z = rms_norm(u)
                 with torch.no_grad():
-                    r = be.router(u, p["wg"], k)
-                logits = u @ p["wg"]
+                    r = be.router(z, p["wg"], k)
+                logits = z @ p["wg"]
                 w = torch.softmax(torch.gather(logits, 1, r.idx.long()), 1)
                 wgt, wut = CpuBackend._split(p["w_ug"])
                 y = torch.zeros_like(u)
@@ -105,7 +106,7 @@ def _reference(M, N, args):
                     for e in range(E):
                         m = r.idx[:, s].long() == e
                         if m.any():
-                            ue = u[m]
+                            ue = z[m]
                             ye = (torch.nn.functional.silu(ue @ wgt[e].t()) * (ue @ wut[e].t())) @ p["w_d"][e].t()
                             y = y.index_add(0, m.nonzero()[:, 0], w[m, s:s + 1] * ye)
                 h = u + y

@@ -392,6 +392,18 @@ def run_zp(args, ws, rank, local):
         return
     met = compute_metrics(graph, tl, tokens_per_iteration=tokens_iter)
     viol = validate_measured_timeline(graph, tl)
+    # measured mean duration per task kind on its home role vs the profiled (simulated) one
+    kinds = {}
+    for t in graph.tasks:
+        ranks = range(0, M) if t.device == "attn" else range(M, ws)
+        ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in ranks if t.id in tl.per_rank[r]]
+        if ds:
+            k_ = kinds.setdefault(t.kind.value, [0.0, 0.0, 0])
+            k_[0] += sum(ds) / len(ds)
+            k_[1] += t.duration
+            k_[2] += 1
+    task_ms = {k: {"measured_ms": round(v[0] / v[2] / 1e6, 3), "simulated_ms": round(v[1] / v[2] / 1e6, 3)}
+               for k, v in sorted(kinds.items())}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
@@ -414,6 +426,7 @@ def run_zp(args, ws, rank, local):
             "attn_utilization": float(met.devices["attn"].utilization_of_makespan),
             "exp_utilization": float(met.devices["exp"].utilization_of_makespan),
             "timeline_violations": len(viol),
+            "task_durations": task_ms,
         },
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -42,14 +42,16 @@ constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 // CTAS = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (UMMA M=256):
 //           each CTA stages its own 128 rows of A and half (128 columns) of B, the leader CTA
 //           issues the MMAs, each CTA's TMEM receives its 128 accumulator rows.
+constexpr int kBookkeepingBytes = 3072;  // GemmShared, placed first; tiles start 1024-aligned
+
 template <int CTAS>
 struct TileCfg {
   static constexpr int kTileM = kBM * CTAS;           // output rows per (cluster) tile
   static constexpr int kBRows = kBN / CTAS;           // B rows (N) staged per CTA
   static constexpr int kBTileBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CTAS == 1 ? 4 : 6;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align slack*/ + 4096 /*bookkeeping*/;
+  static constexpr int kStages = CTAS == 1 ? 4 : 7;
+  static constexpr int kSmemBytes = kBookkeepingBytes + kStages * kStageBytes;
 };
 constexpr int kGemmSmemBytes = TileCfg<1>::kSmemBytes;
 
@@ -179,8 +181,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kStageBytes = Cfg::kStageBytes;
   constexpr int kTileM = Cfg::kTileM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  GemmShared& sh = *reinterpret_cast<GemmShared*>(tiles + kStages * kStageBytes);
+  static_assert(sizeof(GemmShared) <= kBookkeepingBytes, "bookkeeping overflows its slot");
+  // the dynamic shared window starts 1024-aligned (no static shared memory in this kernel);
+  // 128-byte swizzled TMA tiles need that alignment
+  if ((smem_u32(smem_raw) & 1023u) != 0u) __trap();
+  GemmShared& sh = *reinterpret_cast<GemmShared*>(smem_raw);
+  uint8_t* tiles = smem_raw + kBookkeepingBytes;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -232,7 +238,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ======================= TMA producer (both CTAs of a pair) =======================
     if (lane == 0) {
-      const uint64_t pol = policy_evict_normal();
+      // raster n-fastest re-reads B across the inner loop (keep B, stream A); m-fastest keeps A
+      const uint64_t pol_keep = policy_evict_last();
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_a = p.n_fastest ? pol_stream : pol_keep;
+      const uint64_t pol_b = p.n_fastest ? pol_keep : pol_stream;
       uint32_t it = 0;
       int mapped_e = -1;
       for (int tile = tile0; tile < total_tiles; tile += tile_step) {
@@ -272,25 +282,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (!GROUP_K) {
             // A: activation rows [seg0 + m0, +128), K-major box {64, 128}
-            tma_load_2d_any<CTAS>(sa, mA, bar, kb * kBK, seg0 + m0, pol);
+            tma_load_2d_any<CTAS>(sa, mA, bar, kb * kBK, seg0 + m0, pol_a);
             if (!B_MN) {
               // B: W[e] stored [N][K]; box {64, kBRows}
-              tma_load_3d_any<CTAS>(sb, mB, bar, kb * kBK, n0, tc.e, pol);
+              tma_load_3d_any<CTAS>(sb, mB, bar, kb * kBK, n0, tc.e, pol_b);
             } else {
               // B: W[e] stored [K][N]; 64-wide N panels, box {64 (N), 64 (K)}
 #pragma unroll
               for (int q = 0; q < Cfg::kBRows / 64; ++q)
-                tma_load_3d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, tc.e, pol);
+                tma_load_3d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, tc.e, pol_b);
             }
           } else {
             // wgrad: both operands are the expert's [rows = K][cols] activations (MN-major),
             // box {64, 64}; rows past the expert's end are zero-filled by TMA
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-              tma_load_2d_any<CTAS>(sa + q * 8192, mA, bar, m0 + q * 64, kb * kBK, pol);
+              tma_load_2d_any<CTAS>(sa + q * 8192, mA, bar, m0 + q * 64, kb * kBK, pol_a);
 #pragma unroll
             for (int q = 0; q < Cfg::kBRows / 64; ++q)
-              tma_load_2d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, pol);
+              tma_load_2d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, pol_b);
           }
         }
       }

@@ -356,7 +356,8 @@ def run_zp(args, ws, rank, local):
     dev = torch.device("cuda", local)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     exp_ctas = 0 if args.expert_capacity >= 1.0 else int(math.ceil(args.expert_capacity * sms))
-    shape = ZpLayerShape(c.E, c.k, c.d, c.f, args.mb_tokens, attention=not args.no_attention)
+    shape = ZpLayerShape(c.E, c.k, c.d, c.f, args.mb_tokens, attention=not args.no_attention,
+                         router_skew=args.router_skew)
     durs = measure_durations(shape, M, N, expert_max_ctas=exp_ctas, device=dev)
     # every rank must plan identically: use rank 0's measurement
     t = torch.tensor([durs[k] for k in sorted(durs)], dtype=torch.int64, device=dev)
@@ -417,6 +418,7 @@ def run_zp(args, ws, rank, local):
             "microbatches": args.microbatches, "tokens_per_microbatch": args.mb_tokens,
             "attention_block": not args.no_attention, "parallelism": f"zp{M}+{N}",
             "asym_ea_offload": list(assignment.offload), "expert_capacity": args.expert_capacity,
+            "router_skew_zipf": args.router_skew,
             "measured_durations_ns": durs,
             "l2": "activations and weights exceed the 126 MB L2; no flush",
         },
@@ -490,6 +492,8 @@ def main():
     ap.add_argument("--mb-tokens", type=int, default=4096, help="ZP (N>1): tokens per micro-batch per attention rank")
     ap.add_argument("--no-attention", action="store_true", help="ZP: identity attention block")
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
+    ap.add_argument("--router-skew", type=float, default=0.0,
+                    help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
     ap.add_argument("--expert-capacity", type=float, default=1.0,
                     help="ZP: capacity weight of expert ranks (grouped-GEMM grid = ceil(w*SMs))")
     args = ap.parse_args()

@@ -49,13 +49,13 @@ const char* hm_last_error(void);
 int hm_num_sms(void);
 
 /* ---- K1 router: logits (fixed-order fp32), top-k, softmax over the k, histogram, offsets ----
- * x[T,d] bf16, wg[d,E] bf16 (logits = x . wg). Outputs: idx[T,k] int32, w[T,k] fp32,
+ * x[T,d] bf16, wg[d,E] bf16, bias[E] fp32 or NULL (logits = x . wg + bias). Outputs: idx[T,k] int32, w[T,k] fp32,
  * logits[T,E] fp32 (required scratch, also a result), counts[E], offsets[E+1] int32,
  * chunk_base[hm_router_chunk_elems(T,E)] int32 (consumed by hm_dispatch_permute).
  * Requires d % 256 == 0, 1 <= k <= 8, k <= E <= 256.
  * Replaces: the router/gate folded into ATTN_F (taskgraph.py:220-246). */
-int hm_router_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
-                   float* w, float* logits, int32_t* counts, int32_t* offsets,
+int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
+                   int32_t* idx, float* w, float* logits, int32_t* counts, int32_t* offsets,
                    int32_t* chunk_base, void* stream);
 size_t hm_router_chunk_elems(int T, int E);
 

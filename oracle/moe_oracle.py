@@ -104,9 +104,11 @@ def router_logits_c(x_bf16: torch.Tensor, wg_bf16: torch.Tensor) -> np.ndarray:
     return out
 
 
-def route_c(x_bf16: torch.Tensor, wg_bf16: torch.Tensor, k: int) -> "RoutingRef":
+def route_c(x_bf16: torch.Tensor, wg_bf16: torch.Tensor, k: int, bias=None) -> "RoutingRef":
     """``route`` with the C restatement doing the heavy loops (for full-size parity checks)."""
     logits = router_logits_c(x_bf16, wg_bf16)
+    if bias is not None:
+        logits = (logits + np.asarray(bias, dtype=np.float32)[None, :]).astype(np.float32)
     lib = _clib()
     T, E = logits.shape
     if lib is None:
@@ -170,8 +172,10 @@ class RoutingRef:
     row_of: np.ndarray
 
 
-def route(x: np.ndarray, wg: np.ndarray, k: int) -> RoutingRef:
+def route(x: np.ndarray, wg: np.ndarray, k: int, bias=None) -> RoutingRef:
     logits = router_logits(x, wg)
+    if bias is not None:
+        logits = (logits + np.asarray(bias, dtype=np.float32)[None, :]).astype(np.float32)
     idx, w = topk_softmax(logits, k)
     E = wg.shape[1]
     counts, offsets = counts_offsets(idx, E)

@@ -154,8 +154,8 @@ size_t hm_router_chunk_elems(int T, int E) {
   return static_cast<size_t>((T + hm::kChunk - 1) / hm::kChunk) * static_cast<size_t>(E);
 }
 
-int hm_router_topk(const void* x, const void* wg, int T, int d, int E, int k, int32_t* idx,
-                   float* w, float* logits, int32_t* counts, int32_t* offsets,
+int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
+                   int32_t* idx, float* w, float* logits, int32_t* counts, int32_t* offsets,
                    int32_t* chunk_base, void* stream) {
   if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK || k > E)
     return fail(HM_E_SHAPE, "router: unsupported shape T=%d d=%d E=%d k=%d", T, d, E, k);
@@ -182,15 +182,15 @@ int hm_router_topk(const void* x, const void* wg, int T, int d, int E, int k, in
   if (eg == 8) {
     auto kern = hm::router_logits_kernel<8, 4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, T, d, E, logits);
+    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
   } else if (eg == 16) {
     auto kern = hm::router_logits_kernel<16, 4>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, T, d, E, logits);
+    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
   } else {
     auto kern = hm::router_logits_kernel<32, 2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, T, d, E, logits);
+    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
   }
   if (int rc = check_launch("router_logits")) return rc;
   hm::router_topk_kernel<<<nchunk, 1024, 0, st>>>(logits, T, E, k, idx, w, chunk_base);

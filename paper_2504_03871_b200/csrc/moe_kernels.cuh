@@ -6,6 +6,8 @@
 //    (bf16*bf16 products are exact in fp32, so FMA == mul-then-add), then the 32 lane partials
 //    are combined by an xor butterfly (offsets 16, 8, 4, 2, 1). Indices, counts and the
 //    permutation therefore reproduce bit-for-bit on the CPU.
+//  * an optional per-expert bias is added last (one fp32 rounding): l[t,e] = dot + bias[e]
+//    (router skew for the Asym-EA sweep; bias-based load balancing).
 //  * top-k: k largest logits, ties -> lower expert id; w = softmax over the k selected logits.
 //  * dispatch order: stable by (expert, token); a token appears at most once per expert.
 //    Tokens are processed in chunks of kChunk; chunk c's rows for expert e start at
@@ -26,7 +28,8 @@ constexpr int kRouterWarps = 8;
 template <int EG, int TT>
 __global__ void __launch_bounds__(kRouterWarps * 32)
     router_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                         int T, int d, int E, float* __restrict__ logits) {
+                         const float* __restrict__ bias, int T, int d, int E,
+                         float* __restrict__ logits) {
   extern __shared__ __align__(16) uint8_t smem_r[];
   __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(smem_r);  // [d][EG]
   const int e0 = blockIdx.y * EG;
@@ -105,7 +108,8 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
       if (t < T) {
 #pragma unroll
         for (int e = 0; e < EG; ++e)
-          if (lane == e && e0 + e < E) logits[static_cast<long>(t) * E + e0 + e] = acc[a][e];
+          if (lane == e && e0 + e < E)
+            logits[static_cast<long>(t) * E + e0 + e] = bias ? acc[a][e] + bias[e0 + e] : acc[a][e];
       }
     }
   }

@@ -82,6 +82,7 @@ class ZpLayerShape:
     tokens_per_mb: int  # tokens per micro-batch per attention rank
     heads: int = 0  # attention heads (0 = d // 128)
     attention: bool = True  # include the attention block (False: identity + residual)
+    router_skew: float = 0.0  # Zipf exponent of a per-expert router logit bias (Asym-EA sweep, C5)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -123,9 +124,8 @@ class NativeBackend:
         torch.cuda.synchronize(self.device)
 
     # tensor ops
-    def router(self, u, wg, k):
-        r = self.ops.router_topk(u, wg, k)
-        return r
+    def router(self, u, wg, k, bias=None):
+        return self.ops.router_topk(u, wg, k, bias)
 
     def permute(self, u, r):
         x_perm, _row_src, row_of = self.ops.dispatch_permute(u, r)
@@ -189,6 +189,7 @@ class RankState:
     gw_ug: dict = field(default_factory=dict)  # fp32 accumulators
     gw_d: dict = field(default_factory=dict)
     wg: dict = field(default_factory=dict)  # attention ranks: router [d, E]
+    bias: dict = field(default_factory=dict)  # attention ranks: router logit bias [E] fp32 or None
     gwg: dict = field(default_factory=dict)
     wqkv: dict = field(default_factory=dict)
     wo: dict = field(default_factory=dict)
@@ -242,6 +243,12 @@ class ZpExecutor:
                 st.wqkv[l] = wqkv.to(be.device).requires_grad_()
                 st.wo[l] = wo.to(be.device).requires_grad_()
                 st.wg[l] = wg.to(be.device)
+                st.bias[l] = None
+                if s.router_skew:
+                    from .configs import zipf_bias
+
+                    st.bias[l] = torch.tensor(zipf_bias(s.E, s.router_skew), dtype=torch.float32,
+                                              device=be.device)
                 st.gwg[l] = torch.zeros((s.d, s.E), dtype=torch.float32, device=be.device)
             own = st.own[l - 1]
             if own:
@@ -335,7 +342,7 @@ class ZpExecutor:
         self.u[(l, j)] = u
         self.z[(l, j)] = z
         zd = z.detach()
-        r = be.router(zd, st.wg[l], s.k)
+        r = be.router(zd, st.wg[l], s.k, st.bias[l])
         x_perm, row_of = be.permute(zd, r)
         self.route[(l, j)], self.row_of[(l, j)], self.x_perm[(l, j)] = r, row_of, x_perm
         self.my_counts[(l, j)] = be.counts(r)

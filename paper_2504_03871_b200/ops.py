@@ -94,9 +94,10 @@ class Routing:
     chunk_base: torch.Tensor  # [nchunk, E] int32 per-chunk row bases
 
 
-def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int) -> Routing:
-    """K1: fixed-order fp32 logits, top-k (ties -> lower id), softmax over the k, histogram."""
-    _require_cuda(x, wg)
+def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, bias: torch.Tensor | None = None) -> Routing:
+    """K1: fixed-order fp32 logits (+ optional per-expert fp32 bias), top-k (ties -> lower id),
+    softmax over the k, per-expert histogram and offsets."""
+    _require_cuda(x, wg, bias)
     lib = _native.load()
     T, d = x.shape
     E = wg.shape[1]
@@ -110,7 +111,7 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int) -> Routing:
     chunk_base = torch.empty((max(nce, 1),), dtype=torch.int32, device=dev)
     _tk = _begin("router_topk")
     rc = lib.hm_router_topk(
-        _ptr(x), _ptr(wg), T, d, E, k, _ptr(idx), _ptr(w), _ptr(logits), _ptr(counts),
+        _ptr(x), _ptr(wg), _ptr(bias), T, d, E, k, _ptr(idx), _ptr(w), _ptr(logits), _ptr(counts),
         _ptr(offsets), _ptr(chunk_base), _stream(),
     )
     _end(_tk)

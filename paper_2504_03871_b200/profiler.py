@@ -48,11 +48,16 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
 
     x = rnd(T, d)
     wqkv, wo, wg = rnd(d, 3 * d, std=d ** -0.5), rnd(d, d, std=d ** -0.5), rnd(d, E, std=d ** -0.5)
+    bias = None
+    if getattr(shape, "router_skew", 0.0):
+        from .configs import zipf_bias
+
+        bias = torch.tensor(zipf_bias(E, shape.router_skew), dtype=torch.float32, device=dev)
 
     def attn_step():
         u = attention_block(x, wqkv, wo, heads) if shape.attention else x
         z = rms_norm(u)
-        r = ops.router_topk(z, wg, k)
+        r = ops.router_topk(z, wg, k, bias)
         ops.dispatch_permute(z, r)
 
     attn_ms = _time_ms(attn_step)

@@ -50,8 +50,10 @@ class CpuBackend:
         return w.t().contiguous()
 
     # -- routing
-    def router(self, u, wg, k):
+    def router(self, u, wg, k, bias=None):
         logits = u.float() @ wg.float()
+        if bias is not None:
+            logits = logits + bias
         E = wg.shape[1]
         # ties -> lower id: stable descending sort on (-logit, e)
         order = torch.argsort(-logits, dim=1, stable=True)

@@ -47,6 +47,42 @@ def test_router_bit_exact(cfg):
     assert np.abs(r.w.cpu().numpy() - ref.w).max() <= TOL_GATE
 
 
+@pytest.mark.parametrize("cfg", ROUTER_CASES[:3], ids=lambda c: c.name)
+def test_router_with_bias_bit_exact(cfg):
+    from paper_2504_03871_b200.configs import zipf_bias
+
+    inp = make_inputs(cfg, seed=4)
+    bias = np.asarray(zipf_bias(cfg.E, 1.0), dtype=np.float32)
+    ref = orc.route(inp.x.float().numpy(), inp.wg.float().numpy(), cfg.k, bias=bias)
+    r = ops.router_topk(inp.x.cuda(), inp.wg.cuda(), cfg.k, torch.from_numpy(bias).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(r.logits.cpu().numpy().view(np.uint32), ref.logits.view(np.uint32))
+    assert np.array_equal(r.idx.cpu().numpy(), ref.idx)
+    assert np.array_equal(r.counts.cpu().numpy(), ref.counts)
+
+
+@pytest.mark.parametrize("cfg", [C2, C3], ids=lambda c: c.name)
+def test_full_size_routing_and_permutation_bit_exact(cfg):
+    """Full BASELINE sizes (T=16384): the C restatement of the router checks every index,
+    count, offset and row map; the permuted rows are checked as a gather of x."""
+    g = torch.Generator().manual_seed(21)
+    x = (torch.randn((cfg.T, cfg.d), generator=g)).to(torch.bfloat16)
+    wg = (torch.randn((cfg.d, cfg.E), generator=g) * cfg.d ** -0.5).to(torch.bfloat16)
+    ref = orc.route_c(x, wg, cfg.k)
+    xc = x.cuda()
+    r = ops.router_topk(xc, wg.cuda(), cfg.k)
+    x_perm, row_src, row_of = ops.dispatch_permute(xc, r)
+    torch.cuda.synchronize()
+    assert np.array_equal(r.logits.cpu().numpy().view(np.uint32), ref.logits.view(np.uint32))
+    assert np.array_equal(r.idx.cpu().numpy(), ref.idx)
+    assert np.array_equal(r.counts.cpu().numpy(), ref.counts)
+    assert np.array_equal(r.offsets.cpu().numpy(), ref.offsets)
+    assert np.array_equal(row_src.cpu().numpy(), ref.row_src)
+    assert np.array_equal(row_of.cpu().numpy(), ref.row_of)
+    assert torch.equal(x_perm, xc[row_src.long()])
+    assert int(r.offsets[-1]) == cfg.T * cfg.k  # dropless: every copy placed
+
+
 @pytest.mark.parametrize("cfg", ROUTER_CASES, ids=lambda c: c.name)
 def test_permute_bit_exact(cfg):
     inp = make_inputs(cfg, seed=2)

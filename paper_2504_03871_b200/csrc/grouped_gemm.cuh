@@ -238,11 +238,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     // ======================= TMA producer (both CTAs of a pair) =======================
     if (lane == 0) {
-      // raster n-fastest re-reads B across the inner loop (keep B, stream A); m-fastest keeps A
-      const uint64_t pol_keep = policy_evict_last();
-      const uint64_t pol_stream = policy_evict_first();
-      const uint64_t pol_a = p.n_fastest ? pol_stream : pol_keep;
-      const uint64_t pol_b = p.n_fastest ? pol_keep : pol_stream;
+      // evict_normal for both operands: a panel streamed by one wave is still read by the other
+      // clusters of that wave at slightly different times (evict_first/last measured worse:
+      // 4x the DRAM reads, profiles/r1_gemm_full_2cta_policies.md)
+      const uint64_t pol_a = policy_evict_normal();
+      const uint64_t pol_b = pol_a;
       uint32_t it = 0;
       int mapped_e = -1;
       for (int tile = tile0; tile < total_tiles; tile += tile_step) {

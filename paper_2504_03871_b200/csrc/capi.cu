@@ -101,7 +101,7 @@ int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
 
 template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
-                int max_ctas, cudaStream_t stream) {
+                long ub_tiles, int max_ctas, cudaStream_t stream) {
   auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI, CTAS>;
   constexpr int smem = hm::TileCfg<CTAS>::kSmemBytes;
   static bool attr_set = false;
@@ -110,10 +110,23 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
     if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attr: %s", cudaGetErrorString(e));
     attr_set = true;
   }
-  int grid = num_sms();
-  if (max_ctas > 0 && max_ctas < grid) grid = max_ctas;
-  grid = (grid / CTAS) * CTAS;
-  if (grid < CTAS) grid = CTAS;
+  // Default: one cluster per tile (upper bound `ub_tiles`), scheduled dynamically with cluster
+  // launch control. A capacity cap (max_ctas > 0) instead runs a persistent grid of max_ctas
+  // CTAs with static tile striding (the per-rank capacity-weight emulation).
+  int grid;
+  hm::GroupedGemmParams pp = p;
+  if (max_ctas > 0) {
+    grid = max_ctas < num_sms() ? max_ctas : num_sms();
+    grid = (grid / CTAS) * CTAS;
+    if (grid < CTAS) grid = CTAS;
+    pp.dynamic = 0;
+  } else {
+    long g = ub_tiles * CTAS;
+    if (g < CTAS) g = CTAS;
+    if (g > 0x7fffffffL) g = 0x7fffffffL / CTAS * CTAS;
+    grid = static_cast<int>(g);
+    pp.dynamic = 1;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(hm::kGemmThreads);
@@ -126,7 +139,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, pp);
   if (e != cudaSuccess) return fail(static_cast<int>(e), "grouped_gemm launch: %s", cudaGetErrorString(e));
   return check_launch("grouped_gemm");
 }
@@ -417,27 +430,32 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
     p.expert_maps = maps;
   }
 
+  // upper bound of the tile count (the exact count depends on device-side expert sizes)
+  const long tile_m = 128L * ctas;
+  const long ntl = (N + 255) / 256;
+  const long ub_tiles = wgrad ? static_cast<long>(E) * ((M + tile_m - 1) / tile_m) * ntl
+                              : (static_cast<long>(rows) / tile_m + E) * ntl;
   switch (mode) {
     case HM_GEMM_FWD_UPGATE:
       if (N % 256 != 0 || !out2) return fail(HM_E_SHAPE, "upgate: N=2f must be a multiple of 256 and h given");
-      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 2>(ma, mb, p, max_ctas, st)
-                       : launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                       : launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 1>(ma, mb, p, ub_tiles, max_ctas, st);
     case HM_GEMM_FWD_DOWN:
-      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
-                       : launch_gemm<false, false, false, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                       : launch_gemm<false, false, false, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
     case HM_GEMM_BWD_DACT:
       if (N % 128 != 0 || !aux) return fail(HM_E_SHAPE, "dact: N=f must be a multiple of 128 and h given");
-      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 2>(ma, mb, p, max_ctas, st)
-                       : launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                       : launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 1>(ma, mb, p, ub_tiles, max_ctas, st);
     case HM_GEMM_BWD_DX:
-      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
-                       : launch_gemm<false, false, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                       : launch_gemm<false, false, true, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
     case HM_GEMM_WGRAD:
-      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_STORE, 2>(ma, mb, p, max_ctas, st)
-                       : launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                       : launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
     case HM_GEMM_WGRAD_ACC:
-      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_ACC_F32, 2>(ma, mb, p, max_ctas, st)
-                       : launch_gemm<true, true, true, hm::EPI_ACC_F32, 1>(ma, mb, p, max_ctas, st);
+      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_ACC_F32, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                       : launch_gemm<true, true, true, hm::EPI_ACC_F32, 1>(ma, mb, p, ub_tiles, max_ctas, st);
     default:
       return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
   }

@@ -35,14 +35,16 @@ constexpr int kATileBytes = kBM * kBK * 2;  // 16 KB
 constexpr int kMaxStages = 8;
 constexpr int kMaxExperts = 256;
 constexpr int kEpiWarps = 8;     // two warps per TMEM lane quadrant, each owns 128 columns
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kSchedWarp = 2 + kEpiWarps;  // cluster-launch-control scheduler (dynamic mode)
+constexpr int kGemmThreads = 32 * (kSchedWarp + 1);
 constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 
 // CTAS = 1: one CTA computes a 128 x 256 tile (UMMA M=128, cta_group::1).
 // CTAS = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (UMMA M=256):
 //           each CTA stages its own 128 rows of A and half (128 columns) of B, the leader CTA
 //           issues the MMAs, each CTA's TMEM receives its 128 accumulator rows.
-constexpr int kBookkeepingBytes = 3072;  // GemmShared, placed first; tiles start 1024-aligned
+constexpr int kBookkeepingBytes = 3072;
+constexpr int kGroupM = 8;  // raster group height (tiles)  // GemmShared, placed first; tiles start 1024-aligned
 
 template <int CTAS>
 struct TileCfg {
@@ -50,7 +52,7 @@ struct TileCfg {
   static constexpr int kBRows = kBN / CTAS;           // B rows (N) staged per CTA
   static constexpr int kBTileBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CTAS == 1 ? 4 : 7;
+  static constexpr int kStages = CTAS == 1 ? 4 : 6;
   static constexpr int kSmemBytes = kBookkeepingBytes + kStages * kStageBytes;
 };
 constexpr int kGemmSmemBytes = TileCfg<1>::kSmemBytes;
@@ -70,6 +72,7 @@ struct GroupedGemmParams {
   int n_fastest;  // raster: 1 = n-tile index varies fastest within an expert
   const CUtensorMap* expert_maps;  // GROUP_K: per-expert TMA views, [2e] = A rows, [2e+1] = B rows
   float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
+  int dynamic;  // 1: one cluster per tile + cluster-launch-control work stealing; 0: persistent
 };
 
 // out[0..31] += v[0..31] (fp32), masked to valid_cols
@@ -117,6 +120,9 @@ __global__ void build_expert_maps_kernel(const __grid_constant__ CUtensorMap tmp
 }
 
 struct GemmShared {
+  uint4 clc_resp[2];      // cluster-launch-control responses (double buffered)
+  uint64_t clc_full[2];
+  uint64_t clc_empty[2];
   uint64_t full[kMaxStages];
   uint64_t empty[kMaxStages];
   uint64_t tmem_full[2];
@@ -145,9 +151,37 @@ HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_f
   else mtiles = (sh.seg[lo + 1] - sh.seg[lo] + TILE_M - 1) / TILE_M;
   TileCoord c;
   c.e = lo;
-  if (n_fastest) { c.mt = local / ntiles; c.nt = local % ntiles; }
-  else { c.nt = local / mtiles; c.mt = local % mtiles; }
+  // grouped raster: groups of kGroupM m-tiles, m fastest inside a group, then n, then the
+  // next group. The ~74-148 concurrently running tiles then form an ~8 x 9 block, so every
+  // A and B panel they stream is shared by ~8 concurrent tiles (L2 reuse along long K).
+  (void)n_fastest;
+  const int group = local / (kGroupM * ntiles);
+  const int rem = local - group * kGroupM * ntiles;
+  const int gm = min(kGroupM, mtiles - group * kGroupM);
+  c.mt = group * kGroupM + rem % gm;
+  c.nt = rem / gm;
   return c;
+}
+
+// Tile sequence of every role. Persistent mode (step > 0): tile0 + i*step. Dynamic mode
+// (step == 0): tile0 = this cluster's own index, then the clusters cancelled by the scheduler's
+// clusterlaunchcontrol.try_cancel requests (work stealing: clusters that start late, e.g. on SMs
+// a concurrent NCCL kernel still held, simply find less work). Returns -1 when done.
+template <int CTAS, bool WARP>
+HM_DEV int next_tile(GemmShared& sh, int cur, int step, uint32_t& ci, bool arrive) {
+  if (step) return cur + step;
+  const int s = ci & 1;
+  const uint32_t ph = (ci >> 1) & 1;
+  ++ci;
+  mbar_wait(&sh.clc_full[s], ph);
+  const int x = clc_decode(&sh.clc_resp[s]);
+  fence_proxy_async_smem();  // our generic read precedes the next async write into the slot
+  if (WARP) __syncwarp();
+  if (arrive) {
+    if (CTAS == 2) mbar_arrive_cluster(mapa_shared(&sh.clc_empty[s], 0));
+    else mbar_arrive(&sh.clc_empty[s]);
+  }
+  return x < 0 ? -1 : x / CTAS;
 }
 
 HM_DEV float silu_f(float g) { return g / (1.0f + __expf(-g)); }
@@ -194,7 +228,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t rank = (CTAS == 2) ? cluster_ctarank() : 0u;
   const bool leader = (rank == 0);
   const int tile0 = (CTAS == 2) ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
-  const int tile_step = (CTAS == 2) ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
+  const int tile_step = p.dynamic ? 0 : ((CTAS == 2) ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x));
 
   // ---- per-CTA bookkeeping: expert segment table and tile prefix sums --------------------
   const int ntiles = (p.N + kBN - 1) / kBN;
@@ -216,6 +250,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&sh.tmem_full[a], 1);
       mbar_init(&sh.tmem_empty[a], kEpiWarps * CTAS);
+      // tile-stream consumers: producer + epilogue warps in every CTA, MMA warp in the leader
+      mbar_init(&sh.clc_full[a], 1);
+      mbar_init(&sh.clc_empty[a], (1 + kEpiWarps) * CTAS + 1);
     }
     fence_barrier_init();
   }
@@ -245,7 +282,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_b = pol_a;
       uint32_t it = 0;
       int mapped_e = -1;
-      for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+      uint32_t ci = 0;
+      for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
+           tile = next_tile<CTAS, false>(sh, tile, tile_step, ci, true)) {
+        if (tile >= total_tiles) continue;  // a stolen cluster index past the real tile count
         const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
         const int seg0 = sh.seg[tc.e];
         const int me = sh.seg[tc.e + 1] - seg0;
@@ -310,7 +350,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr uint32_t idesc = make_idesc_bf16(kTileM, kBN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
     uint32_t it = 0, tcount = 0;
     if (leader) {
-      for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+      uint32_t ci = 0;
+      for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
+           tile = next_tile<CTAS, true>(sh, tile, tile_step, ci, lane == 0)) {
+        if (tile >= total_tiles) continue;
         const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
         const int seg0 = sh.seg[tc.e];
         const int me = sh.seg[tc.e + 1] - seg0;
@@ -353,13 +396,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ++tcount;
       }
     }
+  } else if (warp == kSchedWarp) {
+    // ======================= tile scheduler (dynamic mode, leader CTA) =======================
+    if (p.dynamic && leader && lane == 0) {
+      for (uint32_t i = 0;; ++i) {
+        const int s = i & 1;
+        const uint32_t ph = (i >> 1) & 1;
+        mbar_wait(&sh.clc_empty[s], ph ^ 1);  // every consumer of both CTAs released the slot
+        mbar_arrive_expect_tx(&sh.clc_full[s], 16);
+        if (CTAS == 2) mbar_arrive_expect_tx_cluster(mapa_shared(&sh.clc_full[s], 1), 16);
+        clc_try_cancel<CTAS == 2>(&sh.clc_resp[s], &sh.clc_full[s]);
+        mbar_wait(&sh.clc_full[s], ph);
+        if (clc_decode(&sh.clc_resp[s]) < 0) break;  // nothing left to steal
+      }
+    }
   } else {
     // ======================= epilogue (warps 2..9) =======================
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;  // column half of the 256-wide accumulator
     const int row_in_tile = static_cast<int>(rank) * kBM + quad * 32 + lane;
-    uint32_t tcount = 0;
-    for (int tile = tile0; tile < total_tiles; tile += tile_step) {
+    uint32_t tcount = 0, ci = 0;
+    for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
+         tile = next_tile<CTAS, true>(sh, tile, tile_step, ci, lane == 0)) {
+      if (tile >= total_tiles) continue;
       const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
       const int seg0 = sh.seg[tc.e];
       const int me = sh.seg[tc.e + 1] - seg0;

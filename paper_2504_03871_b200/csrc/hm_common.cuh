@@ -391,3 +391,52 @@ HM_DEV void tma_load_3d_any(void* smem_dst, const CUtensorMap* map, uint32_t bar
   }
 }
 }  // namespace hm
+
+// ---------------------------------------------------------------------------------------------
+// cluster launch control (sm_100 hardware work stealing)
+
+namespace hm {
+
+HM_DEV void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
+                   cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+
+// Ask the hardware to cancel one not-yet-launched cluster of this grid; the 16-byte response
+// lands at `resp` (of every CTA of the cluster when MULTICAST) and completes 16 tx bytes on
+// the mbarrier at the same offset.
+template <bool MULTICAST>
+HM_DEV void clc_try_cancel(void* resp, uint64_t* bar) {
+  if (MULTICAST)
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes"
+        ".multicast::cluster::all.b128 [%0], [%1];" ::"r"(smem_u32(resp)),
+        "r"(smem_u32(bar))
+        : "memory");
+  else
+    asm volatile(
+        "clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128"
+        " [%0], [%1];" ::"r"(smem_u32(resp)),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Decode a response: returns the first CTA id (x) of the cancelled cluster, or -1 when there
+// was nothing left to cancel.
+HM_DEV int clc_decode(const void* resp) {
+  uint32_t x = 0, ok = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b128 r;\n\t"
+      "ld.shared.b128 r, [%2];\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+      "selp.u32 %1, 1, 0, p;\n\t"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%0, _, _, _}, r;\n\t}"
+      : "=r"(x), "=r"(ok)
+      : "r"(smem_u32(resp))
+      : "memory");
+  return ok ? static_cast<int>(x) : -1;
+}
+
+}  // namespace hm

@@ -187,6 +187,30 @@ def test_grouped_ffn_vs_fp32(segs, df):
     assert orc.rel_err(gw_d, 2 * wdr.grad) < TOL_W
 
 
+def test_grouped_ffn_capacity_cap_matches_dynamic_schedule():
+    """max_ctas (persistent, static tile striding: the capacity-weight emulation) and the
+    default dynamic cluster-launch-control schedule compute identical results."""
+    segs = [300, 0, 1000, 257, 31, 700]
+    d, f = 512, 384
+    E = len(segs)
+    g = torch.Generator().manual_seed(5)
+    bf = lambda *s, std=1.0: (torch.randn(s, generator=g) * std).to(torch.bfloat16).cuda()  # noqa: E731
+    x = bf(sum(segs), d)
+    w_ug = bf(E, 2 * f, d, std=d ** -0.5)
+    w_d = bf(E, d, f, std=f ** -0.5)
+    dy = bf(sum(segs), d)
+    seg = torch.from_numpy(_ragged_offsets(segs)).cuda()
+    outs = []
+    for cap in (0, 20, 7):
+        y, h, act = ops.grouped_ffn_fwd(x, seg, w_ug, w_d, max_ctas=cap)
+        dx, dwu, dwd = ops.grouped_ffn_bwd(dy, x, h, act, seg, w_ug, w_d, max_ctas=cap)
+        outs.append((y, h, act, dx, dwu, dwd))
+    torch.cuda.synchronize()
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("cfg", [with_tokens(C1, 1024), LayerConfig("c3ish", 16, 4, 512, 384, 700)],
                          ids=lambda c: c.name)
 def test_moe_layer_fwd_bwd(cfg):

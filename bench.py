@@ -24,6 +24,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
@@ -363,8 +364,12 @@ def run_zp(args, ws, rank, local):
     t = torch.tensor([durs[k] for k in sorted(durs)], dtype=torch.int64, device=dev)
     dist.broadcast(t, 0)
     durs = dict(zip(sorted(durs), (int(v) for v in t.tolist())))
+    from fractions import Fraction
+
+    plan_durs = {k_: v for k_, v in durs.items() if k_ != "gamma_x100"}
     spec = make_zp_spec(M, N, args.layers, args.microbatches, c.E, c.k, args.mb_tokens, c.d,
-                        asym_ea=not args.no_asym_ea, **durs)
+                        asym_ea=not args.no_asym_ea, gamma=Fraction(durs["gamma_x100"], 100),
+                        **plan_durs)
     dur = derive_task_durations(spec)
     assignment = plan_assignment(spec, dur)
     graph = build_zp_graph(spec, dur, assignment, mode="zp-full")

@@ -72,8 +72,16 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
     seg1 = torch.tensor([0, B], dtype=torch.int32, device=dev)
     single_ms = _time_ms(lambda: ops.grouped_ffn_fwd(xb, seg1, w_ug[:1].contiguous(), w_d[:1].contiguous(),
                                                      attn_max_ctas))
+    # backward factor gamma: the expert layer's measured backward / forward time (the reference
+    # applies one gamma to every task kind, core.py:113-122)
+    y, h, act = ops.grouped_ffn_fwd(xb, seg, w_ug, w_d, expert_max_ctas)
+    gw_ug = torch.zeros(w_ug.shape, dtype=torch.float32, device=dev)
+    gw_d = torch.zeros(w_d.shape, dtype=torch.float32, device=dev)
+    bwd_ms = _time_ms(lambda: ops.grouped_ffn_bwd_acc(y, xb, h, act, seg, w_ug, w_d, gw_ug, gw_d,
+                                                      expert_max_ctas))
     comm_ns = T * k * d * 2 / (NVLINK_GBS * 1e9) * 1e9
     return {
+        "gamma_x100": int(round(100 * bwd_ms / exp_ms)),
         "attn_fwd_ns": int(attn_ms * 1e6),
         "expert_layer_fwd_ns": int(exp_ms * 1e6),
         "single_expert_fwd_ns": int(single_ms * 1e6),

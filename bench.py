@@ -318,7 +318,7 @@ def run_ours(args, ws, rank, local):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_baseline_tokens)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        _emit(out)
 
 
 def cpu_baseline(cfg, tokens: int):
@@ -441,7 +441,7 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200 import simulate, default_orders
 
     out["zp"]["simulated_makespan_ms"] = simulate(graph, default_orders(graph)).makespan / 1e6
-    print(json.dumps(out), flush=True)
+    _emit(out)
 
 
 def run_reference(args, ws, rank):
@@ -477,10 +477,25 @@ def run_reference(args, ws, rank):
                          "sample": f"{c.T} tokens per step, fp32 CPU oracle fwd+bwd"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    _emit(out)
+
+
+_OUT = sys.stdout
+
+
+def _emit(obj) -> None:
+    """Print the one JSON result line on the original stdout."""
+    _OUT.write(json.dumps(obj) + "\n")
+    _OUT.flush()
 
 
 def main():
+    global _OUT
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # native libraries (NCCL) may print banners on fd 1; keep fd 1 for stderr and write the
+        # JSON line to a duplicate of the original stdout
+        _OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -206,9 +206,9 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
     kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
   }
   if (int rc = check_launch("router_logits")) return rc;
-  hm::router_topk_kernel<<<nchunk, 1024, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+  hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
   if (int rc = check_launch("router_topk")) return rc;
-  hm::router_scan_kernel<<<1, 256, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
+  hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
   return check_launch("router_scan");
 }
 

@@ -18,7 +18,7 @@
 
 namespace hm {
 
-constexpr int kChunk = 256;         // tokens per dispatch chunk (one permute CTA)
+constexpr int kChunk = 64;          // tokens per dispatch chunk (one permute CTA)
 constexpr int kMaxTopK = 8;
 constexpr int kRouterWarps = 8;
 
@@ -184,17 +184,22 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ------------------------------------------------------------------------------------------
-// K1c: counts / offsets / chunk bases. Single CTA; thread e owns expert e.
-__global__ void __launch_bounds__(256)
+// K1c: counts / offsets / chunk bases. Single CTA of 1024 threads; warp w owns experts
+// w, w+32, ...: (1) per-expert totals with warp reductions over the chunks, (2) exclusive scan
+// over experts, (3) per-expert exclusive scans over chunks (warp shuffles, 32 chunks per step).
+__global__ void __launch_bounds__(1024)
     router_scan_kernel(int32_t* __restrict__ chunk_counts /*in: counts, out: bases*/, int nchunk,
                        int E, int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
   __shared__ int tot[256];
   __shared__ int off[257];
-  const int e = threadIdx.x;
-  int s = 0;
-  if (e < E)
-    for (int c = 0; c < nchunk; ++c) s += chunk_counts[static_cast<long>(c) * E + e];
-  tot[e] = (e < E) ? s : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int e = warp; e < E; e += nw) {
+    int s = 0;
+    for (int c = lane; c < nchunk; c += 32) s += chunk_counts[static_cast<long>(c) * E + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tot[e] = s;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int a = 0;
@@ -202,19 +207,26 @@ __global__ void __launch_bounds__(256)
     off[E] = a;
   }
   __syncthreads();
-  if (e < E) {
-    counts[e] = tot[e];
-    offsets[e] = off[e];
+  for (int e = warp; e < E; e += nw) {
     int base = off[e];
-    for (int c = 0; c < nchunk; ++c) {
-      const int n = chunk_counts[static_cast<long>(c) * E + e];
-      chunk_counts[static_cast<long>(c) * E + e] = base;
-      base += n;
+    for (int c0 = 0; c0 < nchunk; c0 += 32) {
+      const int c = c0 + lane;
+      const int v = c < nchunk ? chunk_counts[static_cast<long>(c) * E + e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += n;
+      }
+      if (c < nchunk) chunk_counts[static_cast<long>(c) * E + e] = base + incl - v;
+      base += __shfl_sync(0xffffffffu, incl, 31);
     }
+    if (lane == 0) { counts[e] = tot[e]; offsets[e] = off[e]; }
   }
   if (threadIdx.x == 0) offsets[E] = off[E];
 }
 
+// ------------------------------------------------------------------------------------------
 // Stable destination rows of one chunk: warp w handles experts w, w+8, ...; for each expert it
 // scans the chunk's (token, slot) entries 32 at a time with a ballot, so entry i of expert e
 // gets row base[e] + #(earlier entries of e). Tokens hold distinct experts, so entry order ==

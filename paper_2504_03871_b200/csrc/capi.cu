@@ -303,42 +303,39 @@ int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, co
   return check_launch("combine_bwd");
 }
 
-size_t hm_router_bwd_part_elems(int T, int d, int E) {
-  const int nsplit = 64;
-  (void)T;
-  return static_cast<size_t>(nsplit) * E * d;
+size_t hm_router_bwd_part_elems(int T, int d, int E, int k) {
+  // dlogit in permuted-row order (T*k) followed by the per-split dWg partials
+  return static_cast<size_t>(T) * k + static_cast<size_t>(hm::kWgSplit) * E * d;
 }
 
 int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
-                  const float* dw, const void* x, const void* wg_t, int T, int d, int E, int k,
-                  void* dx, float* dlogit, void* dwg, float* part, void* stream) {
+                  const float* dw, const void* x_perm, const int32_t* offsets, const void* wg_t,
+                  int T, int d, int E, int k, void* dx, float* dlogit, void* dwg, float* part,
+                  void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E < 1 || E > 256) return fail(HM_E_SHAPE, "router_bwd: bad shape");
-  if (!aligned16(dx_perm) || !aligned16(dx) || !aligned16(wg_t))
+  if (!aligned16(dx_perm) || !aligned16(dx) || !aligned16(wg_t) || (dwg && !aligned16(x_perm)))
     return fail(HM_E_ALIGN, "router_bwd: alignment");
   cudaStream_t st = S(stream);
   if (T == 0) {
     if (dwg) cudaMemsetAsync(dwg, 0, static_cast<size_t>(d) * E * 2, st);
     return check_launch("router_bwd(empty)");
   }
+  if (dwg && (!part || !offsets || !x_perm)) return fail(HM_E_ARG, "router_bwd: dwg needs x_perm, offsets and part");
   auto dp = static_cast<const __nv_bfloat16*>(dx_perm);
   auto gt = static_cast<const __nv_bfloat16*>(wg_t);
   auto out = static_cast<__nv_bfloat16*>(dx);
-  HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dlogit)));
+  float* dl_perm = dwg ? part : nullptr;
+  HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dlogit, dl_perm)));
   if (int rc = check_launch("unpermute_router_bwd")) return rc;
   if (dwg) {
-    if (!dlogit || !part) return fail(HM_E_ARG, "router_bwd: dwg needs dlogit and part");
-    const int nsplit = 64;
-    const int per = (T + nsplit - 1) / nsplit;
-    dim3 grid((d + 255) / 256, nsplit);
-    const size_t smem = static_cast<size_t>(E) * 256 * 4;
-    auto kern = hm::router_wgrad_partial_kernel;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 256, smem, st>>>(static_cast<const __nv_bfloat16*>(x), idx, dlogit, T, d, E, k,
-                                  per, part);
-    if (int rc = check_launch("router_wgrad_partial")) return rc;
+    float* partials = part + static_cast<size_t>(T) * k;
+    dim3 grid(E * hm::kWgSplit, (d + 2047) / 2048);
+    hm::router_wgrad_perm_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x_perm),
+                                                       dl_perm, offsets, d, E, partials);
+    if (int rc = check_launch("router_wgrad_perm")) return rc;
     const long n = static_cast<long>(d) * E;
     hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(
-        part, nsplit, d, E, static_cast<__nv_bfloat16*>(dwg));
+        partials, hm::kWgSplit, d, E, static_cast<__nv_bfloat16*>(dwg));
     return check_launch("router_wgrad_reduce");
   }
   return 0;

@@ -416,7 +416,8 @@ __global__ void __launch_bounds__(256)
                                 const int32_t* __restrict__ row_of, const int32_t* __restrict__ idx,
                                 const float* __restrict__ w, const float* __restrict__ dw,
                                 const __nv_bfloat16* __restrict__ wg_t, int T, int d,
-                                __nv_bfloat16* __restrict__ dx, float* __restrict__ dlogit) {
+                                __nv_bfloat16* __restrict__ dx, float* __restrict__ dlogit,
+                                float* __restrict__ dl_perm) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(256)
       const float ws = w[static_cast<long>(t) * K + s];
       dl[s] = ws * (dw[static_cast<long>(t) * K + s] - wsum);
       if (lane == 0 && dlogit) dlogit[static_cast<long>(t) * K + s] = dl[s];
+      if (lane == 0 && dl_perm) dl_perm[rows[s]] = dl[s];
     }
     for (int q = lane; q < nv; q += 32) {
       float acc[8];
@@ -493,30 +495,37 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------------------------------
-// Router weight gradient dWg[i,e] = sum_t x[t,i] * dlogit_dense[t,e] (only the k selected
-// experts are non-zero). grid = (d/256, nsplit); each CTA owns 256 columns and a token range,
-// accumulates per-expert sums in shared memory ([E][256] fp32), and writes a partial slab
-// part[split][e][i]. router_wgrad_reduce sums the slabs in split order (deterministic).
+// Router weight gradient dWg[i,e] = sum over expert e's permuted rows r of dl_perm[r] * x_perm[r,i]
+// (each token's routed copy carries its own dlogit). grid = (E * kWgSplit, ceil(d / 2048)); a
+// thread owns 8 consecutive columns (one 16-byte load per row) and a slice of the expert's rows;
+// per-split partial sums are reduced in split order by router_wgrad_reduce (deterministic).
+constexpr int kWgSplit = 16;
 __global__ void __launch_bounds__(256)
-    router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
-                                const float* __restrict__ dlogit, int T, int d, int E, int k,
-                                int tokens_per_split, float* __restrict__ part) {
-  extern __shared__ float accs[];  // [E][256]
-  const int col = blockIdx.x * 256 + threadIdx.x;
-  for (int e = 0; e < E; ++e) accs[e * 256 + threadIdx.x] = 0.f;
-  const int t0 = blockIdx.y * tokens_per_split;
-  const int t1 = min(T, t0 + tokens_per_split);
-  for (int t = t0; t < t1; ++t) {
-    const float xv = (col < d) ? __bfloat162float(x[static_cast<long>(t) * d + col]) : 0.f;
-    for (int s = 0; s < k; ++s) {
-      const int e = idx[static_cast<long>(t) * k + s];
-      const float g = dlogit[static_cast<long>(t) * k + s];
-      accs[e * 256 + threadIdx.x] = __fmaf_rn(xv, g, accs[e * 256 + threadIdx.x]);
+    router_wgrad_perm_kernel(const __nv_bfloat16* __restrict__ x_perm, const float* __restrict__ dl_perm,
+                             const int32_t* __restrict__ offsets, int d, int E,
+                             float* __restrict__ part /*[kWgSplit][E][d]*/) {
+  const int e = blockIdx.x / kWgSplit;
+  const int split = blockIdx.x % kWgSplit;
+  const int col = (blockIdx.y * 256 + threadIdx.x) * 8;
+  const int r0 = offsets[e], r1 = offsets[e + 1];
+  const int n = r1 - r0;
+  const int a = r0 + static_cast<int>((static_cast<long>(n) * split) / kWgSplit);
+  const int b = r0 + static_cast<int>((static_cast<long>(n) * (split + 1)) / kWgSplit);
+  float acc[8];
+#pragma unroll
+  for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+  if (col < d) {
+    for (int r = a; r < b; ++r) {
+      const float g = __ldg(dl_perm + r);
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(x_perm + static_cast<long>(r) * d + col));
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+      for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(g, bf16_to_f32(h[z]), acc[z]);
     }
+    float4* out = reinterpret_cast<float4*>(part + (static_cast<long>(split) * E + e) * d + col);
+    out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
-  if (col < d)
-    for (int e = 0; e < E; ++e)
-      part[(static_cast<long>(blockIdx.y) * E + e) * d + col] = accs[e * 256 + threadIdx.x];
 }
 
 __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nsplit, int d, int E,

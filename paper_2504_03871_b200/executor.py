@@ -140,8 +140,8 @@ class NativeBackend:
     def combine_bwd(self, dy, y_perm, row_of, r):
         return self.ops.combine_bwd(dy, y_perm, row_of, r.w)
 
-    def router_bwd(self, dx_perm, row_of, r, dw, u, wg_t):
-        dx, _dl, dwg = self.ops.router_bwd(dx_perm, row_of, r, dw, u, wg_t, want_dwg=True)
+    def router_bwd(self, dx_perm, row_of, r, dw, x_perm, wg_t):
+        dx, _dl, dwg = self.ops.router_bwd(dx_perm, row_of, r, dw, x_perm, wg_t, want_dwg=True)
         return dx, dwg
 
     def transpose(self, w):
@@ -416,7 +416,7 @@ class ZpExecutor:
         if l not in self.wg_t:
             self.wg_t[l] = be.transpose(st.wg[l])
         dz, dwg = be.router_bwd(self.dx_perm[(l, j)], self.row_of[(l, j)], r, self.dw[(l, j)],
-                                z.detach(), self.wg_t[l])
+                                self.x_perm[(l, j)], self.wg_t[l])
         st.gwg[l] += dwg.float()
         h = self.h_in[(l, j)]
         with torch.enable_grad():

@@ -196,24 +196,24 @@ def transpose_bf16(a: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def router_bwd(dx_perm, row_of, r: Routing, dw, x, wg_t, want_dwg: bool = True):
-    """dx = unpermute_sum(dx_perm) + dlogit . Wg^T ; dWg = x^T . dlogit."""
-    _require_cuda(dx_perm, row_of, dw, x, wg_t)
+def router_bwd(dx_perm, row_of, r: Routing, dw, x_perm, wg_t, want_dwg: bool = True):
+    """dx = unpermute_sum(dx_perm) + dlogit . Wg^T ; dWg = sum_rows dlogit * x_perm (per expert)."""
+    _require_cuda(dx_perm, row_of, dw, x_perm, wg_t)
     lib = _native.load()
     T, k = row_of.shape
-    d = x.shape[1]
+    d = x_perm.shape[1]
     E = wg_t.shape[0]
-    dev = x.device
-    dx = torch.empty((T, d), dtype=x.dtype, device=dev)
+    dev = x_perm.device
+    dx = torch.empty((T, d), dtype=x_perm.dtype, device=dev)
     dlogit = torch.empty((T, k), dtype=torch.float32, device=dev)
     dwg = part = None
     if want_dwg:
-        dwg = torch.empty((d, E), dtype=x.dtype, device=dev)
-        part = torch.empty((lib.hm_router_bwd_part_elems(T, d, E),), dtype=torch.float32, device=dev)
+        dwg = torch.empty((d, E), dtype=x_perm.dtype, device=dev)
+        part = torch.empty((lib.hm_router_bwd_part_elems(T, d, E, k),), dtype=torch.float32, device=dev)
     _tk = _begin("router_bwd")
     rc = lib.hm_router_bwd(
-        _ptr(dx_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(dw), _ptr(x), _ptr(wg_t), T, d, E,
-        k, _ptr(dx), _ptr(dlogit), _ptr(dwg), _ptr(part), _stream(),
+        _ptr(dx_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(dw), _ptr(x_perm), _ptr(r.offsets),
+        _ptr(wg_t), T, d, E, k, _ptr(dx), _ptr(dlogit), _ptr(dwg), _ptr(part), _stream(),
     )
     _end(_tk)
     _native.check(rc, "hm_router_bwd")

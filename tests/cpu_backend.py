@@ -88,15 +88,20 @@ class CpuBackend:
         dw = (y_perm[row_of.reshape(-1)].reshape(T, k, -1) * dy[:, None, :]).sum(-1)
         return dy_perm, dw
 
-    def router_bwd(self, dx_perm, row_of, r, dw, u, wg_t):
+    def router_bwd(self, dx_perm, row_of, r, dw, x_perm, wg_t):
         T, k = row_of.shape
         dx = dx_perm[row_of.reshape(-1)].reshape(T, k, -1).sum(1)
         dl = r.w * (dw - (r.w * dw).sum(1, keepdim=True))
         dx = dx + (dl[:, :, None] * wg_t[r.idx.long()]).sum(1)
         E = wg_t.shape[0]
-        dense = torch.zeros(T, E)
-        dense.scatter_(1, r.idx.long(), dl)
-        return dx, u.float().t() @ dense
+        # each permuted row is a routed copy of one token: dWg[:, e] = sum_rows dl * x_perm
+        dl_perm = torch.zeros(T * k)
+        dl_perm[row_of.reshape(-1)] = dl.reshape(-1)
+        dwg = torch.zeros(x_perm.shape[1], E)
+        off = r.offsets.tolist()
+        for e in range(E):
+            dwg[:, e] = x_perm[off[e]:off[e + 1]].float().t() @ dl_perm[off[e]:off[e + 1]]
+        return dx, dwg
 
     # -- experts (gate/up interleaved in 128-row blocks, as on the GPU)
     @staticmethod

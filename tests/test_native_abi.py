@@ -28,4 +28,4 @@ def test_pure_host_entry_points():
     assert lib.hm_abi_version() == 1
     assert lib.hm_router_chunk_elems(4096, 8) == 64 * 8
     assert lib.hm_router_chunk_elems(1, 64) == 64
-    assert lib.hm_router_bwd_part_elems(16384, 4096, 8) == 64 * 8 * 4096
+    assert lib.hm_router_bwd_part_elems(16384, 4096, 8, 2) == 16384 * 2 + 16 * 8 * 4096

@@ -256,39 +256,59 @@ def run_ours(args, ws, rank, local):
         "gemm_ms_per_step": round(gemm_ms, 3),
     }
 
-    # ---- end-to-end through the public API with host buffers
+    # ---- end-to-end through the public API with host buffers: every step copies its inputs
+    # (x, dY) from pinned host memory and reads its result (the step's per-expert token
+    # histogram) back; the H2D copy of step i+1 runs on a copy stream under step i's compute
+    # (double-buffered device inputs), all inside the timed region.
     x_host = x.detach().cpu().pin_memory()
     dy_host = dy.detach().cpu().pin_memory()
     counts_host = torch.empty((cfg.E,), dtype=torch.int32).pin_memory()
-    x_dev = torch.empty_like(x.detach())
-    dy_dev = torch.empty_like(dy)
-    from paper_2504_03871_b200.layer import _MoEFunction  # noqa: F401
+    x_dev = [torch.empty_like(x.detach()) for _ in range(2)]
+    dy_dev = [torch.empty_like(dy) for _ in range(2)]
+    copy_stream = torch.cuda.Stream(dev)
+    copied = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def e2e_step():
-        x_dev.copy_(x_host, non_blocking=True)
-        dy_dev.copy_(dy_host, non_blocking=True)
-        xin = x_dev.detach().requires_grad_()
+    def h2d(i):
+        b = i & 1
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(consumed[b])  # buffer b's previous step finished with it
+            x_dev[b].copy_(x_host, non_blocking=True)
+            dy_dev[b].copy_(dy_host, non_blocking=True)
+            copied[b].record(copy_stream)
+
+    def e2e_step(i):
+        b = i & 1
+        stream.wait_event(copied[b])
+        if i + 1 < args.steps + 1:
+            h2d(i + 1)
+        xin = x_dev[b].detach().requires_grad_()
         for p in params:
             p.grad = None
         y, idx = moe_forward(xin, params[0], params[1], params[2], cfg.k, args.max_ctas)
-        y.backward(dy_dev)
-        # step result read back: per-expert token histogram of this step
+        y.backward(dy_dev[b])
+        consumed[b].record(stream)
         counts = torch.bincount(idx.reshape(-1), minlength=cfg.E)
         counts_host.copy_(counts.to(torch.int32), non_blocking=True)
 
-    e2e_step()
+    for ev in consumed:
+        ev.record(stream)
+    h2d(0)
+    e2e_step(0)  # warm-up of the pipelined path (also prefetches step 1)
     barrier(ws)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    for i in range(1, args.steps + 1):
+        e2e_step(i)
     e1.record(stream)
     barrier(ws)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws)
     e2e = {"value": tokens_total / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": x_host.numel() * 2 + dy_host.numel() * 2,
            "d2h_bytes_per_step": cfg.E * 4,
-           "ms_per_step": round(e2e_ms / args.steps, 3)}
+           "ms_per_step": round(e2e_ms / args.steps, 3),
+           "note": "pinned H2D of each step's x and dY (prefetched one step ahead on a copy stream) "
+                   "+ D2H of the step's expert histogram, through moe_forward/backward"}
 
     out = {
         "metric": METRIC,

@@ -100,6 +100,19 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
                     const void* aux, int ld_aux, void* workspace, int max_ctas, void* stream);
 size_t hm_grouped_gemm_workspace_bytes(int mode, int E);
 
+/* Weight gradient over R segments (micro-batches) at once: out[e] (+)= sum_j A_j[seg_j(e)]^T . B_j[seg_j(e)]
+ * a_list/b_list: R host arrays of device pointers ([rows_j, M] and [rows_j, N] bf16); rows_list: R
+ * host ints; seg_offsets: device [R][E+1]; out bf16 (accumulate=0) or fp32 (accumulate=1,
+ * out += ...). One GEMM whose K loop runs over each expert's rows in every segment, so
+ * micro-batched weight gradients are formed once per layer instead of read-modify-written per
+ * micro-batch. workspace: hm_grouped_wgrad_multi_workspace_bytes(E, R), 128-byte aligned.
+ * R <= 16. Replaces the per-micro-batch part of EXP_B / OFF_EXP_B. */
+int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void* const* b_list,
+                           const int* rows_list, const int32_t* seg_offsets, int R, int E, int M,
+                           int N, void* out, int ldo, void* workspace, int max_ctas,
+                           void* stream);
+size_t hm_grouped_wgrad_multi_workspace_bytes(int E, int R);
+
 /* SwiGLU expert FFN forward over permuted rows:
  *   h[rows,2f]  = x_perm . w_ug[e]^T   (gate|up interleaved in 128-column blocks, saved for bwd)
  *   act[rows,f] = silu(gate) * up

@@ -370,6 +370,7 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
   if (rows == 0 && !wgrad) return 0;
 
   hm::GroupedGemmParams p{};
+  p.R = 1;
   p.seg_offsets = seg_offsets;
   p.E = E;
   p.M = M;
@@ -420,9 +421,11 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
     p.n_fastest = (M >= N) ? 1 : 0;
     // per-expert views (device side, no host sync on the expert sizes)
     CUtensorMap* maps = static_cast<CUtensorMap*>(workspace);
+    hm::SegBases bases{};
+    bases.a[0] = static_cast<const uint8_t*>(a);
+    bases.b[0] = static_cast<const uint8_t*>(b);
     hm::build_expert_maps_kernel<<<(E + 127) / 128, 128, 0, st>>>(
-        ma, mb, seg_offsets, E, static_cast<const uint8_t*>(a), static_cast<long>(M) * 2,
-        static_cast<const uint8_t*>(b), static_cast<long>(N) * 2, maps);
+        ma, mb, seg_offsets, E, 1, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
     if (int rc = check_launch("build_expert_maps")) return rc;
     p.expert_maps = maps;
   }
@@ -456,6 +459,60 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
     default:
       return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
   }
+}
+
+size_t hm_grouped_wgrad_multi_workspace_bytes(int E, int R) {
+  return static_cast<size_t>(2 * E) * R * sizeof(CUtensorMap);
+}
+
+int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void* const* b_list,
+                           const int* rows_list, const int32_t* seg_offsets, int R, int E, int M,
+                           int N, void* out, int ldo, void* workspace, int max_ctas,
+                           void* stream) {
+  if (R < 1 || R > hm::kMaxSegs) return fail(HM_E_SHAPE, "wgrad_multi: R=%d out of [1,%d]", R, hm::kMaxSegs);
+  if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "wgrad_multi: E=%d out of range", E);
+  if (M <= 0 || M % 8 || N <= 0 || N % 8 || ldo % 8) return fail(HM_E_SHAPE, "wgrad_multi: bad M/N/ldo");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 127u))
+    return fail(HM_E_ARG, "wgrad_multi: needs a 128-byte aligned workspace");
+  cudaStream_t st = S(stream);
+  hm::SegBases bases{};
+  for (int j = 0; j < R; ++j) {
+    if (!aligned16(a_list[j]) || !aligned16(b_list[j])) return fail(HM_E_ALIGN, "wgrad_multi: alignment");
+    bases.a[j] = static_cast<const uint8_t*>(a_list[j]);
+    bases.b[j] = static_cast<const uint8_t*>(b_list[j]);
+  }
+  const int rows0 = rows_list[0] > 0 ? rows_list[0] : 1;
+  CUtensorMap ma, mb;
+  uint64_t dims_a[2] = {(uint64_t)M, (uint64_t)rows0};
+  uint64_t str_a[1] = {(uint64_t)M * 2};
+  uint32_t box[2] = {64, 64};
+  if (int rc = make_map(&ma, a_list[0], 2, dims_a, str_a, box)) return rc;
+  uint64_t dims_b[2] = {(uint64_t)N, (uint64_t)rows0};
+  uint64_t str_b[1] = {(uint64_t)N * 2};
+  if (int rc = make_map(&mb, b_list[0], 2, dims_b, str_b, box)) return rc;
+  CUtensorMap* maps = static_cast<CUtensorMap*>(workspace);
+  hm::build_expert_maps_kernel<<<(E * R + 127) / 128, 128, 0, st>>>(
+      ma, mb, seg_offsets, E, R, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
+  if (int rc = check_launch("build_expert_maps")) return rc;
+  hm::GroupedGemmParams p{};
+  p.seg_offsets = seg_offsets;  // segment 0 row table doubles as the GROUP_M bookkeeping
+  p.R = R;
+  p.E = E;
+  p.M = M;
+  p.N = N;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.out_f32 = static_cast<float*>(out);
+  p.ldo = ldo;
+  p.n_fastest = (M >= N) ? 1 : 0;
+  p.expert_maps = maps;
+  const int ctas = gemm_ctas();
+  const long tile_m = 128L * ctas;
+  const long ub_tiles = static_cast<long>(E) * ((M + tile_m - 1) / tile_m) * ((N + 255) / 256);
+  if (accumulate)
+    return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_ACC_F32, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                     : launch_gemm<true, true, true, hm::EPI_ACC_F32, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+  return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
+                   : launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
 }
 
 int hm_grouped_ffn_fwd(const void* x_perm, int rows, const int32_t* seg_offsets, int E,

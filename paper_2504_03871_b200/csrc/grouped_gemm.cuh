@@ -43,8 +43,9 @@ constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 // CTAS = 2: a CTA pair computes a 256 x 256 tile with tcgen05.mma.cta_group::2 (UMMA M=256):
 //           each CTA stages its own 128 rows of A and half (128 columns) of B, the leader CTA
 //           issues the MMAs, each CTA's TMEM receives its 128 accumulator rows.
-constexpr int kBookkeepingBytes = 3072;
-constexpr int kGroupM = 8;  // raster group height (tiles)  // GemmShared, placed first; tiles start 1024-aligned
+constexpr int kBookkeepingBytes = 4096;  // GemmShared, placed first; tiles start 1024-aligned
+constexpr int kGroupM = 8;                // raster group height (tiles)
+constexpr int kMaxSegs = 16;              // wgrad: micro-batch segments per expert (K concatenation)
 
 template <int CTAS>
 struct TileCfg {
@@ -70,7 +71,8 @@ struct GroupedGemmParams {
   const __nv_bfloat16* aux;  // SWIGLU_BWD: h saved by the forward [rows, 2N]
   int ld_aux;
   int n_fastest;  // raster: 1 = n-tile index varies fastest within an expert
-  const CUtensorMap* expert_maps;  // GROUP_K: per-expert TMA views, [2e] = A rows, [2e+1] = B rows
+  const CUtensorMap* expert_maps;  // GROUP_K: per-(expert, segment) TMA views, [(e*R+j)*2] = A, +1 = B
+  int R;                           // GROUP_K: segments per expert (seg_offsets is [R][E+1])
   float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
   int dynamic;  // 1: one cluster per tile + cluster-launch-control work stealing; 0: persistent
 };
@@ -92,30 +94,38 @@ HM_DEV void acc_row32(float* dst, const float* v, int valid_cols) {
   }
 }
 
-// Per-expert TMA views for the variable-K weight gradient: copies of the whole-buffer maps
-// whose base address is moved to the expert's first row and whose row extent is m_e, so TMA
-// zero-fills every row past the expert's end (no contraction over a neighbour's rows).
+// Per-(expert, segment) TMA views for the variable-K weight gradient: copies of the whole-buffer
+// maps whose base address is moved to the first row of expert e in segment (micro-batch) j and
+// whose row extent is m_{e,j}, so TMA zero-fills every row past the segment's end (no
+// contraction over a neighbour's rows). The K loop of an expert runs over its R segments.
+struct SegBases {
+  const uint8_t* a[kMaxSegs];
+  const uint8_t* b[kMaxSegs];
+};
+
 __global__ void build_expert_maps_kernel(const __grid_constant__ CUtensorMap tmpl_a,
                                          const __grid_constant__ CUtensorMap tmpl_b,
-                                         const int* __restrict__ seg_offsets, int E,
-                                         const uint8_t* base_a, long row_bytes_a,
-                                         const uint8_t* base_b, long row_bytes_b,
+                                         const int* __restrict__ seg_offsets /*[R][E+1]*/, int E,
+                                         int R, const __grid_constant__ SegBases bases,
+                                         long row_bytes_a, long row_bytes_b,
                                          CUtensorMap* __restrict__ out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  const int s0 = seg_offsets[e];
-  const int me = seg_offsets[e + 1] - s0;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E * R) return;
+  const int e = i / R, j = i % R;
+  const int s0 = seg_offsets[j * (E + 1) + e];
+  const int me = seg_offsets[j * (E + 1) + e + 1] - s0;
   const uint32_t rows = me > 0 ? static_cast<uint32_t>(me) : 1u;
   const uint4* ta = reinterpret_cast<const uint4*>(&tmpl_a);
   const uint4* tb = reinterpret_cast<const uint4*>(&tmpl_b);
-  uint4* oa = reinterpret_cast<uint4*>(out + 2 * e);
-  uint4* ob = reinterpret_cast<uint4*>(out + 2 * e + 1);
+  CUtensorMap* ma = out + 2 * i;
+  uint4* oa = reinterpret_cast<uint4*>(ma);
+  uint4* ob = reinterpret_cast<uint4*>(ma + 1);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) { oa[i] = ta[i]; ob[i] = tb[i]; }
-  tensormap_set_address(out + 2 * e, base_a + static_cast<long>(s0) * row_bytes_a);
-  tensormap_set_dim(out + 2 * e, 1, rows);
-  tensormap_set_address(out + 2 * e + 1, base_b + static_cast<long>(s0) * row_bytes_b);
-  tensormap_set_dim(out + 2 * e + 1, 1, rows);
+  for (int q = 0; q < 8; ++q) { oa[q] = ta[q]; ob[q] = tb[q]; }
+  tensormap_set_address(ma, bases.a[j] + static_cast<long>(s0) * row_bytes_a);
+  tensormap_set_dim(ma, 1, rows);
+  tensormap_set_address(ma + 1, bases.b[j] + static_cast<long>(s0) * row_bytes_b);
+  tensormap_set_dim(ma + 1, 1, rows);
   tensormap_release();
 }
 
@@ -129,6 +139,7 @@ struct GemmShared {
   uint64_t tmem_empty[2];
   uint32_t tmem_base;
   int tile_prefix[kMaxExperts + 1];  // first global tile index of each expert
+  int nk[kMaxExperts];               // GROUP_K: K blocks of each expert over all segments
   int seg[kMaxExperts + 1];          // copy of seg_offsets
 };
 
@@ -241,6 +252,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       sh.tile_prefix[e] = acc;
       const int me = sh.seg[e + 1] - sh.seg[e];
       acc += (GROUP_K ? mtiles_fixed : (me + kTileM - 1) / kTileM) * ntiles;
+      if (GROUP_K) {
+        int nk = 0;
+        for (int j = 0; j < p.R; ++j) {
+          const int mj = p.seg_offsets[j * (E + 1) + e + 1] - p.seg_offsets[j * (E + 1) + e];
+          nk += (mj + kBK - 1) / kBK;
+        }
+        sh.nk[e] = nk;
+      }
     }
     sh.tile_prefix[E] = acc;
     for (int s = 0; s < kStages; ++s) {
@@ -281,30 +300,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = pol_a;
       uint32_t it = 0;
-      int mapped_e = -1;
       uint32_t ci = 0;
       for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
            tile = next_tile<CTAS, false>(sh, tile, tile_step, ci, true)) {
         if (tile >= total_tiles) continue;  // a stolen cluster index past the real tile count
         const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
         const int seg0 = sh.seg[tc.e];
-        const int me = sh.seg[tc.e + 1] - seg0;
-        const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
+        const int nk = GROUP_K ? sh.nk[tc.e] : (p.K + kBK - 1) / kBK;
         const CUtensorMap* mA = &map_a;
         const CUtensorMap* mB = &map_b;
-        if (GROUP_K) {
-          mA = p.expert_maps + 2 * tc.e;
-          mB = mA + 1;
-          if (nk > 0 && tc.e != mapped_e) {
-            tensormap_acquire(mA);
-            tensormap_acquire(mB);
-            mapped_e = tc.e;
-          }
-        }
         // this CTA's share of the tile: A rows (M) and B rows (N)
         const int m0 = tc.mt * kTileM + static_cast<int>(rank) * kBM;
         const int n0 = tc.nt * kBN + static_cast<int>(rank) * Cfg::kBRows;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        // GROUP_K: the K loop walks the expert's segments (micro-batches); kb_in = K block
+        // inside the current segment, read through that segment's TMA views
+        int seg_j = -1, kb_in = 0, seg_nk = 0;
+        for (int kb = 0; kb < nk; ++kb, ++it, ++kb_in) {
+          if (GROUP_K && kb_in == seg_nk) {
+            do {
+              ++seg_j;
+              const int* so = p.seg_offsets + seg_j * (E + 1) + tc.e;
+              seg_nk = (so[1] - so[0] + kBK - 1) / kBK;
+            } while (seg_nk == 0);
+            kb_in = 0;
+            mA = p.expert_maps + 2 * (tc.e * p.R + seg_j);
+            mB = mA + 1;
+            tensormap_acquire(mA);
+            tensormap_acquire(mB);
+          }
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
           mbar_wait(&sh.empty[s], ph ^ 1);
@@ -337,10 +360,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             // box {64, 64}; rows past the expert's end are zero-filled by TMA
 #pragma unroll
             for (int q = 0; q < 2; ++q)
-              tma_load_2d_any<CTAS>(sa + q * 8192, mA, bar, m0 + q * 64, kb * kBK, pol_a);
+              tma_load_2d_any<CTAS>(sa + q * 8192, mA, bar, m0 + q * 64, kb_in * kBK, pol_a);
 #pragma unroll
             for (int q = 0; q < Cfg::kBRows / 64; ++q)
-              tma_load_2d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb * kBK, pol_b);
+              tma_load_2d_any<CTAS>(sb + q * 8192, mB, bar, n0 + q * 64, kb_in * kBK, pol_b);
           }
         }
       }
@@ -355,9 +378,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
            tile = next_tile<CTAS, true>(sh, tile, tile_step, ci, lane == 0)) {
         if (tile >= total_tiles) continue;
         const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
-        const int seg0 = sh.seg[tc.e];
-        const int me = sh.seg[tc.e + 1] - seg0;
-        const int nk = GROUP_K ? (me + kBK - 1) / kBK : (p.K + kBK - 1) / kBK;
+        const int nk = GROUP_K ? sh.nk[tc.e] : (p.K + kBK - 1) / kBK;
         if (nk == 0) continue;  // epilogue writes zeros for this tile without touching TMEM
         const int acc = tcount & 1;
         const uint32_t aph = (tcount >> 1) & 1;
@@ -433,7 +454,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         row_ok = tc.mt * kTileM + row_in_tile < p.M;
         grow = static_cast<long>(tc.e) * p.M + tc.mt * kTileM + row_in_tile;
       }
-      if (GROUP_K && me == 0) {
+      if (GROUP_K && sh.nk[tc.e] == 0) {
         // empty expert: its weight gradient is exactly zero (nothing to add when accumulating)
         if (row_ok && EPI != EPI_ACC_F32) {
           float z[32];

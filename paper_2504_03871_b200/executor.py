@@ -153,6 +153,17 @@ class NativeBackend:
     def ffn_bwd_acc(self, dy, x, h, act, seg, w_ug, w_d, gw_ug, gw_d):
         return self.ops.grouped_ffn_bwd_acc(dy, x, h, act, seg, w_ug, w_d, gw_ug, gw_d, self.max_ctas)
 
+    def ffn_bwd_data(self, dy, x, h, act, seg, w_ug, w_d):
+        return self.ops.grouped_ffn_bwd_data(dy, x, h, act, seg, w_ug, w_d, self.max_ctas)
+
+    def ffn_wgrad_multi(self, parts, seg_lists, gw_ug, gw_d):
+        """parts: per micro-batch (dh, x, dy, act); one grouped GEMM per weight over all of them."""
+        seg = torch.tensor(seg_lists, dtype=torch.int32, device=self.device)
+        self.ops.grouped_wgrad_multi([p[0] for p in parts], [p[1] for p in parts], seg, gw_ug,
+                                     accumulate=True, max_ctas=self.max_ctas, name="gemm_wgrad_ug")
+        self.ops.grouped_wgrad_multi([p[2] for p in parts], [p[3] for p in parts], seg, gw_d,
+                                     accumulate=True, max_ctas=self.max_ctas, name="gemm_wgrad_down")
+
     def tensor(self, shape, dtype=None):
         return torch.empty(shape, dtype=dtype or self.dtype, device=self.device)
 
@@ -395,13 +406,28 @@ class ZpExecutor:
         self._exchange(l, j, self.dy_perm.get((l, j)), dy_recv, True, self.disp_group)
 
     def _exp_b(self, l, j):
+        """Data gradients now; the layer's weight gradients once, after its last micro-batch:
+        one grouped GEMM over all R micro-batches (K concatenation) instead of an fp32
+        read-modify-write of every expert gradient per micro-batch."""
         st, be = self.st, self.be
         seg = self.seg[(l, j)]
         n = max(seg[-1], 1)
-        dx = be.ffn_bwd_acc(self.dy_recv[(l, j)][:n], self.x_recv[(l, j)][:n], self.h_save[(l, j)],
-                            self.act[(l, j)], self.seg_t[(l, j)], st.w_ug[l], st.w_d[l],
-                            st.gw_ug[l], st.gw_d[l])
+        dy = self.dy_recv[(l, j)][:n]
+        dx, dh = be.ffn_bwd_data(dy, self.x_recv[(l, j)][:n], self.h_save[(l, j)], self.act[(l, j)],
+                                 self.seg_t[(l, j)], st.w_ug[l], st.w_d[l])
         self.dx_recv[(l, j)] = dx
+        self.dh[(l, j)] = dh
+        if j == self.R:
+            parts, segs = [], []
+            for jj in range(1, self.R + 1):
+                nn = max(self.seg[(l, jj)][-1], 1)
+                parts.append((self.dh[(l, jj)], self.x_recv[(l, jj)][:nn], self.dy_recv[(l, jj)][:nn],
+                              self.act[(l, jj)]))
+                segs.append(self.seg[(l, jj)])
+            be.ffn_wgrad_multi(parts, segs, st.gw_ug[l], st.gw_d[l])
+            for jj in range(1, self.R + 1):  # the layer's backward activations are done
+                self.dh.pop((l, jj), None)
+                self.h_save.pop((l, jj), None)
 
     def _comb_b(self, l, j):
         s, be = self.s, self.be
@@ -474,7 +500,7 @@ class ZpExecutor:
         self.events, marks = {}, {}
         for name in ("u", "z", "h_in", "route", "row_of", "x_perm", "my_counts", "counts", "send_off",
                      "recv_pos", "seg", "seg_t", "x_recv", "y_recv", "h_save", "act", "y_perm",
-                     "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm"):
+                     "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm", "dh"):
             setattr(self, name, {})
         self.wg_t = {}
         for gdict in (self.st.gw_ug, self.st.gw_d, self.st.gwg):

@@ -12,6 +12,7 @@ expert FFN -> EXP_F, ``costmodel.py:28-37``); their semantics come from the pape
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -283,6 +284,57 @@ def grouped_ffn_bwd(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: i
     grouped_gemm(_native.GEMM_WGRAD, dy_perm, act, seg_offsets, E, rows, d, f, 0, dw_d, f,
                  max_ctas=max_ctas, name="gemm_wgrad_down")
     return dx_perm, dw_ug, dw_d
+
+
+def grouped_ffn_bwd_data(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: int = 0):
+    """Data-gradient half of the FFN backward: dh = SwiGLU'(dy . w_d[e]), dx = dh . w_ug[e].
+    Returns (dx_perm, dh); the weight gradients are formed later by grouped_wgrad_multi."""
+    _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d)
+    rows, d = x_perm.shape
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    dh = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=x_perm.device)
+    dx_perm = torch.empty((rows, d), dtype=x_perm.dtype, device=x_perm.device)
+    grouped_gemm(_native.GEMM_BWD_DACT, dy_perm, w_d, seg_offsets, E, rows, 0, f, d, dh, 2 * f,
+                 aux=h, ld_aux=2 * f, max_ctas=max_ctas, name="gemm_bwd_dact")
+    grouped_gemm(_native.GEMM_BWD_DX, dh, w_ug, seg_offsets, E, rows, 0, d, 2 * f, dx_perm, d,
+                 max_ctas=max_ctas, name="gemm_bwd_dx")
+    return dx_perm, dh
+
+
+def grouped_wgrad_multi(a_list, b_list, seg_multi, out, accumulate: bool = True,
+                        max_ctas: int = 0, name: str = "gemm_wgrad_multi") -> None:
+    """out[e] (+)= sum_j a_list[j][seg_j(e)]^T . b_list[j][seg_j(e)] in ONE grouped GEMM whose K
+    loop runs over every segment (micro-batch). seg_multi: int32 [R, E+1] on the device."""
+    lib = _native.load()
+    R = len(a_list)
+    if not accumulate and (R > 16 or out.dtype != torch.bfloat16):
+        raise ValueError("non-accumulating grouped_wgrad_multi needs bf16 out and at most 16 segments")
+    if accumulate and out.dtype != torch.float32:
+        raise ValueError("accumulating grouped_wgrad_multi needs an fp32 out")
+    E = seg_multi.shape[1] - 1
+    M = a_list[0].shape[1]
+    N = b_list[0].shape[1]
+    dev = a_list[0].device
+    for j0 in range(0, R, 16):
+        a = a_list[j0:j0 + 16]
+        b = b_list[j0:j0 + 16]
+        r = len(a)
+        nbytes = lib.hm_grouped_wgrad_multi_workspace_bytes(E, r)
+        ws = torch.empty((nbytes + 128,), dtype=torch.uint8, device=dev)
+        off = (-ws.data_ptr()) % 128
+        ws = ws[off:off + nbytes]
+        ap = (ctypes.c_void_p * r)(*[t.data_ptr() for t in a])
+        bp = (ctypes.c_void_p * r)(*[t.data_ptr() for t in b])
+        rows = (ctypes.c_int * r)(*[t.shape[0] for t in a])
+        seg = seg_multi[j0:j0 + r].contiguous()
+        acc = 1 if (accumulate or j0 > 0) else 0
+        _tk = _begin(name)
+        rc = lib.hm_grouped_wgrad_multi(acc, ap, bp, rows, _ptr(seg), r, E, M, N, _ptr(out), N,
+                                        _ptr(ws), max_ctas, _stream())
+        _end(_tk)
+        _native.check(rc, "hm_grouped_wgrad_multi")
+        _count(2)
 
 
 def grouped_ffn_bwd_acc(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, gw_ug, gw_d,

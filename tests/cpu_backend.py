@@ -129,6 +129,36 @@ class CpuBackend:
             y = torch.cat([y, torch.zeros(x.shape[0] - y.shape[0], y.shape[1])])
         return y, cat(hs, 2 * f), cat(acts, f)
 
+    def ffn_bwd_data(self, dy, x, h, act, seg, w_ug, w_d):
+        wg, wu = self._split(w_ug)
+        seg = seg.tolist()
+        f = w_d.shape[2]
+        dx = torch.zeros_like(x)
+        dh = torch.zeros(x.shape[0], 2 * f)
+        for e in range(len(seg) - 1):
+            a0, a1 = seg[e], seg[e + 1]
+            g, u = h[a0:a1, :f], h[a0:a1, f:]
+            da = dy[a0:a1] @ w_d[e]
+            sg = torch.sigmoid(g)
+            dg = da * u * sg * (1 + g * (1 - sg))
+            du = da * torch.nn.functional.silu(g)
+            dx[a0:a1] = dg @ wg[e] + du @ wu[e]
+            dh[a0:a1] = torch.cat([dg, du], 1)
+        return dx, dh
+
+    def ffn_wgrad_multi(self, parts, seg_lists, gw_ug, gw_d):
+        f = gw_d.shape[2]
+        E = gw_d.shape[0]
+        for (dh, x, dy, act), seg in zip(parts, seg_lists):
+            for e in range(E):
+                a0, a1 = seg[e], seg[e + 1]
+                dg, du = dh[a0:a1, :f], dh[a0:a1, f:]
+                g_gate = dg.t() @ x[a0:a1]
+                g_up = du.t() @ x[a0:a1]
+                inter = torch.stack([g_gate.reshape(f // 128, 128, -1), g_up.reshape(f // 128, 128, -1)], 1)
+                gw_ug[e] += inter.reshape(2 * f, -1)
+                gw_d[e] += dy[a0:a1].t() @ act[a0:a1]
+
     def ffn_bwd_acc(self, dy, x, h, act, seg, w_ug, w_d, gw_ug, gw_d):
         wg, wu = self._split(w_ug)
         seg = seg.tolist()

@@ -47,6 +47,9 @@ int hm_abi_version(void);
 const char* hm_last_error(void);
 /* number of SMs of the current device (grid sizing for max_ctas) */
 int hm_num_sms(void);
+/* diagnostics: grouped-GEMM cycle accounting gathered when HM_GEMM_STATS=1 (8 counters, see
+ * csrc/grouped_gemm.cuh g_gemm_stats); reads and resets them, synchronising the device */
+int hm_gemm_stats(unsigned long long* out);
 
 /* ---- K1 router: logits (fixed-order fp32), top-k, softmax over the k, histogram, offsets ----
  * x[T,d] bf16, wg[d,E] bf16, bias[E] fp32 or NULL (logits = x . wg + bias). Outputs: idx[T,k] int32, w[T,k] fp32,

@@ -99,6 +99,8 @@ int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
   return 0;
 }
 
+int gemm_stats_enabled();
+
 template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
                 long ub_tiles, int max_ctas, cudaStream_t stream) {
@@ -115,6 +117,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
   // CTAs with static tile striding (the per-rank capacity-weight emulation).
   int grid;
   hm::GroupedGemmParams pp = p;
+  pp.stats = gemm_stats_enabled();
   if (max_ctas > 0) {
     grid = max_ctas < num_sms() ? max_ctas : num_sms();
     grid = (grid / CTAS) * CTAS;
@@ -144,6 +147,15 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
   return check_launch("grouped_gemm");
 }
 
+int gemm_stats_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("HM_GEMM_STATS");
+    v = (s && atoi(s) != 0) ? 1 : 0;
+  }
+  return v;
+}
+
 // CTA-pair (cta_group::2) tiles for the GROUP_M GEMMs unless HM_GEMM_CTAS=1
 int gemm_ctas() {
   static int v = 0;
@@ -159,6 +171,18 @@ int gemm_ctas() {
 extern "C" {
 
 int hm_abi_version(void) { return HM_ABI_VERSION; }
+
+// Read (and reset) the grouped-GEMM cycle accounting collected when HM_GEMM_STATS=1:
+// out[0] MMA waiting on TMA, [1] MMA waiting on a free accumulator, [2] MMA role cycles,
+// [3] producer waiting on free stages, [4] tiles, [5] CTAs. Synchronises the device.
+int hm_gemm_stats(unsigned long long* out) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out, hm::g_gemm_stats, 8 * sizeof(unsigned long long));
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(hm::g_gemm_stats, z, sizeof(z));
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "gemm_stats: %s", cudaGetErrorString(e));
+  return 0;
+}
 const char* hm_last_error(void) { return g_last_error.c_str(); }
 int hm_num_sms(void) { return num_sms(); }
 

@@ -75,6 +75,7 @@ struct GroupedGemmParams {
   int R;                           // GROUP_K: segments per expert (seg_offsets is [R][E+1])
   float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
   int dynamic;  // 1: one cluster per tile + cluster-launch-control work stealing; 0: persistent
+  int stats;    // accumulate g_gemm_stats
 };
 
 // out[0..31] += v[0..31] (fp32), masked to valid_cols
@@ -127,6 +128,17 @@ __global__ void build_expert_maps_kernel(const __grid_constant__ CUtensorMap tmp
   tensormap_set_address(ma + 1, bases.b[j] + static_cast<long>(s0) * row_bytes_b);
   tensormap_set_dim(ma + 1, 1, rows);
   tensormap_release();
+}
+
+// Optional cycle accounting (HM_GEMM_STATS=1): where the MMA issuer and the TMA producer wait.
+// [0] MMA waiting for smem stages (TMA not landed), [1] MMA waiting for a free TMEM accumulator
+// (epilogue behind), [2] MMA role total, [3] producer waiting for free stages, [4] tiles, [5] CTAs
+__device__ unsigned long long g_gemm_stats[8];
+
+HM_DEV unsigned long long clk() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
 }
 
 struct GemmShared {
@@ -300,6 +312,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = pol_a;
       uint32_t it = 0;
+      unsigned long long st_empty = 0;
       uint32_t ci = 0;
       for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
            tile = next_tile<CTAS, false>(sh, tile, tile_step, ci, true)) {
@@ -330,7 +343,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
+          const unsigned long long w0 = p.stats ? clk() : 0ull;
           mbar_wait(&sh.empty[s], ph ^ 1);
+          if (p.stats) st_empty += clk() - w0;
           uint8_t* sa = tiles + s * kStageBytes;
           uint8_t* sb = sa + kATileBytes;
           uint32_t bar;
@@ -367,11 +382,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
+      if (p.stats) atomicAdd(&g_gemm_stats[3], st_empty);
     }
   } else if (warp == 1) {
     // ======================= MMA issuer (leader CTA) =======================
     constexpr uint32_t idesc = make_idesc_bf16(kTileM, kBN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
     uint32_t it = 0, tcount = 0;
+    unsigned long long st_full = 0, st_tmem = 0, st_tiles = 0;
+    const unsigned long long st_t0 = clk();
     if (leader) {
       uint32_t ci = 0;
       for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
@@ -382,13 +400,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (nk == 0) continue;  // epilogue writes zeros for this tile without touching TMEM
         const int acc = tcount & 1;
         const uint32_t aph = (tcount >> 1) & 1;
+        unsigned long long w0 = p.stats ? clk() : 0ull;
         mbar_wait(&sh.tmem_empty[acc], aph ^ 1);
+        if (p.stats) { st_tmem += clk() - w0; ++st_tiles; }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
           const uint32_t ph = (it / kStages) & 1;
+          if (p.stats) w0 = clk();
           mbar_wait(&sh.full[s], ph);
+          if (p.stats) st_full += clk() - w0;
           tc_fence_after();
           uint8_t* sa = tiles + s * kStageBytes;
           uint8_t* sb = sa + kATileBytes;
@@ -415,6 +437,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           __syncwarp();
         }
         ++tcount;
+      }
+      if (p.stats && lane == 0) {
+        atomicAdd(&g_gemm_stats[0], st_full);
+        atomicAdd(&g_gemm_stats[1], st_tmem);
+        atomicAdd(&g_gemm_stats[2], clk() - st_t0);
+        atomicAdd(&g_gemm_stats[4], st_tiles);
+        atomicAdd(&g_gemm_stats[5], 1ull);
       }
     }
   } else if (warp == kSchedWarp) {

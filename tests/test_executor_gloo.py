@@ -124,9 +124,10 @@ def _close(a, b, tol=1e-4):
     (1, 1, (0, 2), False),
     (2, 2, (1, 0), True),
     (1, 2, (0, 1), False),
+    (4, 4, (1, 1), False),  # the 8-GPU layout of BASELINE C4 (2 experts per expert rank)
 ])
 def test_executor_matches_single_process_reference(M, N, offload, attention):
-    L, R, E, k, T, d, f = 2, 2, 4, 2, 16, 256, 128
+    L, R, E, k, T, d, f = 2, 2, (8 if N == 4 else 4), 2, 16, 256, 128
     args = (L, R, E, k, T, d, f, list(offload), attention)
     W = M + N
     ctx = mp.get_context("spawn")

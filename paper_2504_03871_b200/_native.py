@@ -12,7 +12,8 @@ import os
 import threading
 
 LIB_NAME = "libhetermoe_kernels.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("HM_KERNELS_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 # GEMM modes (include/hetermoe.h)
 GEMM_FWD_UPGATE = 0

@@ -53,7 +53,10 @@ struct TileCfg {
   static constexpr int kBRows = kBN / CTAS;           // B rows (N) staged per CTA
   static constexpr int kBTileBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CTAS == 1 ? 4 : 6;
+#ifndef HM_PAIR_STAGES
+#define HM_PAIR_STAGES 6
+#endif
+  static constexpr int kStages = CTAS == 1 ? 4 : HM_PAIR_STAGES;
   static constexpr int kSmemBytes = kBookkeepingBytes + kStages * kStageBytes;
 };
 constexpr int kGemmSmemBytes = TileCfg<1>::kSmemBytes;

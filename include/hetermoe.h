@@ -92,6 +92,33 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
 size_t hm_router_bwd_part_elems(int T, int d, int E, int k);
 int hm_transpose_bf16(const void* in, int R, int C, void* out, void* stream);
 
+/* ---- NVLink peer-memory transport (fused compute + dispatch/combine; the DISP and COMB lanes,
+ * taskgraph.py:56-59) ----
+ * dest_base[E]: device pointers (possibly peer-mapped) of each expert owner's receive buffer;
+ * dest_start[E]: first row of THIS sender's rows of expert e in that buffer. Row (t,s) of expert e
+ * is written to dest_base[e] + (dest_start[e] + row_of[t,s] - offsets[e]) * d. */
+int hm_dispatch_permute_p2p(const void* x, const int32_t* idx, const int32_t* chunk_base,
+                            const int32_t* offsets, int T, int d, int E, int k, void* x_perm,
+                            int32_t* row_src, int32_t* row_of, const unsigned long long* dest_base,
+                            const int32_t* dest_start, void* stream);
+/* combine backward whose dy_perm rows go straight to the owners (same addressing); dw local */
+int hm_combine_bwd_p2p(const void* dy, const void* y_perm, const int32_t* row_of, const int32_t* idx,
+                       const float* w, const int32_t* offsets, int T, int d, int k,
+                       const unsigned long long* dest_base, const int32_t* dest_start, float* dw,
+                       void* stream);
+/* grouped GEMM (HM_GEMM_FWD_DOWN / HM_GEMM_BWD_DX) whose epilogue stores output row r at the
+ * device pointer out_rows[r] (local or peer): the expert FFN's last GEMM fused with the return */
+int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* seg_offsets,
+                         int E, int rows, int M, int N, int K, void* out, int ldo, void* out2,
+                         int ldo2, const void* aux, int ld_aux, void* workspace,
+                         const unsigned long long* out_rows, int max_ctas, void* stream);
+/* after this stream's prior work: atomically add 1 (release, system scope) to n <= 8 counters
+ * (host array of device pointers, typically peer-mapped) */
+int hm_signal_peers(const unsigned long long* flag_ptrs, int n, void* stream);
+/* stall this stream until the local counters flags[i*stride] >= targets[i] (acquire, system) */
+int hm_wait_flags(const unsigned int* flags, int stride, const unsigned int* targets, int n,
+                  void* stream);
+
 /* ---- K3 grouped expert GEMM (tcgen05 / TMEM / TMA) ----
  * seg_offsets[E+1] (device) delimit each expert's rows of the activation buffers.
  * GROUP_M modes: a = activations [rows, K]; b = per-expert weights ([E][N][K] or [E][K][N]).

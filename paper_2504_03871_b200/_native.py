@@ -44,6 +44,11 @@ SIGNATURES = {
     "hm_transpose_bf16": (_I, [_P, _I, _I, _P, _P]),
     "hm_grouped_gemm": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P]),
     "hm_grouped_gemm_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
+    "hm_grouped_gemm_rows": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _P, _P, _I, _P]),
+    "hm_dispatch_permute_p2p": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "hm_combine_bwd_p2p": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P]),
+    "hm_signal_peers": (_I, [_P, _I, _P]),
+    "hm_wait_flags": (_I, [_P, _I, _P, _I, _P]),
     "hm_grouped_wgrad_multi": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _I, _P]),
     "hm_grouped_wgrad_multi_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
     "hm_grouped_ffn_fwd": (_I, [_P, _I, _P, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P]),

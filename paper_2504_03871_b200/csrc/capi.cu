@@ -365,6 +365,69 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   return 0;
 }
 
+int hm_dispatch_permute_p2p(const void* x, const int32_t* idx, const int32_t* chunk_base,
+                            const int32_t* offsets, int T, int d, int E, int k, void* x_perm,
+                            int32_t* row_src, int32_t* row_of, const unsigned long long* dest_base,
+                            const int32_t* dest_start, void* stream) {
+  if (T < 0 || d <= 0 || d % 256 != 0 || d / 256 > 16 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK)
+    return fail(HM_E_SHAPE, "permute_p2p: unsupported shape T=%d d=%d E=%d k=%d", T, d, E, k);
+  if (!aligned16(x) || (x_perm && !aligned16(x_perm))) return fail(HM_E_ALIGN, "permute_p2p: alignment");
+  if (T == 0) return 0;
+  cudaStream_t st = S(stream);
+  const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
+  auto xb = static_cast<const __nv_bfloat16*>(x);
+  auto xp = static_cast<__nv_bfloat16*>(x_perm);
+#define HM_P2P_CASE(V)                                                                        \
+  case V:                                                                                     \
+    hm::dispatch_permute_p2p_kernel<V><<<nchunk, 256, 0, st>>>(xb, idx, chunk_base, offsets, T, d, \
+                                                                E, k, xp, row_src, row_of,    \
+                                                                dest_base, dest_start);       \
+    break;
+  switch (d / 256) {
+    HM_P2P_CASE(1)
+    HM_P2P_CASE(2)
+    HM_P2P_CASE(4)
+    HM_P2P_CASE(8)
+    HM_P2P_CASE(16)
+    default:
+      return fail(HM_E_SHAPE, "permute_p2p: d=%d must be 256 x {1,2,4,8,16}", d);
+  }
+#undef HM_P2P_CASE
+  return check_launch("dispatch_permute_p2p");
+}
+
+int hm_combine_bwd_p2p(const void* dy, const void* y_perm, const int32_t* row_of, const int32_t* idx,
+                       const float* w, const int32_t* offsets, int T, int d, int k,
+                       const unsigned long long* dest_base, const int32_t* dest_start, float* dw,
+                       void* stream) {
+  if (T < 0 || d <= 0 || d % 8 != 0) return fail(HM_E_SHAPE, "combine_bwd_p2p: bad shape");
+  if (!aligned16(dy) || !aligned16(y_perm)) return fail(HM_E_ALIGN, "combine_bwd_p2p: alignment");
+  if (T == 0) return 0;
+  auto g = static_cast<const __nv_bfloat16*>(dy);
+  auto yp = static_cast<const __nv_bfloat16*>(y_perm);
+  HM_K_SWITCH(k, (hm::combine_bwd_p2p_kernel<K><<<row_grid(T), 256, 0, S(stream)>>>(g, yp, row_of, idx, w, offsets, T, d, dest_base, dest_start, dw)));
+  return check_launch("combine_bwd_p2p");
+}
+
+int hm_signal_peers(const unsigned long long* flag_ptrs, int n, void* stream) {
+  if (n < 0 || n > hm::kMaxPeers) return fail(HM_E_ARG, "signal_peers: n=%d", n);
+  if (n == 0) return 0;
+  hm::PeerFlags f{};
+  for (int i = 0; i < n; ++i) f.ptr[i] = flag_ptrs[i];
+  hm::signal_add_kernel<<<1, 32, 0, S(stream)>>>(f, n);
+  return check_launch("signal_peers");
+}
+
+int hm_wait_flags(const unsigned int* flags, int stride, const unsigned int* targets, int n,
+                  void* stream) {
+  if (n < 0 || n > hm::kMaxPeers) return fail(HM_E_ARG, "wait_flags: n=%d", n);
+  if (n == 0) return 0;
+  hm::FlagTargets t{};
+  for (int i = 0; i < n; ++i) t.v[i] = targets[i];
+  hm::wait_geq_kernel<<<1, 32, 0, S(stream)>>>(flags, stride, t, n);
+  return check_launch("wait_flags");
+}
+
 int hm_transpose_bf16(const void* in, int R, int C, void* out, void* stream) {
   if (R <= 0 || C <= 0) return fail(HM_E_SHAPE, "transpose: bad shape");
   dim3 grid((C + 31) / 32, (R + 31) / 32);
@@ -378,12 +441,27 @@ size_t hm_grouped_gemm_workspace_bytes(int mode, int E) {
   return (mode == HM_GEMM_WGRAD || mode == HM_GEMM_WGRAD_ACC) ? static_cast<size_t>(2 * E) * sizeof(CUtensorMap) : 0;
 }
 
+int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* seg_offsets,
+                         int E, int rows, int M, int N, int K, void* out, int ldo, void* out2,
+                         int ldo2, const void* aux, int ld_aux, void* workspace,
+                         const unsigned long long* out_rows, int max_ctas, void* stream);
+
 int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_offsets, int E,
                     int rows, int M, int N, int K, void* out, int ldo, void* out2, int ldo2,
                     const void* aux, int ld_aux, void* workspace, int max_ctas, void* stream) {
+  return hm_grouped_gemm_rows(mode, a, b, seg_offsets, E, rows, M, N, K, out, ldo, out2, ldo2, aux,
+                              ld_aux, workspace, nullptr, max_ctas, stream);
+}
+
+int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* seg_offsets,
+                         int E, int rows, int M, int N, int K, void* out, int ldo, void* out2,
+                         int ldo2, const void* aux, int ld_aux, void* workspace,
+                         const unsigned long long* out_rows, int max_ctas, void* stream) {
   if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "gemm: E=%d out of range", E);
   if (rows < 0 || N <= 0 || N % 8 != 0) return fail(HM_E_SHAPE, "gemm: bad rows/N");
-  if (!aligned16(a) || !aligned16(b) || !aligned16(out)) return fail(HM_E_ALIGN, "gemm: alignment");
+  if (!aligned16(a) || !aligned16(b) || (!out_rows && !aligned16(out))) return fail(HM_E_ALIGN, "gemm: alignment");
+  if (out_rows && mode != HM_GEMM_FWD_DOWN && mode != HM_GEMM_BWD_DX)
+    return fail(HM_E_ARG, "gemm: per-row destinations only for the plain-store GEMMs");
   if (ldo % 8 != 0) return fail(HM_E_ALIGN, "gemm: ldo must be a multiple of 8");
   cudaStream_t st = S(stream);
   const bool wgrad = (mode == HM_GEMM_WGRAD || mode == HM_GEMM_WGRAD_ACC);
@@ -402,6 +480,7 @@ int hm_grouped_gemm(int mode, const void* a, const void* b, const int32_t* seg_o
   p.K = K;
   p.out = static_cast<__nv_bfloat16*>(out);
   p.out_f32 = static_cast<float*>(out);
+  p.out_rows = out_rows;
   p.ldo = ldo;
   p.out2 = static_cast<__nv_bfloat16*>(out2);
   p.ldo2 = ldo2;

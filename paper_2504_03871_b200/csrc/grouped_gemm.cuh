@@ -79,6 +79,8 @@ struct GroupedGemmParams {
   float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
   int dynamic;  // 1: one cluster per tile + cluster-launch-control work stealing; 0: persistent
   int stats;    // accumulate g_gemm_stats
+  const unsigned long long* out_rows;  // EPI_STORE: optional per-output-row destination pointer
+                                       // (row r -> bf16* out_rows[r], may be a peer GPU's memory)
 };
 
 // out[0..31] += v[0..31] (fp32), masked to valid_cols
@@ -576,9 +578,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tmem_ld_32x32b_x32(t_row + c, r);
             tmem_ld_wait();
             if (row_ok && c < ncols_valid) {
-              if (EPI == EPI_STORE)
-                store_row32(p.out + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
-                            min(32, ncols_valid - c));
+              if (EPI == EPI_STORE) {
+                __nv_bfloat16* dst = p.out_rows
+                    ? reinterpret_cast<__nv_bfloat16*>(p.out_rows[grow]) + n0 + c
+                    : p.out + grow * p.ldo + n0 + c;
+                store_row32(dst, reinterpret_cast<float*>(r), min(32, ncols_valid - c));
+              }
               else
                 acc_row32(p.out_f32 + grow * p.ldo + n0 + c, reinterpret_cast<float*>(r),
                           min(32, ncols_valid - c));

@@ -538,6 +538,147 @@ __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int n
   dwg[i] = __float2bfloat16_rn(s);
 }
 
+
+// ------------------------------------------------------------------------------------------
+// NVLink peer-memory transport (the fused dispatch / combine of the ZP executor).
+//
+// Fused permute + dispatch: each token row is read once and written (a) optionally to the local
+// permuted buffer and (b) straight into the receive buffer of the expert's owner, which may be
+// another GPU (a peer-mapped pointer): row (t, s) of expert e lands at
+//   dest_base[e] + (dest_start[e] + (row_of[t,s] - offsets[e])) * d.
+template <int VPL>
+__global__ void __launch_bounds__(256)
+    dispatch_permute_p2p_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
+                                const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ offsets,
+                                int T, int d, int E, int k, __nv_bfloat16* __restrict__ x_perm,
+                                int32_t* __restrict__ row_src, int32_t* __restrict__ row_of,
+                                const unsigned long long* __restrict__ dest_base,
+                                const int32_t* __restrict__ dest_start) {
+  __shared__ int s_idx[kChunk * kMaxTopK];
+  __shared__ int s_row[kChunk * kMaxTopK];
+  const int c = blockIdx.x;
+  const int tbeg = c * kChunk;
+  const int nt = min(kChunk, T - tbeg);
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) s_idx[i] = idx[static_cast<long>(tbeg) * k + i];
+  __syncthreads();
+  assign_rows_ballot(s_idx, s_row, chunk_base + static_cast<long>(c) * E, nt * k, E);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+    const int r = s_row[i];
+    row_of[static_cast<long>(tbeg) * k + i] = r;
+    if (row_src) row_src[r] = tbeg + i / k;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int tt = warp; tt < nt; tt += 8) {
+    const long t = tbeg + tt;
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+    uint4 v[VPL];
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) v[q] = __ldg(src + q * 32 + lane);
+    for (int s = 0; s < k; ++s) {
+      const int r = s_row[tt * k + s];
+      const int e = s_idx[tt * k + s];
+      if (x_perm) {
+        uint4* dst = reinterpret_cast<uint4*>(x_perm + static_cast<long>(r) * d);
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) dst[q * 32 + lane] = v[q];
+      }
+      __nv_bfloat16* peer = reinterpret_cast<__nv_bfloat16*>(dest_base[e]) +
+                            (static_cast<long>(dest_start[e]) + r - offsets[e]) * d;
+      uint4* dst = reinterpret_cast<uint4*>(peer);
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) dst[q * 32 + lane] = v[q];
+    }
+  }
+}
+
+// Fused combine backward + dispatch of dY: dy_perm row (t, s) = w[t,s] * dy[t] goes straight to
+// the owner's receive buffer (same addressing as the forward dispatch); dw[t,s] = <dy[t], y_perm[row]>.
+template <int K>
+__global__ void __launch_bounds__(256)
+    combine_bwd_p2p_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ y_perm,
+                           const int32_t* __restrict__ row_of, const int32_t* __restrict__ idx,
+                           const float* __restrict__ w, const int32_t* __restrict__ offsets, int T, int d,
+                           const unsigned long long* __restrict__ dest_base,
+                           const int32_t* __restrict__ dest_start, float* __restrict__ dw) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nv = d / 8;
+  for (int t = warp; t < T; t += nwarps) {
+    int rows[K];
+    float ws[K], dot[K];
+    uint4* dsts[K];
+    for (int s = 0; s < K; ++s) {
+      rows[s] = row_of[static_cast<long>(t) * K + s];
+      ws[s] = w[static_cast<long>(t) * K + s];
+      dot[s] = 0.f;
+      const int e = idx[static_cast<long>(t) * K + s];
+      dsts[s] = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dest_base[e]) +
+                                         (static_cast<long>(dest_start[e]) + rows[s] - offsets[e]) * d);
+    }
+    for (int q = lane; q < nv; q += 32) {
+      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy + static_cast<long>(t) * d) + q);
+      const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g);
+      float gf[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z) gf[z] = bf16_to_f32(gh[z]);
+      for (int s = 0; s < K; ++s) {
+        const uint4 yv = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q);
+        const uint16_t* yh = reinterpret_cast<const uint16_t*>(&yv);
+#pragma unroll
+        for (int z = 0; z < 8; ++z) dot[s] = __fmaf_rn(gf[z], bf16_to_f32(yh[z]), dot[s]);
+        uint4 o;
+        o.x = pack_bf16x2(ws[s] * gf[0], ws[s] * gf[1]);
+        o.y = pack_bf16x2(ws[s] * gf[2], ws[s] * gf[3]);
+        o.z = pack_bf16x2(ws[s] * gf[4], ws[s] * gf[5]);
+        o.w = pack_bf16x2(ws[s] * gf[6], ws[s] * gf[7]);
+        dsts[s][q] = o;
+      }
+    }
+    for (int s = 0; s < K; ++s) {
+      float v = dot[s];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) dw[static_cast<long>(t) * K + s] = v;
+    }
+  }
+}
+
+// Completion signalling between GPUs: after the data writes of this stream completed, add 1 to
+// each listed (peer-mapped) 32-bit counter with release semantics at system scope.
+constexpr int kMaxPeers = 8;
+struct PeerFlags {
+  unsigned long long ptr[kMaxPeers];
+};
+struct FlagTargets {
+  unsigned int v[kMaxPeers];
+};
+
+__global__ void signal_add_kernel(const __grid_constant__ PeerFlags flags, int n) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    __threadfence_system();
+    unsigned int* f = reinterpret_cast<unsigned int*>(flags.ptr[i]);
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(f) : "memory");
+  }
+}
+
+// Wait (acquire, system scope) until local counters flags[i*stride] reach targets[i]. The
+// counters are written by peers over NVLink, never by another kernel of this GPU.
+__global__ void wait_geq_kernel(const unsigned int* __restrict__ flags, int stride,
+                                const __grid_constant__ FlagTargets targets, int n) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    const unsigned int want = targets.v[i];
+    const unsigned int* f = flags + static_cast<long>(i) * stride;
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    } while (static_cast<int>(v - want) < 0);
+  }
+}
+
 // bf16 transpose [R][C] -> [C][R] (router weight layout helper)
 __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ in, int R, int C,
                                       __nv_bfloat16* __restrict__ out) {

@@ -378,3 +378,102 @@ def split_gate_up(w_ug: torch.Tensor, block: int = BLOCK_F):
     f = two_f // 2
     v = w_ug.reshape(E, f // block, 2, block, d)
     return v[:, :, 0].reshape(E, f, d), v[:, :, 1].reshape(E, f, d)
+
+
+# ---------------------------------------------------------------------------------------------
+# NVLink peer-memory transport (fused compute + dispatch / combine; used by executor.P2P)
+
+
+def dispatch_permute_p2p(x: torch.Tensor, r: Routing, dest_base: torch.Tensor, dest_start: torch.Tensor,
+                         keep_local: bool = True):
+    """Fused permute + dispatch: each routed row goes to its expert owner's receive buffer
+    (dest_base[e] + (dest_start[e] + row - offsets[e]) * d, possibly a peer GPU); optionally also
+    to the local permuted buffer. Returns (x_perm or None, row_of)."""
+    _require_cuda(x, dest_base, dest_start)
+    T, d = x.shape
+    k = r.idx.shape[1]
+    E = r.counts.shape[0]
+    x_perm = torch.empty((T * k, d), dtype=x.dtype, device=x.device) if keep_local else None
+    row_of = torch.empty((T, k), dtype=torch.int32, device=x.device)
+    _tk = _begin("dispatch_permute_p2p")
+    rc = _native.load().hm_dispatch_permute_p2p(
+        _ptr(x), _ptr(r.idx), _ptr(r.chunk_base), _ptr(r.offsets), T, d, E, k, _ptr(x_perm), None,
+        _ptr(row_of), _ptr(dest_base), _ptr(dest_start), _stream())
+    _end(_tk)
+    _native.check(rc, "hm_dispatch_permute_p2p")
+    _count(1)
+    return x_perm, row_of
+
+
+def combine_bwd_p2p(dy, y_perm, row_of, r: Routing, dest_base, dest_start):
+    """Fused combine backward + dispatch of dY rows to the owners; returns dw [T,k] (local)."""
+    _require_cuda(dy, y_perm, row_of, dest_base, dest_start)
+    T, k = row_of.shape
+    d = dy.shape[1]
+    dw = torch.empty((T, k), dtype=torch.float32, device=dy.device)
+    _tk = _begin("combine_bwd_p2p")
+    rc = _native.load().hm_combine_bwd_p2p(
+        _ptr(dy), _ptr(y_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(r.offsets), T, d, k,
+        _ptr(dest_base), _ptr(dest_start), _ptr(dw), _stream())
+    _end(_tk)
+    _native.check(rc, "hm_combine_bwd_p2p")
+    _count(1)
+    return dw
+
+
+def _gemm_rows(mode, a, b, seg, E, rows, N, K, out_rows, max_ctas, name):
+    _tk = _begin(name)
+    rc = _native.load().hm_grouped_gemm_rows(mode, _ptr(a), _ptr(b), _ptr(seg), E, rows, 0, N, K, None,
+                                             N, None, 0, None, 0, None, _ptr(out_rows), max_ctas,
+                                             _stream())
+    _end(_tk)
+    _native.check(rc, "hm_grouped_gemm_rows")
+    _count(1)
+
+
+def grouped_ffn_fwd_rows(x_perm, seg_offsets, w_ug, w_d, out_rows, max_ctas: int = 0):
+    """Forward whose down-projection epilogue writes output row r to out_rows[r] (the combine
+    return fused into the GEMM). Returns (h, act)."""
+    _require_cuda(x_perm, seg_offsets, w_ug, w_d, out_rows)
+    rows, d = x_perm.shape
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    h = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=x_perm.device)
+    act = torch.empty((rows, f), dtype=x_perm.dtype, device=x_perm.device)
+    grouped_gemm(_native.GEMM_FWD_UPGATE, x_perm, w_ug, seg_offsets, E, rows, 0, 2 * f, d, act, f,
+                 out2=h, ldo2=2 * f, max_ctas=max_ctas, name="gemm_fwd_upgate")
+    _gemm_rows(_native.GEMM_FWD_DOWN, act, w_d, seg_offsets, E, rows, d, f, out_rows, max_ctas,
+               "gemm_fwd_down_p2p")
+    return h, act
+
+
+def grouped_ffn_bwd_data_rows(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, out_rows, max_ctas: int = 0):
+    """Data-gradient backward whose dX epilogue writes row r to out_rows[r]. Returns dh."""
+    _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, out_rows)
+    rows, d = x_perm.shape
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    dh = torch.empty((rows, 2 * f), dtype=x_perm.dtype, device=x_perm.device)
+    grouped_gemm(_native.GEMM_BWD_DACT, dy_perm, w_d, seg_offsets, E, rows, 0, f, d, dh, 2 * f,
+                 aux=h, ld_aux=2 * f, max_ctas=max_ctas, name="gemm_bwd_dact")
+    _gemm_rows(_native.GEMM_BWD_DX, dh, w_ug, seg_offsets, E, rows, d, 2 * f, out_rows, max_ctas,
+               "gemm_bwd_dx_p2p")
+    return dh
+
+
+def signal_peers(flag_ptrs) -> None:
+    """+1 (release, system scope) on each listed device counter after this stream's prior work."""
+    n = len(flag_ptrs)
+    arr = (ctypes.c_ulonglong * max(n, 1))(*flag_ptrs)
+    rc = _native.load().hm_signal_peers(arr, n, _stream())
+    _native.check(rc, "hm_signal_peers")
+    _count(1 if n else 0)
+
+
+def wait_flags(flags_ptr: int, stride: int, targets) -> None:
+    """Stall the current stream until counters flags[i*stride] >= targets[i]."""
+    n = len(targets)
+    arr = (ctypes.c_uint * max(n, 1))(*targets)
+    rc = _native.load().hm_wait_flags(flags_ptr, stride, arr, n, _stream())
+    _native.check(rc, "hm_wait_flags")
+    _count(1 if n else 0)

@@ -366,7 +366,8 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200 import build_zp_graph, derive_task_durations
     from paper_2504_03871_b200 import ops
     from paper_2504_03871_b200.configs import CONFIGS
-    from paper_2504_03871_b200.executor import NativeBackend, ZpExecutor, ZpLayerShape, execute
+    from paper_2504_03871_b200.executor import (NativeBackend, ZpExecutor, ZpLayerShape, ZpP2PExecutor,
+                                                execute)
     from paper_2504_03871_b200.planner import make_zp_spec, plan_assignment
     from paper_2504_03871_b200.profiler import measure_durations
     from paper_2504_03871_b200.simulator import compute_metrics, validate_measured_timeline
@@ -396,7 +397,8 @@ def run_zp(args, ws, rank, local):
     disp = dist.new_group(list(range(ws)))
     comb = dist.new_group(list(range(ws)))
     be = NativeBackend(dev, max_ctas=exp_ctas if rank >= M else 0)
-    ex = ZpExecutor(graph, shape, M, N, rank, be, disp, comb, seed=1234)
+    ex_cls = ZpP2PExecutor if args.transport == "p2p" else ZpExecutor
+    ex = ex_cls(graph, shape, M, N, rank, be, disp, comb, seed=1234)
     for _ in range(args.warmup):
         ex.run()
     l0 = ops.LAUNCHES[0]
@@ -442,7 +444,8 @@ def run_zp(args, ws, rank, local):
             "E": c.E, "k": c.k, "d_model": c.d, "d_ff": c.f, "layers": args.layers,
             "microbatches": args.microbatches, "tokens_per_microbatch": args.mb_tokens,
             "attention_block": not args.no_attention, "parallelism": f"zp{M}+{N}",
-            "asym_ea_offload": list(assignment.offload), "expert_capacity": args.expert_capacity,
+            "asym_ea_offload": list(assignment.offload),
+            "transport": args.transport, "expert_capacity": args.expert_capacity,
             "router_skew_zipf": args.router_skew,
             "measured_durations_ns": durs,
             "l2": "activations and weights exceed the 126 MB L2; no flush",
@@ -534,6 +537,8 @@ def main():
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
     ap.add_argument("--router-skew", type=float, default=0.0,
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="ZP: NVLink peer-memory transport fused into the kernels, or NCCL send/recv")
     ap.add_argument("--expert-capacity", type=float, default=1.0,
                     help="ZP: capacity weight of expert ranks (grouped-GEMM grid = ceil(w*SMs))")
     args = ap.parse_args()

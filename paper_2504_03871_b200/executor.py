@@ -158,7 +158,7 @@ class NativeBackend:
 
     def ffn_wgrad_multi(self, parts, seg_lists, gw_ug, gw_d):
         """parts: per micro-batch (dh, x, dy, act); one grouped GEMM per weight over all of them."""
-        seg = torch.tensor(seg_lists, dtype=torch.int32, device=self.device)
+        seg = self.h2d(seg_lists, torch.int32)
         self.ops.grouped_wgrad_multi([p[0] for p in parts], [p[1] for p in parts], seg, gw_ug,
                                      accumulate=True, max_ctas=self.max_ctas, name="gemm_wgrad_ug")
         self.ops.grouped_wgrad_multi([p[2] for p in parts], [p[3] for p in parts], seg, gw_d,
@@ -167,8 +167,32 @@ class NativeBackend:
     def tensor(self, shape, dtype=None):
         return torch.empty(shape, dtype=dtype or self.dtype, device=self.device)
 
+    def h2d(self, data, dtype):
+        """Small host table -> device on the current stream without a host sync (pinned staging;
+        the caching host allocator keeps the staging buffer alive until the copy is done)."""
+        return torch.as_tensor(data, dtype=dtype).pin_memory().to(self.device, non_blocking=True)
+
     def seg_tensor(self, offsets):
-        return torch.tensor(offsets, dtype=torch.int32, device=self.device)
+        return self.h2d(offsets, torch.int32)
+
+    # peer-memory transport (ZpP2PExecutor)
+    def permute_p2p(self, u, r, dest_base, dest_start):
+        return self.ops.dispatch_permute_p2p(u, r, dest_base, dest_start, keep_local=True)
+
+    def combine_bwd_p2p(self, dy, y_perm, row_of, r, dest_base, dest_start):
+        return self.ops.combine_bwd_p2p(dy, y_perm, row_of, r, dest_base, dest_start)
+
+    def ffn_fwd_rows(self, x, seg, w_ug, w_d, out_rows):
+        return self.ops.grouped_ffn_fwd_rows(x, seg, w_ug, w_d, out_rows, self.max_ctas)
+
+    def ffn_bwd_data_rows(self, dy, x, h, act, seg, w_ug, w_d, out_rows):
+        return self.ops.grouped_ffn_bwd_data_rows(dy, x, h, act, seg, w_ug, w_d, out_rows, self.max_ctas)
+
+    def signal(self, flag_ptrs):
+        self.ops.signal_peers(flag_ptrs)
+
+    def wait_flags(self, flags_ptr, targets):
+        self.ops.wait_flags(flags_ptr, 1, targets)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -280,14 +304,16 @@ class ZpExecutor:
     def _ev(self, key):
         return self.events.get(key)
 
-    def _recv_layout(self, l: int, counts_all):
-        """Expert-major receive layout on this rank for layer l: for each owned expert, the rows
-        of every attention rank in rank order. Returns (segment offsets per owned expert,
-        {(a, e): (recv_off, rows)})."""
+    def _recv_layout(self, l: int, counts_all, rank: Optional[int] = None):
+        """Expert-major receive layout on `rank` (default: this rank) for layer l: for each
+        owned expert, the rows of every attention rank in rank order. Returns (segment offsets
+        per owned expert, {(a, e): (recv_off, rows)})."""
         seg = [0]
         pos = {}
         off = 0
-        for e in self.st.own[l - 1]:
+        owners = self.st.owners[l - 1]
+        me = self.rank if rank is None else rank
+        for e in (e for e in range(self.s.E) if owners[e] == me):
             for a in range(self.M):
                 c = counts_all[a][e]
                 pos[(a, e)] = (off, c)
@@ -354,9 +380,14 @@ class ZpExecutor:
         self.z[(l, j)] = z
         zd = z.detach()
         r = be.router(zd, st.wg[l], s.k, st.bias[l])
-        x_perm, row_of = be.permute(zd, r)
-        self.route[(l, j)], self.row_of[(l, j)], self.x_perm[(l, j)] = r, row_of, x_perm
+        self.route[(l, j)] = r
         self.my_counts[(l, j)] = be.counts(r)
+        self.zd[(l, j)] = zd
+        self._attn_permute(l, j, zd, r)
+
+    def _attn_permute(self, l, j, zd, r):
+        x_perm, row_of = self.be.permute(zd, r)
+        self.row_of[(l, j)], self.x_perm[(l, j)] = row_of, x_perm
 
     def _disp_f(self, l, j):
         s, be = self.s, self.be
@@ -451,13 +482,16 @@ class ZpExecutor:
         dh = h.grad
         if l > 1:
             self.dh_next[(l - 1, j)] = dh
-            dy_perm, dw = be.combine_bwd(dh, self.y_perm[(l - 1, j)], self.row_of[(l - 1, j)],
-                                         self.route[(l - 1, j)])
-            self.dy_perm[(l - 1, j)], self.dw[(l - 1, j)] = dy_perm, dw
+            self._attn_combine_bwd(l - 1, j, dh)
         # free the layer's activations early
         self.u.pop((l, j), None)
         self.z.pop((l, j), None)
+        self.zd.pop((l, j), None)
         self.h_in.pop((l, j), None)
+
+    def _attn_combine_bwd(self, l, j, dh):
+        dy_perm, dw = self.be.combine_bwd(dh, self.y_perm[(l, j)], self.row_of[(l, j)], self.route[(l, j)])
+        self.dy_perm[(l, j)], self.dw[(l, j)] = dy_perm, dw
 
     _HANDLERS = {
         K.ATTN_F: ("_attn_f", "compute", "attn"),
@@ -498,7 +532,7 @@ class ZpExecutor:
         """One forward+backward iteration. Returns {task_id: (start_ns, end_ns)} measured on
         this rank (relative to the iteration start event), for the tasks it took part in."""
         self.events, marks = {}, {}
-        for name in ("u", "z", "h_in", "route", "row_of", "x_perm", "my_counts", "counts", "send_off",
+        for name in ("u", "z", "zd", "h_in", "route", "row_of", "x_perm", "my_counts", "counts", "send_off",
                      "recv_pos", "seg", "seg_t", "x_recv", "y_recv", "h_save", "act", "y_perm",
                      "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm", "dh"):
             setattr(self, name, {})
@@ -531,6 +565,225 @@ class ZpExecutor:
         be.synchronize()
         out = {tid: (be.elapsed_ns(t0, a), be.elapsed_ns(t0, b)) for tid, (a, b) in marks.items()}
         return out
+
+
+# ---------------------------------------------------------------------------------------------
+# peer-memory (NVLink) transport
+
+
+def p2p_dispatch_dest(owners, recv_pos_by_rank, a: int, E: int):
+    """Sender side of the fused dispatch for attention rank a: per expert, the owner rank and the
+    first row of a's rows inside the owner's expert-major receive buffer."""
+    dest_rank = [owners[e] for e in range(E)]
+    dest_start = [recv_pos_by_rank[owners[e]][(a, e)][0] for e in range(E)]
+    return dest_rank, dest_start
+
+
+def p2p_return_rows(recv_pos, send_off_by_rank):
+    """Owner side of the fused return: for every received row (expert-major order) the attention
+    rank it came from and its row in that rank's permuted buffer, so the owner's last GEMM can
+    store the row straight back (numpy arrays; rows in receive order)."""
+    import numpy as np
+
+    n = sum(c for _, c in recv_pos.values())
+    ranks = np.zeros(n, dtype=np.int64)
+    rows = np.zeros(n, dtype=np.int64)
+    for (a, e), (off, c) in recv_pos.items():
+        if c:
+            ranks[off:off + c] = a
+            rows[off:off + c] = send_off_by_rank[a][e] + np.arange(c)
+    return ranks, rows
+
+
+class PeerArena:
+    """Symmetric device memory over all ranks of `group` (torch symmetric memory: the same
+    allocation mapped into every peer over NVLink), carved into per-(layer, micro-batch) slots:
+
+      [flags: 4 kinds x W uint32 counters | per (l, j): x | dy (owner receive, `cap` rows each)
+                                               | y | dx (attention receive, T*k rows each)]
+
+    Every rank has the same layout, so a slot's offset is rank-independent and a peer's slot
+    address is ``ptrs[peer] + offset``. Flag counters are monotonic over the arena's lifetime."""
+
+    FLAG_BYTES = 4096
+    DF, CF, DB, CB = range(4)
+
+    def __init__(self, L: int, R: int, cap: int, tk: int, d: int, W: int, group, device):
+        import torch.distributed._symmetric_memory as symm
+
+        self.L, self.R, self.cap, self.tk, self.d, self.W = L, R, cap, tk, d, W
+        self.rb = d * 2
+        self.slot_bytes = (2 * cap + 2 * tk) * self.rb
+        nbytes = self.FLAG_BYTES + L * R * self.slot_bytes
+        self.buf = symm.empty(nbytes, dtype=torch.uint8, device=device)
+        self.handle = symm.rendezvous(self.buf, group)
+        self.ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        self.rank = self.handle.rank
+        self.buf[: self.FLAG_BYTES].zero_()
+        torch.cuda.synchronize(device)
+        dist.barrier(group=group)
+
+    def offset(self, l: int, j: int, which: str) -> int:
+        base = self.FLAG_BYTES + ((l - 1) * self.R + (j - 1)) * self.slot_bytes
+        cap, tk, rb = self.cap, self.tk, self.rb
+        return base + {"x": 0, "dy": cap * rb, "y": 2 * cap * rb, "dx": (2 * cap + tk) * rb}[which]
+
+    def view(self, l, j, which, rows):
+        off = self.offset(l, j, which)
+        return self.buf[off:off + rows * self.rb].view(torch.bfloat16).view(rows, self.d)
+
+    def addr(self, rank, l, j, which) -> int:
+        return self.ptrs[rank] + self.offset(l, j, which)
+
+    def flag_addr(self, rank, kind, sender) -> int:
+        return self.ptrs[rank] + (kind * self.W + sender) * 4
+
+    def local_flags(self, kind) -> int:
+        return self.ptrs[self.rank] + kind * self.W * 4
+
+
+class ZpP2PExecutor(ZpExecutor):
+    """ZP executor whose dispatch / combine move rows over NVLink peer memory instead of NCCL
+    send/recv, each fused into the kernel that produces the rows:
+
+      DISP_F  permute kernel stores every routed row straight into its owner's receive slot
+      EXP_F   the down-projection GEMM epilogue stores each output row into its sender's y slot
+      DISP_B  combine-backward kernel stores w*dY rows into the owners' dy slots
+      EXP_B   the dX GEMM epilogue stores each row into its sender's dx slot
+
+    A transfer completes with a release add on the receiver's flag counter (one per kind and
+    sender) after the producing kernel; the receiver's stream waits (acquire) for the count of
+    exchanges it expects. Only the expert-count all-gather (one per layer and micro-batch, as in
+    the NCCL path) stays a collective. Same task graph, streams and issue order as ZpExecutor."""
+
+    def __init__(self, graph, shape, M, N, rank, backend, disp_group=None, comb_group=None,
+                 seed: int = 0, durations_hint=None):
+        super().__init__(graph, shape, M, N, rank, backend, disp_group, comb_group, seed, durations_hint)
+        if self.W > 8:
+            raise ValueError("p2p transport supports at most 8 ranks (one NVSwitch domain)")
+        s = shape
+        max_own = max(sum(1 for o in ow if o == r) for ow in self.st.owners for r in range(self.W))
+        cap = s.tokens_per_mb * M * min(s.k, max_own)  # worst case rows one owner can receive
+        self.arena = PeerArena(self.L, self.R, cap, s.tokens_per_mb * s.k, s.d, self.W,
+                               disp_group, backend.device)
+        if self.arena.rank != rank:
+            raise ValueError("the dispatch group must rank processes like the world")
+        self.expected = [[0] * self.W for _ in range(4)]  # per kind, per sender: exchanges seen
+        self.owner_sets = [sorted(set(ow)) for ow in self.st.owners]
+
+    # signalling helpers
+    def _signal(self, kind, receivers):
+        a = self.arena
+        self.be.signal([a.flag_addr(r, kind, self.rank) for r in receivers])
+
+    def _wait(self, kind, senders):
+        exp = self.expected[kind]
+        for s_ in senders:
+            exp[s_] += 1
+        self.be.wait_flags(self.arena.local_flags(kind), exp)
+
+    # task handlers
+    def _attn_permute(self, l, j, zd, r):
+        pass  # the permute runs fused with the dispatch, once the receive layout is known
+
+    def _disp_f(self, l, j):
+        s, be, ar = self.s, self.be, self.arena
+        mine = self.my_counts.get((l, j))
+        if mine is None:
+            mine = be.tensor((s.E,), torch.int32).zero_()
+        gathered = [be.tensor((s.E,), torch.int32) for _ in range(self.W)]
+        dist.all_gather(gathered, mine.to(torch.int32), group=self.disp_group)
+        allc = torch.stack(gathered).cpu()  # the one host sync per (layer, micro-batch)
+        counts_all = [[int(v) for v in allc[a].tolist()] for a in range(self.M)]
+        self.counts[(l, j)] = counts_all
+        owners = self.st.owners[l - 1]
+        send_off = {a: self._send_offsets(counts_all[a]) for a in range(self.M)}
+        pos_by = {o: self._recv_layout(l, counts_all, o)[1] for o in self.owner_sets[l - 1]}
+        seg, pos = self._recv_layout(l, counts_all)
+        self.seg[(l, j)], self.recv_pos[(l, j)] = seg, pos
+        if self.is_attn:
+            dest_rank, dest_start = p2p_dispatch_dest(owners, pos_by, self.rank, s.E)
+            self.dest_start[(l, j)] = st_t = be.h2d(dest_start, torch.int32)
+            self.dest_x[(l, j)] = bx = be.h2d([ar.addr(o, l, j, "x") for o in dest_rank], torch.int64)
+            self.dest_dy[(l, j)] = be.h2d([ar.addr(o, l, j, "dy") for o in dest_rank], torch.int64)
+            x_perm, row_of = be.permute_p2p(self.zd[(l, j)], self.route[(l, j)], bx, st_t)
+            self.x_perm[(l, j)], self.row_of[(l, j)] = x_perm, row_of
+            self._signal(ar.DF, self.owner_sets[l - 1])
+        if seg[-1] or self.st.own[l - 1]:
+            if self.st.own[l - 1]:
+                self._wait(ar.DF, range(self.M))
+            ranks, rows = p2p_return_rows(pos, send_off)
+            y_addr = [ar.addr(a, l, j, "y") for a in range(self.M)]
+            import numpy as np
+
+            out = np.asarray(y_addr, dtype=np.int64)[ranks] + rows * ar.rb if len(ranks) else np.zeros(1, np.int64)
+            self.out_rows[(l, j)] = be.h2d(out, torch.int64)
+        self.x_recv[(l, j)] = ar.view(l, j, "x", max(seg[-1], 1))
+
+    def _exp_f(self, l, j):
+        st, be = self.st, self.be
+        seg = self.seg[(l, j)]
+        self.seg_t[(l, j)] = seg_t = be.seg_tensor(seg)
+        x = self.x_recv[(l, j)]
+        h, act = be.ffn_fwd_rows(x, seg_t, st.w_ug[l], st.w_d[l], self.out_rows[(l, j)])
+        self.h_save[(l, j)], self.act[(l, j)] = h, act
+
+    def _comb_f(self, l, j):
+        ar = self.arena
+        if self.st.own[l - 1]:
+            self._signal(ar.CF, range(self.M))
+        if self.is_attn:
+            self._wait(ar.CF, self.owner_sets[l - 1])
+            self.y_perm[(l, j)] = ar.view(l, j, "y", self.s.tokens_per_mb * self.s.k)
+
+    def _attn_combine_bwd(self, l, j, dh):
+        pass  # fused with the dY dispatch in DISP_B(l, j)
+
+    def _disp_b(self, l, j):
+        be, ar = self.be, self.arena
+        if self.is_attn:
+            if l == self.L:
+                self.dh_next[(l, j)] = self.out_grads[j]
+            r = self.route[(l, j)]
+            self.dw[(l, j)] = be.combine_bwd_p2p(self.dh_next[(l, j)], self.y_perm[(l, j)], self.row_of[(l, j)],
+                                                 r, self.dest_dy[(l, j)], self.dest_start[(l, j)])
+            self._signal(ar.DB, self.owner_sets[l - 1])
+        if self.st.own[l - 1]:
+            self._wait(ar.DB, range(self.M))
+        self.dy_recv[(l, j)] = ar.view(l, j, "dy", max(self.seg[(l, j)][-1], 1))
+
+    def _exp_b(self, l, j):
+        st, be, ar = self.st, self.be, self.arena
+        seg = self.seg[(l, j)]
+        if (l, j) not in self.out_rows_dx:
+            delta = ar.offset(l, j, "dx") - ar.offset(l, j, "y")
+            self.out_rows_dx[(l, j)] = self.out_rows[(l, j)] + delta
+        dh = be.ffn_bwd_data_rows(self.dy_recv[(l, j)], self.x_recv[(l, j)], self.h_save[(l, j)],
+                                  self.act[(l, j)], self.seg_t[(l, j)], st.w_ug[l], st.w_d[l],
+                                  self.out_rows_dx[(l, j)])
+        self.dh[(l, j)] = dh
+        if j == self.R:
+            parts, segs = [], []
+            for jj in range(1, self.R + 1):
+                parts.append((self.dh[(l, jj)], self.x_recv[(l, jj)], self.dy_recv[(l, jj)], self.act[(l, jj)]))
+                segs.append(self.seg[(l, jj)])
+            be.ffn_wgrad_multi(parts, segs, st.gw_ug[l], st.gw_d[l])
+            for jj in range(1, self.R + 1):
+                self.dh.pop((l, jj), None)
+                self.h_save.pop((l, jj), None)
+
+    def _comb_b(self, l, j):
+        ar = self.arena
+        if self.st.own[l - 1]:
+            self._signal(ar.CB, range(self.M))
+        if self.is_attn:
+            self._wait(ar.CB, self.owner_sets[l - 1])
+            self.dx_perm[(l, j)] = ar.view(l, j, "dx", self.s.tokens_per_mb * self.s.k)
+
+    def run(self) -> dict:
+        for name in ("dest_start", "dest_x", "dest_dy", "out_rows", "out_rows_dx"):
+            setattr(self, name, {})
+        return super().run()
 
 
 def merge_rank_intervals(graph: TaskGraph, per_rank: list, M: int) -> Timeline:

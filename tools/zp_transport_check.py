@@ -1,0 +1,128 @@
+"""Equivalence + timing of the two ZP transports on real GPUs (run under torchrun, 2-8 ranks):
+the NCCL send/recv executor (ZpExecutor) and the fused NVLink peer-memory executor
+(ZpP2PExecutor) run the same seeded iteration; every gradient must agree, then both are timed.
+
+  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/zp_transport_check.py [--big]
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2504_03871_b200 import ExpertAssignment, build_zp_graph, derive_task_durations  # noqa: E402
+from paper_2504_03871_b200.executor import (NativeBackend, ZpExecutor, ZpLayerShape,  # noqa: E402
+                                            ZpP2PExecutor)
+from paper_2504_03871_b200.planner import make_zp_spec  # noqa: E402
+
+
+def grads(ex):
+    st = ex.st
+    out = {}
+    for l in range(1, ex.L + 1):
+        for name, t in (("gw_ug", st.gw_ug.get(l)), ("gw_d", st.gw_d.get(l)), ("gwg", st.gwg.get(l)),
+                        ("wqkv", st.wqkv[l].grad if l in st.wqkv else None),
+                        ("wo", st.wo[l].grad if l in st.wo else None)):
+            if t is not None:
+                out[f"{name}{l}"] = t.detach().float().clone()
+    return out
+
+
+def zero_attn_grads(ex):
+    for d in (ex.st.wqkv, ex.st.wo):
+        for t in d.values():
+            t.grad = None
+
+
+def timed(ex, iters):
+    ex.run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        ex.run()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / iters], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true", help="C2 shapes (d=4096, f=14336)")
+    ap.add_argument("--offload", type=int, default=-1)
+    ap.add_argument("--iters", type=int, default=3)
+    args = ap.parse_args()
+    os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
+    # attention backward (SDPA) may accumulate with atomics; the check wants run-to-run
+    # determinism so that any difference is the transport's
+    torch.use_deterministic_algorithms(True, warn_only=True)
+    dist.init_process_group("nccl")
+    W, rank = dist.get_world_size(), dist.get_rank()
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    M = W // 2
+    N = W - M
+    if args.big:
+        E, k, d, f, T, L, R = 8, 2, 4096, 14336, 2048, 2, 4
+    else:
+        E, k, d, f, T, L, R = 8, 2, 512, 512, 512, 2, 3
+    off = args.offload if args.offload >= 0 else (1 if E // N > 1 else 0)
+    spec = make_zp_spec(M, N, L, R, E, k, T, d, attn_fwd_ns=3000, expert_layer_fwd_ns=4000,
+                        single_expert_fwd_ns=3000, dispatch_ns=100, combine_ns=100)
+    graph = build_zp_graph(spec, derive_task_durations(spec), ExpertAssignment(tuple([off] * L)),
+                           mode="zp-full")
+    shape = ZpLayerShape(E, k, d, f, T)
+    disp = dist.new_group(list(range(W)))
+    comb = dist.new_group(list(range(W)))
+    be = NativeBackend(dev)
+    results = {}
+    ex_n = ZpExecutor(graph, shape, M, N, rank, be, disp, comb, seed=5)
+    ex_n.run()
+    torch.cuda.synchronize()
+    g_n = grads(ex_n)
+    zero_attn_grads(ex_n)
+    ex_n.run()  # run-to-run noise floor of the NCCL executor itself
+    torch.cuda.synchronize()
+    self_rel = max(float((a - b).norm() / a.norm().clamp_min(1e-30)) for a, b in
+                   zip(g_n.values(), grads(ex_n).values()))
+    ex_p = ZpP2PExecutor(graph, shape, M, N, rank, be, disp, comb, seed=5)
+    worst = 0.0
+    for it in range(2):  # the second iteration re-uses the arena and the monotonic flags
+        zero_attn_grads(ex_p)
+        ex_p.run()
+        torch.cuda.synchronize()
+        g_p = grads(ex_p)
+        for key, a in g_n.items():
+            b = g_p[key]
+            rel = float((a - b).norm() / a.norm().clamp_min(1e-30))
+            worst = max(worst, rel)
+            if it == 0:
+                results[key] = {"rel": rel, "bitwise": bool(torch.equal(a, b))}
+    zero_attn_grads(ex_n)
+    zero_attn_grads(ex_p)
+    ms_n = timed(ex_n, args.iters)
+    ms_p = timed(ex_p, args.iters)
+    wt = torch.tensor([worst, self_rel], device=dev)
+    dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+    worst, self_rel = float(wt[0]), float(wt[1])
+    if rank == 0:
+        print(json.dumps({"world": W, "M": M, "N": N, "shape": [E, k, d, f, T, L, R], "offload": off,
+                          "worst_rel_err": worst, "nccl_rerun_rel_err": self_rel, "rank0": results,
+                          "ms_per_iter": {"nccl": ms_n, "p2p": ms_p}}))
+    dist.barrier()
+    dist.destroy_process_group()
+    if worst > max(1e-3, 4 * self_rel):
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()

@@ -414,6 +414,8 @@ def run_zp(args, ws, rank, local):
     ms = max_over_ranks(ev0.elapsed_time(ev1), ws)
     launches = (ops.LAUNCHES[0] - l0) // args.steps
     tl = execute(graph, ex)  # one more iteration, measured per task
+    hw = torch.tensor([ex.host_wait_s], device=dev)
+    dist.all_reduce(hw, op=dist.ReduceOp.MAX)
     tokens_iter = args.mb_tokens * M * args.microbatches
     value = tokens_iter * args.layers * args.steps / (ms / 1e3)
     if rank != 0:
@@ -464,6 +466,23 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200 import simulate, default_orders
 
     out["zp"]["simulated_makespan_ms"] = simulate(graph, default_orders(graph)).makespan / 1e6
+    # the same schedule replayed with each compute task at its measured duration: what the
+    # executor would reach with no issue stalls (communication tasks keep their planned time)
+    import dataclasses
+
+    from paper_2504_03871_b200.taskgraph import TaskGraph
+
+    comm = {"DispF", "CombF", "DispB", "CombB"}
+    newt = []
+    for t in graph.tasks:
+        ranks = range(0, M) if t.device == "attn" else range(M, ws)
+        ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in ranks if t.id in tl.per_rank[r]]
+        dur = t.duration if (t.kind.value in comm or not ds) else int(sum(ds) / len(ds))
+        newt.append(dataclasses.replace(t, duration=dur))
+    g2 = TaskGraph(graph.mode, graph.layers, graph.microbatches, tuple(newt), graph.edges,
+                   graph.assignment, graph.forward_only)
+    out["zp"]["resimulated_makespan_ms"] = simulate(g2, default_orders(g2)).makespan / 1e6
+    out["zp"]["host_count_wait_ms_max_rank"] = round(float(hw) * 1e3, 3)
     _emit(out)
 
 

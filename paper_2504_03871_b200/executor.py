@@ -37,6 +37,7 @@ from __future__ import annotations
 import contextlib
 import math
 import os
+import time
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -91,6 +92,10 @@ class ZpLayerShape:
 
 class NativeBackend:
     """Product backend: sm_100a kernels (``ops``) on three CUDA streams of one device."""
+
+    # communication is stream-ordered (NCCL / device flags), so the executor may defer a
+    # task's host-blocking half without changing any communicator's op order on the device
+    defer_host_sync = True
 
     def __init__(self, device, max_ctas: int = 0):
         from . import ops  # requires the built extension; fails loudly otherwise
@@ -321,6 +326,28 @@ class ZpExecutor:
             seg.append(off)
         return seg, pos
 
+    def _disp_f(self, l, j):
+        """DISP_F, first half: enqueue the expert-count all-gather over the dispatch group.
+        The second half (`_disp_f_finish`: the host reads the counts — the one host sync per
+        (layer, micro-batch), since the receive layout sizes the owners' buffers and GEMM
+        launches — then the row transfer) is deferred by the issue loop until a later task
+        needs it, so the host keeps issuing other streams' work while the counts travel."""
+        s, be = self.s, self.be
+        mine = self.my_counts.get((l, j))
+        if mine is None:
+            mine = be.tensor((s.E,), torch.int32).zero_()
+        gathered = [be.tensor((s.E,), torch.int32) for _ in range(self.W)]
+        dist.all_gather(gathered, mine.to(torch.int32), group=self.disp_group)
+        return lambda: self._disp_f_finish(l, j, gathered)
+
+    def _counts_wait(self, l, j, gathered):
+        t0 = time.perf_counter()
+        allc = torch.stack(gathered).cpu()
+        self.host_wait_s += time.perf_counter() - t0
+        counts_all = [[int(v) for v in allc[a].tolist()] for a in range(self.M)]
+        self.counts[(l, j)] = counts_all
+        return counts_all
+
     def _send_offsets(self, counts_row):
         off, acc = [], 0
         for c in counts_row:
@@ -389,16 +416,9 @@ class ZpExecutor:
         x_perm, row_of = self.be.permute(zd, r)
         self.row_of[(l, j)], self.x_perm[(l, j)] = row_of, x_perm
 
-    def _disp_f(self, l, j):
+    def _disp_f_finish(self, l, j, gathered):
         s, be = self.s, self.be
-        mine = self.my_counts.get((l, j))
-        if mine is None:
-            mine = be.tensor((s.E,), torch.int32).zero_()
-        gathered = [be.tensor((s.E,), torch.int32) for _ in range(self.W)]
-        dist.all_gather(gathered, mine.to(torch.int32), group=self.disp_group)
-        allc = torch.stack(gathered).cpu()  # the one host sync per (layer, micro-batch)
-        counts_all = [[int(v) for v in allc[a].tolist()] for a in range(self.M)]
-        self.counts[(l, j)] = counts_all
+        counts_all = self._counts_wait(l, j, gathered)
         for a in range(self.M):
             self.send_off[(l, j, a)] = self._send_offsets(counts_all[a])
         seg, pos = self._recv_layout(l, counts_all)
@@ -528,6 +548,58 @@ class ZpExecutor:
             raise IndexError(f"rank {self.rank}: router index out of range at L{task.layer} M{task.microbatch}")
 
     # ------------------------------------------------------------------ iteration
+    def _host_preds(self, tasks, preds):
+        """Per task, the nearest ancestors this rank takes part in: a task may need host state
+        (e.g. the receive layout) from a local task two edges up, through a task it skips."""
+        mine = {t.id for t in tasks}
+        near: dict = {}
+
+        def nearest(tid):
+            stack, acc, seen = list(preds[tid]), set(), set()
+            while stack:
+                p = stack.pop()
+                if p in seen:
+                    continue
+                seen.add(p)
+                if p in mine:
+                    acc.add(p)
+                else:
+                    stack.extend(preds[p])
+            return acc
+
+        for t in tasks:
+            near[t.id] = nearest(t.id)
+        return near
+
+    def _issue(self, task, preds, marks, pending, host_preds) -> None:
+        """Issue one task on its lane's stream after its dependencies' events. Deferred halves of
+        earlier tasks run first when this task depends on them or shares their lane."""
+        be = self.be
+        meth, lane, _ = self._HANDLERS[task.kind]
+        for pid in [p for p, (_, pl, _) in pending.items() if pl == lane or p in host_preds[task.id]]:
+            self._finish(pid, pending, marks)
+        with be.on(lane):
+            for p in preds[task.id]:
+                be.wait(self.events.get(p))
+            start = be.mark()
+            fin = getattr(self, meth)(task.layer, task.microbatch)
+            if fin is not None:
+                pending[task.id] = (fin, lane, start)
+                if not getattr(be, "defer_host_sync", False):
+                    self._finish(task.id, pending, marks)
+                return
+            end = be.mark()
+        self.events[task.id] = end
+        marks[task.id] = (start, end)
+
+    def _finish(self, tid, pending, marks) -> None:
+        fin, lane, start = pending.pop(tid)
+        with self.be.on(lane):
+            fin()
+            end = self.be.mark()
+        self.events[tid] = end
+        marks[tid] = (start, end)
+
     def run(self) -> dict:
         """One forward+backward iteration. Returns {task_id: (start_ns, end_ns)} measured on
         this rank (relative to the iteration start event), for the tasks it took part in."""
@@ -537,6 +609,7 @@ class ZpExecutor:
                      "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm", "dh"):
             setattr(self, name, {})
         self.wg_t = {}
+        self.host_wait_s = 0.0
         for gdict in (self.st.gw_ug, self.st.gw_d, self.st.gwg):
             for t in gdict.values():
                 t.zero_()
@@ -548,20 +621,17 @@ class ZpExecutor:
             t0 = be.mark()
         preds = {t.id: list(self.g.predecessors(t.id)) for t in self.g.tasks}
         debug = os.environ.get("HM_ZP_DEBUG") == "1"
-        for task in self.issue_order:
-            if not self._participates(task):
-                continue
-            meth, lane, _ = self._HANDLERS[task.kind]
-            with be.on(lane):
-                for p in preds[task.id]:
-                    be.wait(self.events.get(p))
-                start = be.mark()
-                getattr(self, meth)(task.layer, task.microbatch)
-                end = be.mark()
+        mine = [t for t in self.issue_order if self._participates(t)]
+        host_preds = self._host_preds(mine, preds)
+        pending: dict = {}
+        for task in mine:
+            self._issue(task, preds, marks, pending, host_preds)
             if debug:
+                for pid in list(pending):
+                    self._finish(pid, pending, marks)
                 self._debug_check(task)
-            self.events[task.id] = end
-            marks[task.id] = (start, end)
+        for pid in list(pending):
+            self._finish(pid, pending, marks)
         be.synchronize()
         out = {tid: (be.elapsed_ns(t0, a), be.elapsed_ns(t0, b)) for tid, (a, b) in marks.items()}
         return out
@@ -686,16 +756,9 @@ class ZpP2PExecutor(ZpExecutor):
     def _attn_permute(self, l, j, zd, r):
         pass  # the permute runs fused with the dispatch, once the receive layout is known
 
-    def _disp_f(self, l, j):
+    def _disp_f_finish(self, l, j, gathered):
         s, be, ar = self.s, self.be, self.arena
-        mine = self.my_counts.get((l, j))
-        if mine is None:
-            mine = be.tensor((s.E,), torch.int32).zero_()
-        gathered = [be.tensor((s.E,), torch.int32) for _ in range(self.W)]
-        dist.all_gather(gathered, mine.to(torch.int32), group=self.disp_group)
-        allc = torch.stack(gathered).cpu()  # the one host sync per (layer, micro-batch)
-        counts_all = [[int(v) for v in allc[a].tolist()] for a in range(self.M)]
-        self.counts[(l, j)] = counts_all
+        counts_all = self._counts_wait(l, j, gathered)
         owners = self.st.owners[l - 1]
         send_off = {a: self._send_offsets(counts_all[a]) for a in range(self.M)}
         pos_by = {o: self._recv_layout(l, counts_all, o)[1] for o in self.owner_sets[l - 1]}

@@ -13,6 +13,7 @@ expert FFN -> EXP_F, ``costmodel.py:28-37``); their semantics come from the pape
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import torch
@@ -21,12 +22,15 @@ from . import _native
 
 BLOCK_F = 128  # gate/up interleave block of the fused W_ug layout
 
-# number of native kernel launches issued through this module (bench.py's gpu_launches)
+# number of native kernel launches issued through this module (bench.py's gpu_launches);
+# the executor issues from one thread per stream, hence the lock
 LAUNCHES = [0]
+_LAUNCH_LOCK = threading.Lock()
 
 
 def _count(n: int) -> None:
-    LAUNCHES[0] += n
+    with _LAUNCH_LOCK:
+        LAUNCHES[0] += n
 
 
 class KernelTimer:

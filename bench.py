@@ -392,8 +392,14 @@ def run_zp(args, ws, rank, local):
                         asym_ea=not args.no_asym_ea, gamma=Fraction(durs["gamma_x100"], 100),
                         **plan_durs)
     dur = derive_task_durations(spec)
-    assignment = plan_assignment(spec, dur)
-    graph = build_zp_graph(spec, dur, assignment, mode="zp-full")
+    if args.schedule == "distep":  # lockstep ablation (no cross-micro-batch overlap, no offload)
+        from paper_2504_03871_b200 import build_distep_graph
+
+        graph = build_distep_graph(spec, dur)
+        assignment = graph.assignment
+    else:
+        assignment = plan_assignment(spec, dur)
+        graph = build_zp_graph(spec, dur, assignment, mode="zp-full")
     disp = dist.new_group(list(range(ws)))
     comb = dist.new_group(list(range(ws)))
     be = NativeBackend(dev, max_ctas=exp_ctas if rank >= M else 0)
@@ -440,14 +446,14 @@ def run_zp(args, ws, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded randn inputs, random-init weights)",
         "config": {
-            "workload": (f"ZP {M} attention + {N} expert ranks: {args.layers}-layer {c.name}-shaped MoE "
+            "workload": (f"{'ZP' if args.schedule == 'zp' else 'DistEP lockstep'} {M} attention + {N} expert ranks: {args.layers}-layer {c.name}-shaped MoE "
                          f"transformer stack, {args.microbatches} micro-batches x {args.mb_tokens} tokens per "
                          f"attention rank; value counts MoE-layer tokens (tokens x layers) per second"),
             "E": c.E, "k": c.k, "d_model": c.d, "d_ff": c.f, "layers": args.layers,
             "microbatches": args.microbatches, "tokens_per_microbatch": args.mb_tokens,
             "attention_block": not args.no_attention, "parallelism": f"zp{M}+{N}",
             "asym_ea_offload": list(assignment.offload),
-            "transport": args.transport, "expert_capacity": args.expert_capacity,
+            "transport": args.transport, "schedule": args.schedule, "expert_capacity": args.expert_capacity,
             "router_skew_zipf": args.router_skew,
             "measured_durations_ns": durs,
             "l2": "activations and weights exceed the 126 MB L2; no flush",
@@ -556,6 +562,8 @@ def main():
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
     ap.add_argument("--router-skew", type=float, default=0.0,
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
+    ap.add_argument("--schedule", default="zp", choices=["zp", "distep"],
+                    help="ZP: zebra-parallel schedule, or the DistEP lockstep ablation")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="ZP: NVLink peer-memory transport fused into the kernels, or NCCL send/recv")
     ap.add_argument("--expert-capacity", type=float, default=1.0,

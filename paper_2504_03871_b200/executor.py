@@ -241,8 +241,9 @@ class ZpExecutor:
     def __init__(self, graph: TaskGraph, shape: ZpLayerShape, M: int, N: int, rank: int,
                  backend, disp_group=None, comb_group=None, seed: int = 0,
                  durations_hint: Optional[dict] = None):
-        if graph.mode != "zp-full":
-            raise ValueError("the executor runs zp-full graphs (layer-L experts + loss turnaround)")
+        if graph.mode not in ("zp-full", "distep"):
+            raise ValueError("the executor runs zp-full graphs (layer-L experts + loss turnaround) "
+                             "or their DistEP lockstep ablation")
         if shape.E % N:
             raise ValueError("N must divide E")
         self.g, self.s, self.M, self.N, self.rank = graph, shape, M, N, rank

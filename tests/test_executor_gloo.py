@@ -24,12 +24,15 @@ def _free_port():
 
 
 def _build(M, N, L, R, E, k, T, d, f, offload):
-    from paper_2504_03871_b200 import ExpertAssignment, build_zp_graph, derive_task_durations
+    from paper_2504_03871_b200 import (ExpertAssignment, build_distep_graph, build_zp_graph,
+                                       derive_task_durations)
     from paper_2504_03871_b200.planner import make_zp_spec
 
     spec = make_zp_spec(M, N, L, R, E, k, T, d, attn_fwd_ns=3000, expert_layer_fwd_ns=4000,
                         single_expert_fwd_ns=3000, dispatch_ns=100, combine_ns=100)
     dur = derive_task_durations(spec)
+    if offload == "distep":  # the lockstep ablation (no offload)
+        return build_distep_graph(spec, dur)
     return build_zp_graph(spec, dur, ExpertAssignment(tuple(offload)), mode="zp-full")
 
 
@@ -125,10 +128,11 @@ def _close(a, b, tol=1e-4):
     (2, 2, (1, 0), True),
     (1, 2, (0, 1), False),
     (4, 4, (1, 1), False),  # the 8-GPU layout of BASELINE C4 (2 experts per expert rank)
+    (2, 2, "distep", False),  # DistEP lockstep ablation on the same executor
 ])
 def test_executor_matches_single_process_reference(M, N, offload, attention):
     L, R, E, k, T, d, f = 2, 2, (8 if N == 4 else 4), 2, 16, 256, 128
-    args = (L, R, E, k, T, d, f, list(offload), attention)
+    args = (L, R, E, k, T, d, f, offload if offload == "distep" else list(offload), attention)
     W = M + N
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

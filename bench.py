@@ -380,7 +380,16 @@ def run_zp(args, ws, rank, local):
     exp_ctas = 0 if args.expert_capacity >= 1.0 else int(math.ceil(args.expert_capacity * sms))
     shape = ZpLayerShape(c.E, c.k, c.d, c.f, args.mb_tokens, attention=not args.no_attention,
                          router_skew=args.router_skew)
-    durs = measure_durations(shape, M, N, expert_max_ctas=exp_ctas, device=dev)
+    loads = None
+    if args.router_skew and not args.no_balanced_placement:
+        # skewed router: expected per-expert loads (rank 0's measurement) drive a load-balanced
+        # expert placement and the busiest-rank expert timing
+        from paper_2504_03871_b200.profiler import measure_loads
+
+        lt = torch.tensor(measure_loads(shape, device=dev), dtype=torch.int64, device=dev)
+        dist.broadcast(lt, 0)
+        loads = [int(v) for v in lt.tolist()]
+    durs = measure_durations(shape, M, N, expert_max_ctas=exp_ctas, device=dev, loads=loads)
     # every rank must plan identically: use rank 0's measurement
     t = torch.tensor([durs[k] for k in sorted(durs)], dtype=torch.int64, device=dev)
     dist.broadcast(t, 0)
@@ -404,7 +413,7 @@ def run_zp(args, ws, rank, local):
     comb = dist.new_group(list(range(ws)))
     be = NativeBackend(dev, max_ctas=exp_ctas if rank >= M else 0)
     ex_cls = ZpP2PExecutor if args.transport == "p2p" else ZpExecutor
-    ex = ex_cls(graph, shape, M, N, rank, be, disp, comb, seed=1234)
+    ex = ex_cls(graph, shape, M, N, rank, be, disp, comb, seed=1234, expert_loads=loads)
     for _ in range(args.warmup):
         ex.run()
     l0 = ops.LAUNCHES[0]
@@ -455,6 +464,8 @@ def run_zp(args, ws, rank, local):
             "asym_ea_offload": list(assignment.offload),
             "transport": args.transport, "schedule": args.schedule, "expert_capacity": args.expert_capacity,
             "router_skew_zipf": args.router_skew,
+            "expert_placement": "contiguous" if loads is None else "load-balanced (LPT over measured loads)",
+            "expert_loads_per_mb": loads,
             "measured_durations_ns": durs,
             "l2": "activations and weights exceed the 126 MB L2; no flush",
         },
@@ -472,8 +483,9 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200 import simulate, default_orders
 
     out["zp"]["simulated_makespan_ms"] = simulate(graph, default_orders(graph)).makespan / 1e6
-    # the same schedule replayed with each compute task at its measured duration: what the
-    # executor would reach with no issue stalls (communication tasks keep their planned time)
+    # the same schedule replayed with each compute task at its measured duration (slowest rank
+    # of its role): what the executor would reach with no issue stalls (communication tasks
+    # keep their planned time)
     import dataclasses
 
     from paper_2504_03871_b200.taskgraph import TaskGraph
@@ -483,7 +495,7 @@ def run_zp(args, ws, rank, local):
     for t in graph.tasks:
         ranks = range(0, M) if t.device == "attn" else range(M, ws)
         ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in ranks if t.id in tl.per_rank[r]]
-        dur = t.duration if (t.kind.value in comm or not ds) else int(sum(ds) / len(ds))
+        dur = t.duration if (t.kind.value in comm or not ds) else max(ds)  # slowest rank of the role
         newt.append(dataclasses.replace(t, duration=dur))
     g2 = TaskGraph(graph.mode, graph.layers, graph.microbatches, tuple(newt), graph.edges,
                    graph.assignment, graph.forward_only)
@@ -562,6 +574,8 @@ def main():
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
     ap.add_argument("--router-skew", type=float, default=0.0,
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
+    ap.add_argument("--no-balanced-placement", action="store_true",
+                    help="ZP with --router-skew: keep the contiguous expert placement")
     ap.add_argument("--schedule", default="zp", choices=["zp", "distep"],
                     help="ZP: zebra-parallel schedule, or the DistEP lockstep ablation")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],

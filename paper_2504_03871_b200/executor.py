@@ -56,14 +56,37 @@ K = TaskKind
 # placement
 
 
-def expert_owners(E: int, M: int, N: int, offload: int) -> list:
+def expert_owners(E: int, M: int, N: int, offload: int, loads=None) -> list:
     """Owner rank of every expert of one layer. Base: expert rank M+i owns experts
     [i*E/N, (i+1)*E/N). With offload o, the last o local experts of each expert rank move to
-    the attention ranks, dealt in (expert rank, local id) order, o*N/M per attention rank."""
+    the attention ranks, dealt in (expert rank, local id) order, o*N/M per attention rank.
+
+    ``loads`` (expected routed rows per expert, e.g. under a skewed router) switches to a
+    load-balanced placement: experts by decreasing load go to the least-loaded expert rank
+    with room (E/N each), and the o experts each rank offloads are the ones whose loads are closest to the
+    rank's mean (the planner prices an offloaded expert at an average share, R4)."""
     per = E // N
-    owners = [M + e // per for e in range(E)]
+    if loads is None:
+        local = [[i * per + q for q in range(per)] for i in range(N)]
+    else:
+        order = sorted(range(E), key=lambda e: (-loads[e], e))
+        local = [[] for _ in range(N)]
+        tot = [0] * N
+        for e in order:  # largest load first, to the least-loaded rank with room (LPT)
+            i = min((i for i in range(N) if len(local[i]) < per), key=lambda i: (tot[i], i))
+            local[i].append(e)
+            tot[i] += loads[e]
+        if offload:
+            for i in range(N):
+                mean = sum(loads[e] for e in local[i]) / per
+                moved = sorted(sorted(local[i], key=lambda e: (abs(loads[e] - mean), e))[:offload])
+                local[i] = sorted(e for e in local[i] if e not in moved) + moved
+    owners = [0] * E
+    for i in range(N):
+        for e in local[i]:
+            owners[e] = M + i
     if offload:
-        moved = [i * per + loc for i in range(N) for loc in range(per - offload, per)]
+        moved = [local[i][q] for i in range(N) for q in range(per - offload, per)]
         block = offload * N // M
         if block * M != offload * N or block < 1:
             raise ValueError(f"offload {offload} does not split evenly over {M} attention ranks")
@@ -240,7 +263,7 @@ class ZpExecutor:
 
     def __init__(self, graph: TaskGraph, shape: ZpLayerShape, M: int, N: int, rank: int,
                  backend, disp_group=None, comb_group=None, seed: int = 0,
-                 durations_hint: Optional[dict] = None):
+                 durations_hint: Optional[dict] = None, expert_loads=None):
         if graph.mode not in ("zp-full", "distep"):
             raise ValueError("the executor runs zp-full graphs (layer-L experts + loss turnaround) "
                              "or their DistEP lockstep ablation")
@@ -255,7 +278,7 @@ class ZpExecutor:
         self.heads = shape.heads or max(1, shape.d // 128)
         self.orders = default_orders(graph)
         self.issue_order = self._issue_order()
-        owners = [expert_owners(shape.E, M, N, o) for o in graph.assignment.offload]
+        owners = [expert_owners(shape.E, M, N, o, expert_loads) for o in graph.assignment.offload]
         own = [sorted(e for e in range(shape.E) if ow[e] == rank) for ow in owners]
         self.st = RankState(owners=owners, own=own)
         self._init_params(seed)
@@ -728,8 +751,9 @@ class ZpP2PExecutor(ZpExecutor):
     the NCCL path) stays a collective. Same task graph, streams and issue order as ZpExecutor."""
 
     def __init__(self, graph, shape, M, N, rank, backend, disp_group=None, comb_group=None,
-                 seed: int = 0, durations_hint=None):
-        super().__init__(graph, shape, M, N, rank, backend, disp_group, comb_group, seed, durations_hint)
+                 seed: int = 0, durations_hint=None, expert_loads=None):
+        super().__init__(graph, shape, M, N, rank, backend, disp_group, comb_group, seed, durations_hint,
+                         expert_loads)
         if self.W > 8:
             raise ValueError("p2p transport supports at most 8 ranks (one NVSwitch domain)")
         s = shape

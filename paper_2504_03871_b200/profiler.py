@@ -32,9 +32,35 @@ def _time_ms(fn, reps: int = 5, warmup: int = 2) -> float:
     return a.elapsed_time(b) / reps
 
 
+def measure_loads(shape, device="cuda", seed: int = 0) -> list:
+    """Routed rows per expert for one micro-batch (attention block, pre-norm, router with the
+    config's logit bias): the expected expert loads for a skew-aware placement."""
+    from . import ops
+    from .executor import attention_block, rms_norm
+
+    dev = torch.device(device)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d, E, k, T = shape.d, shape.E, shape.k, shape.tokens_per_mb
+    heads = shape.heads or max(1, d // 128)
+    rnd = lambda *s, std=1.0: (torch.randn(s, generator=g, device=dev) * std).to(torch.bfloat16)  # noqa: E731
+    x = rnd(T, d)
+    wqkv, wo, wg = rnd(d, 3 * d, std=d ** -0.5), rnd(d, d, std=d ** -0.5), rnd(d, E, std=d ** -0.5)
+    bias = None
+    if getattr(shape, "router_skew", 0.0):
+        from .configs import zipf_bias
+
+        bias = torch.tensor(zipf_bias(E, shape.router_skew), dtype=torch.float32, device=dev)
+    u = attention_block(x, wqkv, wo, heads) if shape.attention else x
+    r = ops.router_topk(rms_norm(u), wg, k, bias)
+    return [int(c) for c in r.counts.tolist()]
+
+
 def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_ctas: int = 0,
-                      device="cuda", seed: int = 0) -> dict:
-    """Duration table (ns) for ``planner.make_zp_spec`` measured with the native kernels."""
+                      device="cuda", seed: int = 0, loads=None) -> dict:
+    """Duration table (ns) for ``planner.make_zp_spec`` measured with the native kernels.
+    With ``loads`` (``measure_loads``) the expert layer is timed on the busiest expert rank of
+    the load-balanced placement (the reference's ``load_factor`` for skew, costmodel.py:54-63),
+    with that rank's real per-expert row counts."""
     from . import ops
     from .executor import attention_block, rms_norm
 
@@ -64,12 +90,26 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
 
     B = T * M * k // N
     e_local = E // N
+    seg_l = [B * i // e_local for i in range(e_local + 1)]
+    if loads is not None:
+        from .executor import expert_owners
+
+        owners = expert_owners(E, M, N, 0, loads)
+        tot = sum(loads)
+        per_rank = [[e for e in range(E) if owners[e] == M + i] for i in range(N)]
+        busiest = max(per_rank, key=lambda es: sum(loads[e] for e in es))
+        rows = [T * M * k * loads[e] // tot for e in busiest]
+        seg_l = [0]
+        for r_ in rows:
+            seg_l.append(seg_l[-1] + r_)
+        B = seg_l[-1]
     w_ug = rnd(max(e_local, 1), 2 * f, d, std=d ** -0.5)
     w_d = rnd(max(e_local, 1), d, f, std=f ** -0.5)
     xb = rnd(B, d)
-    seg = torch.tensor([B * i // e_local for i in range(e_local + 1)], dtype=torch.int32, device=dev)
+    seg = torch.tensor(seg_l, dtype=torch.int32, device=dev)
     exp_ms = _time_ms(lambda: ops.grouped_ffn_fwd(xb, seg, w_ug, w_d, expert_max_ctas))
-    seg1 = torch.tensor([0, B], dtype=torch.int32, device=dev)
+    B1 = T * M * k // N // max(e_local, 1) * e_local  # an offloaded expert: average share
+    seg1 = torch.tensor([0, min(B1, B)], dtype=torch.int32, device=dev)
     single_ms = _time_ms(lambda: ops.grouped_ffn_fwd(xb, seg1, w_ug[:1].contiguous(), w_d[:1].contiguous(),
                                                      attn_max_ctas))
     # backward factor gamma: the expert layer's measured backward / forward time (the reference

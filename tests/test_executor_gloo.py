@@ -218,3 +218,24 @@ def test_p2p_tables_round_trip(M, N, offload):
                 assert ret[o][0][q] == a and ret[o][1][q] == row
     for o in filled:
         assert (filled[o] == 1).all()
+
+
+def test_load_balanced_placement():
+    """Skew-aware placement: every expert rank keeps E/N experts before offload, the busiest
+    rank's load drops well below the contiguous placement's, offload shares are unchanged and
+    the offloaded experts are the near-average ones of each rank."""
+    from paper_2504_03871_b200.configs import zipf_bias  # noqa: F401  (the sweep's skew source)
+    from paper_2504_03871_b200.executor import expert_owners
+
+    E, M, N = 8, 2, 2
+    loads = [int(1000 / (e + 1)) for e in range(E)]  # Zipf(1) loads
+    base = expert_owners(E, M, N, 0)
+    bal = expert_owners(E, M, N, 0, loads)
+    for ow in (base, bal):
+        assert sorted(ow) == sorted([M + i for i in range(N) for _ in range(E // N)])
+    rank_load = lambda ow: [sum(l for l, o in zip(loads, ow) if o == M + i) for i in range(N)]  # noqa: E731
+    assert max(rank_load(bal)) < 0.75 * max(rank_load(base))
+    for o in (1, 2):
+        ow = expert_owners(E, M, N, o, loads)
+        assert [sum(1 for x in ow if x == a) for a in range(M)] == [o * N // M] * M
+        assert [sum(1 for x in ow if x == M + i) for i in range(N)] == [E // N - o] * N

@@ -3,6 +3,7 @@
 // Host-side responsibilities only: argument validation, TMA descriptor encoding
 // (cuTensorMapEncodeTiled through the runtime's driver entry point; no -lcuda), grid sizing
 // and launches on the caller's stream. No allocation, no synchronisation.
+#include <vector>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -100,12 +101,25 @@ int make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
 }
 
 int gemm_stats_enabled();
+int gemm_ctas();
 
-template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS>
+// Upper bound of a GEMM's tile count (the exact count depends on device-side expert sizes).
+struct TileBound {
+  bool group_k;
+  long rows, M, N, E;
+  long tiles(long tile_m, long tile_n) const {
+    const long ntl = (N + tile_n - 1) / tile_n;
+    return group_k ? E * ((M + tile_m - 1) / tile_m) * ntl : (rows / tile_m + E) * ntl;
+  }
+};
+
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS, int NSUB = 1>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
-                long ub_tiles, int max_ctas, cudaStream_t stream) {
-  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI, CTAS>;
-  constexpr int smem = hm::TileCfg<CTAS>::kSmemBytes;
+                const TileBound& tb, int max_ctas, cudaStream_t stream) {
+  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI, CTAS, NSUB>;
+  using Cfg = hm::TileCfg<CTAS, NSUB>;
+  constexpr int smem = Cfg::kSmemBytes;
+  const long ub_tiles = tb.tiles(Cfg::kTileM, Cfg::kTileN);
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -147,11 +161,37 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
   return check_launch("grouped_gemm");
 }
 
+int gemm_wide_mask();
+
+// CTA count / tile width dispatch for one GEMM kind: 1 CTA (HM_GEMM_CTAS=1), a CTA pair with
+// 256 x 256 tiles, or a CTA pair with 256 x 512 tiles (modes in the wide mask)
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
+int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
+                const TileBound& tb, int max_ctas, cudaStream_t st) {
+  if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1>(ma, mb, p, tb, max_ctas, st);
+  if ((gemm_wide_mask() >> mode) & 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
+  return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1>(ma, mb, p, tb, max_ctas, st);
+}
+
 int gemm_stats_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* s = getenv("HM_GEMM_STATS");
     v = (s && atoi(s) != 0) ? 1 : 0;
+  }
+  return v;
+}
+
+// GEMM modes (bit = HM_GEMM_* mode) that use the 256 x 512 "wide" pair tile; HM_GEMM_WIDE
+// overrides the default (measured per mode on B200)
+#ifndef HM_GEMM_WIDE_DEFAULT
+#define HM_GEMM_WIDE_DEFAULT 0x3A  // down, dX, both wgrads: plain-store epilogues, long K
+#endif
+int gemm_wide_mask() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("HM_GEMM_WIDE");
+    v = s ? static_cast<int>(strtol(s, nullptr, 0)) : HM_GEMM_WIDE_DEFAULT;
   }
   return v;
 }
@@ -171,6 +211,51 @@ int gemm_ctas() {
 extern "C" {
 
 int hm_abi_version(void) { return HM_ABI_VERSION; }
+
+// debugging aid (not part of the ABI): the per-expert wgrad TMA views as built on the device
+// (first E*2 maps of `out`) next to the same views encoded on the host (next E*2 maps)
+int hm_debug_expert_maps(const void* a, const void* b, const int32_t* seg_offsets, int E, int rows,
+                         int M, int N, unsigned char* out) {
+  CUtensorMap ma, mb;
+  uint64_t dims_a[2] = {(uint64_t)M, (uint64_t)rows};
+  uint64_t str_a[1] = {(uint64_t)M * 2};
+  uint32_t box[2] = {64, 64};
+  if (int rc = make_map(&ma, a, 2, dims_a, str_a, box)) return rc;
+  uint64_t dims_b[2] = {(uint64_t)N, (uint64_t)rows};
+  uint64_t str_b[1] = {(uint64_t)N * 2};
+  if (int rc = make_map(&mb, b, 2, dims_b, str_b, box)) return rc;
+  CUtensorMap* ws = nullptr;
+  if (cudaMalloc(&ws, 2 * E * sizeof(CUtensorMap)) != cudaSuccess) return -1;
+  hm::SegBases bases{};
+  bases.a[0] = static_cast<const uint8_t*>(a);
+  bases.b[0] = static_cast<const uint8_t*>(b);
+  hm::build_expert_maps_kernel<<<(E + 127) / 128, 128>>>(ma, mb, seg_offsets, E, 1, bases,
+                                                          static_cast<long>(M) * 2, static_cast<long>(N) * 2, ws);
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, ws, 2 * E * sizeof(CUtensorMap), cudaMemcpyDeviceToHost);
+  cudaFree(ws);
+  int* seg = new int[E + 1];
+  cudaMemcpy(seg, seg_offsets, (E + 1) * sizeof(int), cudaMemcpyDeviceToHost);
+  CUtensorMap* host = reinterpret_cast<CUtensorMap*>(out) + 2 * E;
+  for (int e = 0; e < E; ++e) {
+    const int me = seg[e + 1] - seg[e];
+    uint64_t da[2] = {(uint64_t)M, (uint64_t)(me > 0 ? me : 1)};
+    uint64_t db[2] = {(uint64_t)N, (uint64_t)(me > 0 ? me : 1)};
+    make_map(&host[2 * e], static_cast<const uint8_t*>(a) + (long)seg[e] * M * 2, 2, da, str_a, box);
+    make_map(&host[2 * e + 1], static_cast<const uint8_t*>(b) + (long)seg[e] * N * 2, 2, db, str_b, box);
+  }
+  delete[] seg;
+  return 0;
+}
+
+// debugging aid (not part of the ABI): first out-of-range access recorded by an
+// HM_BOUNDS_CHECK build of the grouped GEMM; reads and clears the record
+int hm_debug_read(long long* out8) {
+  cudaError_t e = cudaMemcpyFromSymbol(out8, hm::g_hm_dbg, 8 * sizeof(long long));
+  if (e != cudaSuccess) return static_cast<int>(e);
+  long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  return static_cast<int>(cudaMemcpyToSymbol(hm::g_hm_dbg, z, sizeof(z)));
+}
 
 // Read (and reset) the grouped-GEMM cycle accounting collected when HM_GEMM_STATS=1:
 // out[0] MMA waiting on TMA, [1] MMA waiting on a free accumulator, [2] MMA role cycles,
@@ -527,38 +612,43 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
     hm::SegBases bases{};
     bases.a[0] = static_cast<const uint8_t*>(a);
     bases.b[0] = static_cast<const uint8_t*>(b);
-    hm::build_expert_maps_kernel<<<(E + 127) / 128, 128, 0, st>>>(
-        ma, mb, seg_offsets, E, 1, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
-    if (int rc = check_launch("build_expert_maps")) return rc;
+    if (getenv("HM_HOST_EXPERT_MAPS")) {  // debugging: host-encoded views (host sync)
+      std::vector<int> seg(E + 1);
+      cudaMemcpy(seg.data(), seg_offsets, (E + 1) * sizeof(int), cudaMemcpyDeviceToHost);
+      std::vector<CUtensorMap> hm_maps(2 * E);
+      for (int e = 0; e < E; ++e) {
+        const int me = seg[e + 1] - seg[e];
+        uint64_t da[2] = {(uint64_t)M, (uint64_t)(me > 0 ? me : 1)};
+        uint64_t db[2] = {(uint64_t)N, (uint64_t)(me > 0 ? me : 1)};
+        make_map(&hm_maps[2 * e], static_cast<const uint8_t*>(a) + (long)seg[e] * M * 2, 2, da, str_a, box);
+        make_map(&hm_maps[2 * e + 1], static_cast<const uint8_t*>(b) + (long)seg[e] * N * 2, 2, db, str_b, box);
+      }
+      cudaMemcpy(maps, hm_maps.data(), 2 * E * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+    } else {
+      hm::build_expert_maps_kernel<<<(E + 127) / 128, 128, 0, st>>>(
+          ma, mb, seg_offsets, E, 1, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
+      if (int rc = check_launch("build_expert_maps")) return rc;
+    }
     p.expert_maps = maps;
   }
 
-  // upper bound of the tile count (the exact count depends on device-side expert sizes)
-  const long tile_m = 128L * ctas;
-  const long ntl = (N + 255) / 256;
-  const long ub_tiles = wgrad ? static_cast<long>(E) * ((M + tile_m - 1) / tile_m) * ntl
-                              : (static_cast<long>(rows) / tile_m + E) * ntl;
+  p.out_elems = wgrad ? static_cast<long>(E) * M * ldo : static_cast<long>(rows) * ldo;
+  const TileBound tb{wgrad, rows, M, N, E};
   switch (mode) {
     case HM_GEMM_FWD_UPGATE:
       if (N % 256 != 0 || !out2) return fail(HM_E_SHAPE, "upgate: N=2f must be a multiple of 256 and h given");
-      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                       : launch_gemm<false, false, false, hm::EPI_SWIGLU_FWD, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+      return launch_kind<false, false, false, hm::EPI_SWIGLU_FWD>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_FWD_DOWN:
-      return ctas == 2 ? launch_gemm<false, false, false, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                       : launch_gemm<false, false, false, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+      return launch_kind<false, false, false, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_BWD_DACT:
       if (N % 128 != 0 || !aux) return fail(HM_E_SHAPE, "dact: N=f must be a multiple of 128 and h given");
-      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                       : launch_gemm<false, false, true, hm::EPI_SWIGLU_BWD, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+      return launch_kind<false, false, true, hm::EPI_SWIGLU_BWD>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_BWD_DX:
-      return ctas == 2 ? launch_gemm<false, false, true, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                       : launch_gemm<false, false, true, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+      return launch_kind<false, false, true, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_WGRAD:
-      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                       : launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+      return launch_kind<true, true, true, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_WGRAD_ACC:
-      return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_ACC_F32, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                       : launch_gemm<true, true, true, hm::EPI_ACC_F32, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+      return launch_kind<true, true, true, hm::EPI_ACC_F32>(mode, ma, mb, p, tb, max_ctas, st);
     default:
       return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
   }
@@ -608,14 +698,11 @@ int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void
   p.ldo = ldo;
   p.n_fastest = (M >= N) ? 1 : 0;
   p.expert_maps = maps;
-  const int ctas = gemm_ctas();
-  const long tile_m = 128L * ctas;
-  const long ub_tiles = static_cast<long>(E) * ((M + tile_m - 1) / tile_m) * ((N + 255) / 256);
+  p.out_elems = static_cast<long>(E) * M * ldo;
+  const TileBound tb{true, 0, M, N, E};
   if (accumulate)
-    return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_ACC_F32, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                     : launch_gemm<true, true, true, hm::EPI_ACC_F32, 1>(ma, mb, p, ub_tiles, max_ctas, st);
-  return ctas == 2 ? launch_gemm<true, true, true, hm::EPI_STORE, 2>(ma, mb, p, ub_tiles, max_ctas, st)
-                   : launch_gemm<true, true, true, hm::EPI_STORE, 1>(ma, mb, p, ub_tiles, max_ctas, st);
+    return launch_kind<true, true, true, hm::EPI_ACC_F32>(HM_GEMM_WGRAD_ACC, ma, mb, p, tb, max_ctas, st);
+  return launch_kind<true, true, true, hm::EPI_STORE>(HM_GEMM_WGRAD, ma, mb, p, tb, max_ctas, st);
 }
 
 int hm_grouped_ffn_fwd(const void* x_perm, int rows, const int32_t* seg_offsets, int E,

@@ -260,3 +260,34 @@ def test_moe_layer_fwd_bwd(cfg):
     assert orc.rel_err(dg, ref["dw_gate"]) < TOL_W
     assert orc.rel_err(du, ref["dw_up"]) < TOL_W
     assert orc.rel_err(wd.grad, ref["dw_down"]) < TOL_W
+
+
+@pytest.mark.parametrize("segs,M,N", [
+    ([1, 0, 130, 127, 300, 0, 64, 2], 256, 512),
+    ([100] * 7 + [24], 512, 128),
+    ([4096, 4000, 4200, 3900], 8192, 4096),
+    ([0, 0, 1, 700], 768, 256),
+])
+def test_device_expert_maps_match_host(segs, M, N):
+    """The per-expert TMA views that the wgrad GEMM builds on the device (tensormap.replace of
+    the whole-buffer maps) are byte-identical to the driver's own encoding of the same views."""
+    import ctypes
+
+    from paper_2504_03871_b200 import _native
+
+    lib = _native.load()
+    fn = lib.hm_debug_expert_maps
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4 + [ctypes.c_void_p]
+    E = len(segs)
+    rows = max(sum(segs), 1)
+    off = _ragged_offsets(segs)
+    seg = torch.from_numpy(off).cuda()
+    a = torch.empty((rows, M), dtype=torch.bfloat16, device="cuda")
+    b = torch.empty((rows, N), dtype=torch.bfloat16, device="cuda")
+    buf = (ctypes.c_ubyte * (4 * E * 128))()
+    assert fn(a.data_ptr(), b.data_ptr(), seg.data_ptr(), E, rows, M, N, buf) == 0
+    arr = np.frombuffer(bytes(buf), dtype=np.uint8).reshape(2, E, 2, 128)
+    for e in range(E):
+        for o in range(2):
+            assert np.array_equal(arr[0, e, o], arr[1, e, o]), (e, o, np.nonzero(arr[0, e, o] != arr[1, e, o]))

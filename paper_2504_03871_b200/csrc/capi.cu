@@ -291,6 +291,34 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
   }
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(wg);
+  if (E % 8 == 0 && aligned16(wg) && !getenv("HM_ROUTER_V1")) {
+    // fp32-staged, bank-conflict-free variant (same summation order, bit-identical logits)
+    const int eg2 = E == 8 ? 8 : 16;
+    const size_t smem2 = static_cast<size_t>(d) * eg2 * 4 + static_cast<size_t>(d / 8) * 16;
+    if (smem2 <= 200 * 1024) {
+      const int ngroups = (E + eg2 - 1) / eg2;
+      constexpr int tt = 4;
+      const int per_iter = hm::kRouter2Warps * tt;
+      int gx = (T + per_iter - 1) / per_iter;
+      const int cap = (num_sms() + ngroups - 1) / ngroups;
+      if (gx > cap) gx = cap;
+      dim3 grid(gx, ngroups);
+      if (eg2 == 8) {
+        auto kern = hm::router_logits2_kernel<8, tt>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits);
+      } else {
+        auto kern = hm::router_logits2_kernel<16, tt>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits);
+      }
+      if (int rc = check_launch("router_logits2")) return rc;
+      hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+      if (int rc = check_launch("router_topk")) return rc;
+      hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
+      return check_launch("router_scan");
+    }
+  }
   int eg = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
   const size_t smem = static_cast<size_t>(d) * eg * 2;
   if (smem > 200 * 1024) return fail(HM_E_SHAPE, "router: d*EG too large for shared memory");

@@ -115,6 +115,112 @@ __global__ void __launch_bounds__(kRouterWarps * 32)
   }
 }
 
+// K1a (v2, fp32-staged): same summation order as router_logits_kernel — lane L owns
+// i = 256 j + 8 L + q, accumulates over (j, q) in order, then the xor butterfly — so the logits
+// are bit-identical, but Wg[:, e0:e0+EG] is staged ONCE per CTA as fp32 (no per-token bf16
+// unpacking), rows padded by 16 bytes every 8 rows so that the 8 lanes of each LDS.128 phase
+// (rows 8 apart) hit disjoint banks, with 16 warps per CTA and TT tokens per warp.
+constexpr int kRouter2Warps = 16;
+
+HM_DEV int router2_row_off(int i, int eg) {  // float offset of row i in the padded [d][EG] tile
+  return i * eg + (i >> 3) * 4;
+}
+
+template <int EG, int TT>
+__global__ void __launch_bounds__(kRouter2Warps * 32, 1)
+    router_logits2_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                          const float* __restrict__ bias, int T, int d, int E,
+                          float* __restrict__ logits) {
+  extern __shared__ __align__(16) uint8_t smem_r2[];
+  float* ws = reinterpret_cast<float*>(smem_r2);
+  const int e0 = blockIdx.y * EG;
+  // stage Wg[:, e0:e0+EG] as fp32: one 16-byte load = 8 experts of one row (E % 8 == 0)
+  constexpr int kVec = EG / 8;
+  for (int idx = threadIdx.x; idx < d * kVec; idx += blockDim.x) {
+    const int i = idx / kVec, c = idx % kVec;
+    float* dst = ws + router2_row_off(i, EG) + c * 8;
+    if (e0 + c * 8 < E) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(wg + static_cast<long>(i) * E + e0 + c * 8));
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
+      reinterpret_cast<float4*>(dst)[0] = make_float4(bf16_to_f32(h[0]), bf16_to_f32(h[1]),
+                                                      bf16_to_f32(h[2]), bf16_to_f32(h[3]));
+      reinterpret_cast<float4*>(dst)[1] = make_float4(bf16_to_f32(h[4]), bf16_to_f32(h[5]),
+                                                      bf16_to_f32(h[6]), bf16_to_f32(h[7]));
+    } else {
+      reinterpret_cast<float4*>(dst)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(dst)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = d / 256;
+  const int per_iter = kRouter2Warps * TT;
+  for (int t0 = blockIdx.x * per_iter + warp * TT; t0 < T; t0 += gridDim.x * per_iter) {
+    float acc[TT][EG];
+#pragma unroll
+    for (int a = 0; a < TT; ++a)
+#pragma unroll
+      for (int e = 0; e < EG; ++e) acc[a][e] = 0.f;
+    uint4 xv[TT], xn[TT];
+#pragma unroll
+    for (int a = 0; a < TT; ++a) {
+      const int t = min(t0 + a, T - 1);
+      xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + lane * 8));
+    }
+    for (int j = 0; j < nj; ++j) {
+      const int ibase = j * 256 + lane * 8;
+      if (j + 1 < nj) {
+#pragma unroll
+        for (int a = 0; a < TT; ++a) {
+          const int t = min(t0 + a, T - 1);
+          xn[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase + 256));
+        }
+      }
+      const float* wrow0 = ws + router2_row_off(ibase, EG);  // rows ibase..ibase+7: one 8-row group
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float wv[EG];
+#pragma unroll
+        for (int e = 0; e < EG; e += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(wrow0 + q * EG + e);
+          wv[e] = w4.x; wv[e + 1] = w4.y; wv[e + 2] = w4.z; wv[e + 3] = w4.w;
+        }
+#pragma unroll
+        for (int a = 0; a < TT; ++a) {
+          const float xf = bf16_to_f32(reinterpret_cast<const uint16_t*>(&xv[a])[q]);
+#pragma unroll
+          for (int e = 0; e < EG; ++e) acc[a][e] = __fmaf_rn(xf, wv[e], acc[a][e]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < TT; ++a) xv[a] = xn[a];
+    }
+#pragma unroll
+    for (int a = 0; a < TT; ++a)
+#pragma unroll
+      for (int e = 0; e < EG; ++e) {
+        float v = acc[a][e];
+        v = v + __shfl_xor_sync(0xffffffffu, v, 16);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 8);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 4);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 2);
+        v = v + __shfl_xor_sync(0xffffffffu, v, 1);
+        acc[a][e] = v;
+      }
+    // every lane holds every sum; lane (a * EG + e) % 32 writes
+#pragma unroll
+    for (int a = 0; a < TT; ++a) {
+      const int t = t0 + a;
+#pragma unroll
+      for (int e = 0; e < EG; ++e) {
+        if (lane == ((a * EG + e) & 31) && t < T && e0 + e < E)
+          logits[static_cast<long>(t) * E + e0 + e] = bias ? acc[a][e] + bias[e0 + e] : acc[a][e];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // K1b: top-k + softmax + per-chunk expert histogram. One CTA per chunk of kChunk tokens,
 // one warp per token (looping). E <= 256.

@@ -296,40 +296,55 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(1024)
     router_scan_kernel(int32_t* __restrict__ chunk_counts /*in: counts, out: bases*/, int nchunk,
                        int E, int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
-  __shared__ int tot[256];
+  // thread (g, e): chunk group g of G = blockDim / Epad, expert e; loads are coalesced over e
+  __shared__ int part[1024];  // [G][Epad] partial sums, then exclusive prefixes over g
   __shared__ int off[257];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int e = warp; e < E; e += nw) {
-    int s = 0;
-    for (int c = lane; c < nchunk; c += 32) s += chunk_counts[static_cast<long>(c) * E + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) tot[e] = s;
+  int epad = 1;
+  while (epad < E) epad <<= 1;
+  const int G = blockDim.x / epad;
+  const int g = threadIdx.x / epad, e = threadIdx.x % epad;
+  const int c_lo = static_cast<int>((static_cast<long>(nchunk) * g) / G);
+  const int c_hi = static_cast<int>((static_cast<long>(nchunk) * (g + 1)) / G);
+  int s = 0;
+  if (e < E && g < G) {
+#pragma unroll 8
+    for (int c = c_lo; c < c_hi; ++c) s += chunk_counts[static_cast<long>(c) * E + e];
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < epad) {  // exclusive prefix over the chunk groups of expert e = threadIdx.x
+    int a = 0;
+    for (int gg = 0; gg < G; ++gg) {
+      const int v = part[gg * epad + threadIdx.x];
+      part[gg * epad + threadIdx.x] = a;
+      a += v;
+    }
+    if (threadIdx.x < E) off[threadIdx.x] = a;  // expert total, scanned below
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     int a = 0;
-    for (int i = 0; i < E; ++i) { off[i] = a; a += tot[i]; }
+    for (int i = 0; i < E; ++i) {
+      const int t = off[i];
+      off[i] = a;
+      counts[i] = t;
+      offsets[i] = a;
+      a += t;
+    }
     off[E] = a;
+    offsets[E] = a;
   }
   __syncthreads();
-  for (int e = warp; e < E; e += nw) {
-    int base = off[e];
-    for (int c0 = 0; c0 < nchunk; c0 += 32) {
-      const int c = c0 + lane;
-      const int v = c < nchunk ? chunk_counts[static_cast<long>(c) * E + e] : 0;
-      int incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int n = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += n;
-      }
-      if (c < nchunk) chunk_counts[static_cast<long>(c) * E + e] = base + incl - v;
-      base += __shfl_sync(0xffffffffu, incl, 31);
+  if (e < E && g < G) {
+    int base = off[e] + part[threadIdx.x];
+#pragma unroll 8
+    for (int c = c_lo; c < c_hi; ++c) {
+      int32_t* p = chunk_counts + static_cast<long>(c) * E + e;
+      const int v = *p;
+      *p = base;
+      base += v;
     }
-    if (lane == 0) { counts[e] = tot[e]; offsets[e] = off[e]; }
   }
-  if (threadIdx.x == 0) offsets[E] = off[E];
 }
 
 // ------------------------------------------------------------------------------------------

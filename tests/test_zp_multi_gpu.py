@@ -1,0 +1,33 @@
+"""Multi-GPU check of the ZP executor on real devices (run by `pytest -m gpu`; skipped on a box
+with fewer than 2 GPUs): one seeded iteration of a 2-layer stack through the NCCL send/recv
+executor and through the NVLink peer-memory executor, whose gradients must agree
+(tools/zp_transport_check.py, under torchrun)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs 2 GPUs")
+@pytest.mark.parametrize("world", [2, 4])
+def test_transports_agree_on_gradients(world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + world),
+           os.path.join(ROOT, "tools", "zp_transport_check.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stderr[-3000:]
+    out = json.loads(lines[-1])
+    assert out["worst_rel_err"] <= max(1e-3, 4 * out["nccl_rerun_rel_err"])
+    assert all(v["bitwise"] for k, v in out["rank0"].items() if k.startswith(("gw_ug", "gw_d")))

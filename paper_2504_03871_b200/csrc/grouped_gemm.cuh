@@ -253,7 +253,14 @@ HM_DEV int next_tile(GemmShared& sh, int cur, int step, uint32_t& ci, bool arriv
   return x < 0 ? -1 : x / CTAS;
 }
 
-HM_DEV float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// sigmoid with the MUFU reciprocal (1 + e^-g >= 1, so no denormal / overflow corner: e^-g = inf
+// gives exactly 0); the IEEE division costs ~10 more instructions per element in the epilogue
+HM_DEV float sigmoid_f(float g) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + __expf(-g)));
+  return r;
+}
+HM_DEV float silu_f(float g) { return g * sigmoid_f(g); }
 
 // 32 consecutive fp32 accumulator columns of one row -> 32 bf16 (64 bytes) at dst
 HM_DEV void store_row32(__nv_bfloat16* dst, const float* v, int valid_cols) {
@@ -446,7 +453,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ======================= MMA issuer (leader CTA) =======================
     constexpr uint32_t idesc = make_idesc_bf16(kTileM, kBN, A_MN ? 1u : 0u, B_MN ? 1u : 0u);
     uint32_t it = 0, tcount = 0;
-    unsigned long long st_full = 0, st_tmem = 0, st_tiles = 0;
+    unsigned long long st_full = 0, st_tmem = 0, st_tiles = 0, st_head = 0;
     const unsigned long long st_t0 = clk();
     if (leader) {
       uint32_t ci = 0;
@@ -468,7 +475,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t ph = (it / kStages) & 1;
           if (p.stats) w0 = clk();
           mbar_wait(&sh.full[s], ph);
-          if (p.stats) st_full += clk() - w0;
+          if (p.stats) {
+            const unsigned long long dw = clk() - w0;
+            st_full += dw;
+            if (kb < kStages) st_head += dw;  // waits in a tile's first ring's worth of stages
+          }
           tc_fence_after();
           uint8_t* sa = tiles + s * kStageBytes;
           uint8_t* sb = sa + kATileBytes;
@@ -506,6 +517,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         atomicAdd(&g_gemm_stats[2], clk() - st_t0);
         atomicAdd(&g_gemm_stats[4], st_tiles);
         atomicAdd(&g_gemm_stats[5], 1ull);
+        atomicAdd(&g_gemm_stats[6], st_head);
       }
     }
   } else if (warp == kSchedWarp) {
@@ -618,7 +630,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               for (int j = 0; j < 8; ++j) {
                 const float g = bf16_to_f32(gs[j]);
                 const float u = bf16_to_f32(us[j]);
-                const float sg = 1.0f / (1.0f + __expf(-g));
+                const float sg = sigmoid_f(g);
                 const float d = da[q * 8 + j];
                 du[j] = d * g * sg;
                 dg[j] = d * u * sg * (1.0f + g * (1.0f - sg));

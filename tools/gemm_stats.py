@@ -30,5 +30,5 @@ for rep in range(2):
         v = list(buf)
         if rep == 1:
             tot = max(v[2], 1)
-            print(f"{name}: MMA waits TMA {v[0]/tot:.3f}, waits TMEM {v[1]/tot:.3f}, producer waits "
+            print(f"{name}: MMA waits TMA {v[0]/tot:.3f} (of which tile heads {v[6]/max(v[0],1):.2f}), waits TMEM {v[1]/tot:.3f}, producer waits "
                   f"stage {v[3]/max(v[5],1)/ (tot/max(v[5],1)):.3f}; tiles {v[4]}, leader CTAs {v[5]}")

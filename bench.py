@@ -360,6 +360,47 @@ def cpu_baseline(cfg, tokens: int):
             "sample": f"{tokens} tokens of {cfg.name} (fwd+bwd, fp32 CPU oracle, {dt:.1f}s)"}
 
 
+def stack_single_gpu(shape, layers: int, microbatches: int, dev, seed: int = 7):
+    """The ZP stack's work on ONE GPU with no pipeline (the scaling comparator for N > 1): every
+    micro-batch runs forward and backward through all layers — pre-norm attention block, then
+    the MoE layer through the same native kernels — with gradients accumulated. Returns
+    MoE-layer tokens/s (tokens x layers / time), CUDA-event timed, one iteration after warm-up."""
+    from paper_2504_03871_b200.executor import attention_block, rms_norm
+    from paper_2504_03871_b200.layer import moe_forward
+
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d, f, E, k, T = shape.d, shape.f, shape.E, shape.k, shape.tokens_per_mb
+    heads = shape.heads or max(1, d // 128)
+
+    def rnd(*sz, std=1.0):
+        return (torch.randn(sz, generator=g, device=dev) * std).to(torch.bfloat16).requires_grad_()
+
+    P = [dict(wqkv=rnd(d, 3 * d, std=d ** -0.5), wo=rnd(d, d, std=d ** -0.5), wg=rnd(d, E, std=d ** -0.5),
+              w_ug=rnd(E, 2 * f, d, std=d ** -0.5), w_d=rnd(E, d, f, std=f ** -0.5)) for _ in range(layers)]
+    x = [torch.randn((T, d), generator=g, device=dev).to(torch.bfloat16) for _ in range(2)]
+    gy = [torch.randn((T, d), generator=g, device=dev).to(torch.bfloat16) for _ in range(2)]
+
+    def iteration():
+        for j in range(microbatches):
+            h = x[j & 1]
+            for p in P:
+                u = attention_block(h, p["wqkv"], p["wo"], heads) if shape.attention else h * 1
+                y, _ = moe_forward(rms_norm(u), p["wg"], p["w_ug"], p["w_d"], k)
+                h = u + y
+            h.backward(gy[j & 1])
+
+    iteration()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    iteration()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    del P
+    return T * microbatches * layers / (ms / 1e3), ms
+
+
 def run_zp(args, ws, rank, local):
     """N > 1: zebra-parallel stack of MoE transformer layers (C4 shape at 8 GPUs: 4 attention +
     4 expert ranks). value = MoE-layer tokens/s = tokens/iteration * layers / iteration time."""
@@ -482,6 +523,16 @@ def run_zp(args, ws, rank, local):
     }
     from paper_2504_03871_b200 import simulate, default_orders
 
+    if not args.no_stack_reference:
+        # the same work (all M x R micro-batches, all layers, attention + MoE) on this one GPU
+        # without the pipeline: the per-GPU comparator for scaling (the N = 1 bench line is the
+        # bare MoE layer, BASELINE configs[1])
+        v1, ms1 = stack_single_gpu(shape, args.layers, M * args.microbatches, dev)
+        out["scaling_reference"] = {
+            "value": v1, "unit": UNIT, "ms_per_iteration": round(ms1, 3),
+            "workload": "identical stack and token count on ONE GPU, no pipeline (rank 0, after the timed region)",
+            "per_gpu_efficiency": value / (ws * v1),
+        }
     out["zp"]["simulated_makespan_ms"] = simulate(graph, default_orders(graph)).makespan / 1e6
     # the same schedule replayed with each compute task at its measured duration (slowest rank
     # of its role): what the executor would reach with no issue stalls (communication tasks
@@ -576,6 +627,8 @@ def main():
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
     ap.add_argument("--no-balanced-placement", action="store_true",
                     help="ZP with --router-skew: keep the contiguous expert placement")
+    ap.add_argument("--no-stack-reference", action="store_true",
+                    help="ZP: skip the single-GPU run of the same stack (scaling comparator)")
     ap.add_argument("--schedule", default="zp", choices=["zp", "distep"],
                     help="ZP: zebra-parallel schedule, or the DistEP lockstep ablation")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],

@@ -197,7 +197,7 @@ def split_gate_up(w_ug: torch.Tensor, block: int = BLOCK_F):
 def expert_ffn(x_perm: torch.Tensor, offsets, w_gate, w_up, w_down) -> torch.Tensor:
     """Per expert e: Y = (silu(X Wg^T) * (X Wu^T)) Wd^T over rows [offsets[e], offsets[e+1])."""
     outs = []
-    for e in range(w_gate.shape[0]):
+    for e in range(len(w_gate)):
         a, b = int(offsets[e]), int(offsets[e + 1])
         xe = x_perm[a:b]
         g = xe @ w_gate[e].t()
@@ -221,9 +221,12 @@ def moe_layer(x, wg, w_ug, w_down, k: int, dy=None, routing: RoutingRef | None =
 
     xg = x.clone().requires_grad_(dy is not None)
     wgg = wg.clone().requires_grad_(dy is not None)
-    wgt = w_gate.clone().requires_grad_(dy is not None)
-    wut = w_up.clone().requires_grad_(dy is not None)
-    wdt = w_down.clone().requires_grad_(dy is not None)
+    # one leaf per expert (indexing a stacked leaf would materialise a full-size zero gradient
+    # per expert in the backward)
+    rg = dy is not None
+    wgt = [w_gate[e].clone().requires_grad_(rg) for e in range(w_gate.shape[0])]
+    wut = [w_up[e].clone().requires_grad_(rg) for e in range(w_up.shape[0])]
+    wdt = [w_down[e].clone().requires_grad_(rg) for e in range(w_down.shape[0])]
 
     logits = xg @ wgg  # values differ from the fixed-order logits only by rounding
     idx_t = torch.from_numpy(r.idx.astype(np.int64))
@@ -237,8 +240,46 @@ def moe_layer(x, wg, w_ug, w_down, k: int, dy=None, routing: RoutingRef | None =
     out = {"routing": r, "y": y.detach(), "w": w.detach()}
     if dy is not None:
         y.backward(dy.detach().float().cpu())
-        out.update(dx=xg.grad, dwg=wgg.grad, dw_gate=wgt.grad, dw_up=wut.grad, dw_down=wdt.grad)
+        stack = lambda ws: torch.stack([w.grad if w.grad is not None else torch.zeros_like(w) for w in ws])  # noqa: E731
+        out.update(dx=xg.grad, dwg=wgg.grad, dw_gate=stack(wgt), dw_up=stack(wut), dw_down=stack(wdt))
     return out
+
+
+class CpuLayer:
+    """The same fp32 CPU layer as ``moe_layer`` with its parameters converted ONCE (fp32 master
+    copies with gradients), for timing the CPU path per step (bench.py's ``cpu_baseline`` and
+    ``--impl reference`` arms): each ``step`` routes (fixed-order oracle), runs the forward and
+    the backward, and leaves the gradients in the parameters."""
+
+    def __init__(self, wg, w_ug, w_down, k: int):
+        self.k = k
+        self.wg = wg.detach().float().cpu().clone().requires_grad_()
+        g, u = split_gate_up(w_ug.detach().float().cpu())
+        # one leaf per expert: indexing a stacked [E, ...] leaf would make autograd materialise
+        # a full-size zero gradient per expert (SelectBackward)
+        self.w_gate = [g[e].contiguous().requires_grad_() for e in range(g.shape[0])]
+        self.w_up = [u[e].contiguous().requires_grad_() for e in range(u.shape[0])]
+        wd = w_down.detach().float().cpu()
+        self.w_down = [wd[e].contiguous().requires_grad_() for e in range(wd.shape[0])]
+
+    def params(self):
+        return [self.wg] + self.w_gate + self.w_up + self.w_down
+
+    def step(self, x, dy):
+        for p in self.params():
+            p.grad = None
+        x = x.detach().float().cpu()
+        r = route(x.numpy(), self.wg.detach().numpy(), self.k)
+        T = x.shape[0]
+        xg = x.requires_grad_()
+        logits = xg @ self.wg
+        w = torch.softmax(torch.gather(logits, 1, torch.from_numpy(r.idx.astype(np.int64))), dim=1)
+        x_perm = xg[torch.from_numpy(r.row_src.astype(np.int64))]
+        y_perm = expert_ffn(x_perm, r.offsets, self.w_gate, self.w_up, self.w_down)
+        row_of = torch.from_numpy(r.row_of.astype(np.int64))
+        y = (y_perm[row_of.reshape(-1)].reshape(T, self.k, -1) * w[:, :, None]).sum(1)
+        y.backward(dy.detach().float().cpu())
+        return y.detach()
 
 
 def rel_err(a: torch.Tensor, b: torch.Tensor) -> float:

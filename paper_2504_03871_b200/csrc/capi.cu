@@ -640,23 +640,9 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
     hm::SegBases bases{};
     bases.a[0] = static_cast<const uint8_t*>(a);
     bases.b[0] = static_cast<const uint8_t*>(b);
-    if (getenv("HM_HOST_EXPERT_MAPS")) {  // debugging: host-encoded views (host sync)
-      std::vector<int> seg(E + 1);
-      cudaMemcpy(seg.data(), seg_offsets, (E + 1) * sizeof(int), cudaMemcpyDeviceToHost);
-      std::vector<CUtensorMap> hm_maps(2 * E);
-      for (int e = 0; e < E; ++e) {
-        const int me = seg[e + 1] - seg[e];
-        uint64_t da[2] = {(uint64_t)M, (uint64_t)(me > 0 ? me : 1)};
-        uint64_t db[2] = {(uint64_t)N, (uint64_t)(me > 0 ? me : 1)};
-        make_map(&hm_maps[2 * e], static_cast<const uint8_t*>(a) + (long)seg[e] * M * 2, 2, da, str_a, box);
-        make_map(&hm_maps[2 * e + 1], static_cast<const uint8_t*>(b) + (long)seg[e] * N * 2, 2, db, str_b, box);
-      }
-      cudaMemcpy(maps, hm_maps.data(), 2 * E * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
-    } else {
-      hm::build_expert_maps_kernel<<<(E + 127) / 128, 128, 0, st>>>(
-          ma, mb, seg_offsets, E, 1, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
-      if (int rc = check_launch("build_expert_maps")) return rc;
-    }
+    hm::build_expert_maps_kernel<<<(E + 127) / 128, 128, 0, st>>>(
+        ma, mb, seg_offsets, E, 1, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
+    if (int rc = check_launch("build_expert_maps")) return rc;
     p.expert_maps = maps;
   }
 

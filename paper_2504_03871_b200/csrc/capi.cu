@@ -187,13 +187,13 @@ int gemm_stats_enabled() {
 #ifndef HM_GEMM_WIDE_DEFAULT
 #define HM_GEMM_WIDE_DEFAULT 0x3A  // down, dX, both wgrads: plain-store epilogues, long K
 #endif
+int g_wide_mask = -1;
 int gemm_wide_mask() {
-  static int v = -1;
-  if (v < 0) {
+  if (g_wide_mask < 0) {
     const char* s = getenv("HM_GEMM_WIDE");
-    v = s ? static_cast<int>(strtol(s, nullptr, 0)) : HM_GEMM_WIDE_DEFAULT;
+    g_wide_mask = s ? static_cast<int>(strtol(s, nullptr, 0)) : HM_GEMM_WIDE_DEFAULT;
   }
-  return v;
+  return g_wide_mask;
 }
 
 // CTA-pair (cta_group::2) tiles for the GROUP_M GEMMs unless HM_GEMM_CTAS=1
@@ -267,6 +267,13 @@ int hm_gemm_stats(unsigned long long* out) {
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(hm::g_gemm_stats, z, sizeof(z));
   if (e != cudaSuccess) return fail(static_cast<int>(e), "gemm_stats: %s", cudaGetErrorString(e));
   return 0;
+}
+// tuning aid (not part of the ABI): set the wide-tile GEMM mode mask (-1 = default / env) and
+// return the previous one, so variants can be A/B-timed in one process
+int hm_debug_set_gemm_wide(int mask) {
+  const int old = gemm_wide_mask();
+  g_wide_mask = mask;
+  return old;
 }
 const char* hm_last_error(void) { return g_last_error.c_str(); }
 int hm_num_sms(void) { return num_sms(); }

@@ -113,7 +113,18 @@ HM_DEV bool hm_dbg_bad(bool bad, long long what, long long idx, long long a, lon
 
 // out[0..31] += v[0..31] (fp32), masked to valid_cols
 HM_DEV void acc_row32(float* dst, const float* v, int valid_cols) {
-  if (valid_cols >= 32) {
+  if (valid_cols >= 32 && (reinterpret_cast<uintptr_t>(dst) & 31u) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 lo, hi;
+      ld_global_v8(dst + q * 8, lo, hi);
+      float* o = reinterpret_cast<float*>(&lo);
+      float* o2 = reinterpret_cast<float*>(&hi);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { o[j] += v[q * 8 + j]; o2[j] += v[q * 8 + 4 + j]; }
+      st_global_v8(dst + q * 8, lo, hi);
+    }
+  } else if (valid_cols >= 32) {
     float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -263,18 +274,24 @@ HM_DEV float sigmoid_f(float g) {
 HM_DEV float silu_f(float g) { return g * sigmoid_f(g); }
 
 // 32 consecutive fp32 accumulator columns of one row -> 32 bf16 (64 bytes) at dst
+HM_DEV uint4 pack_bf16x8(const float* v) {
+  uint4 w;
+  w.x = pack_bf16x2(v[0], v[1]);
+  w.y = pack_bf16x2(v[2], v[3]);
+  w.z = pack_bf16x2(v[4], v[5]);
+  w.w = pack_bf16x2(v[6], v[7]);
+  return w;
+}
+
 HM_DEV void store_row32(__nv_bfloat16* dst, const float* v, int valid_cols) {
-  if (valid_cols >= 32) {
+  if (valid_cols >= 32 && (reinterpret_cast<uintptr_t>(dst) & 31u) == 0) {
+    // two 256-bit stores: every lane fills two whole sectors of its own row
+    st_global_v8(dst, pack_bf16x8(v), pack_bf16x8(v + 8));
+    st_global_v8(dst + 16, pack_bf16x8(v + 16), pack_bf16x8(v + 24));
+  } else if (valid_cols >= 32) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint4 w;
-      w.x = pack_bf16x2(v[q * 8 + 0], v[q * 8 + 1]);
-      w.y = pack_bf16x2(v[q * 8 + 2], v[q * 8 + 3]);
-      w.z = pack_bf16x2(v[q * 8 + 4], v[q * 8 + 5]);
-      w.w = pack_bf16x2(v[q * 8 + 6], v[q * 8 + 7]);
-      d4[q] = w;
-    }
+    for (int q = 0; q < 4; ++q) d4[q] = pack_bf16x8(v + q * 8);
   } else {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
@@ -592,13 +609,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int fcol = n0 + c;  // multiple of 32; a 32-chunk never crosses a 128 block
           return p.aux + grow * p.ld_aux + (fcol >> 7) * 256 + (fcol & 127);
         };
+        // 256-bit loads / stores when every row start is 32-byte aligned (the usual case)
+        const bool v8ok = (((reinterpret_cast<uintptr_t>(p.aux) | reinterpret_cast<uintptr_t>(p.out)) & 31u) == 0) &&
+                          (p.ld_aux % 16 == 0) && (p.ldo % 16 == 0);
+        auto ld64 = [&](const __nv_bfloat16* src, uint4 (&dst)[4]) {
+          if (v8ok) {
+            ld_global_v8(src, dst[0], dst[1]);
+            ld_global_v8(src + 16, dst[2], dst[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = *reinterpret_cast<const uint4*>(src + q * 8);
+          }
+        };
+        auto st64 = [&](__nv_bfloat16* dst, const uint4 (&src)[4]) {
+          if (v8ok) {
+            st_global_v8(dst, src[0], src[1]);
+            st_global_v8(dst + 16, src[2], src[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(dst)[q] = src[q];
+          }
+        };
         uint4 gcur[4], ucur[4], gnxt[4], unxt[4];
         if (live) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            gcur[q] = *reinterpret_cast<const uint4*>(hptr(cbeg) + q * 8);
-            ucur[q] = *reinterpret_cast<const uint4*>(hptr(cbeg) + 128 + q * 8);
-          }
+          ld64(hptr(cbeg), gcur);
+          ld64(hptr(cbeg) + 128, ucur);
         }
         mbar_wait(&sh.tmem_full[acc], aph);
         tc_fence_after();
@@ -608,11 +643,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int c = cbeg + 32 * i;
           const bool ok = row_ok && c < ncols_valid;
           if (i < 3 && row_ok && c + 32 < ncols_valid) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              gnxt[q] = *reinterpret_cast<const uint4*>(hptr(c + 32) + q * 8);
-              unxt[q] = *reinterpret_cast<const uint4*>(hptr(c + 32) + 128 + q * 8);
-            }
+            ld64(hptr(c + 32), gnxt);
+            ld64(hptr(c + 32) + 128, unxt);
           }
           uint32_t r[32];
           tmem_ld_32x32b_x32(t_row + c, r);
@@ -621,6 +653,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const float* da = reinterpret_cast<float*>(r);
             const int fcol = n0 + c;
             __nv_bfloat16* dgp = p.out + grow * p.ldo + (fcol >> 7) * 256 + (fcol & 127);
+            uint4 wgs[4], wus[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint16_t* gs = reinterpret_cast<const uint16_t*>(&gcur[q]);
@@ -640,9 +673,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               wg.z = pack_bf16x2(dg[4], dg[5]); wg.w = pack_bf16x2(dg[6], dg[7]);
               wu.x = pack_bf16x2(du[0], du[1]); wu.y = pack_bf16x2(du[2], du[3]);
               wu.z = pack_bf16x2(du[4], du[5]); wu.w = pack_bf16x2(du[6], du[7]);
-              reinterpret_cast<uint4*>(dgp)[q] = wg;
-              reinterpret_cast<uint4*>(dgp + 128)[q] = wu;
+              wgs[q] = wg;
+              wus[q] = wu;
             }
+            st64(dgp, wgs);
+            st64(dgp + 128, wus);
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) { gcur[q] = gnxt[q]; ucur[q] = unxt[q]; }

@@ -51,6 +51,21 @@ HM_DEV uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// 256-bit global access (sm_100: LDG/STG.256). A warp-wide access where each lane touches its
+// own row then fills whole 32-byte sectors, twice the bytes per L1 request of a 128-bit access
+// (the GEMM epilogues write one accumulator row per thread). Address must be 32-byte aligned.
+HM_DEV void st_global_v8(void* p, const uint4& lo, const uint4& hi) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(lo.x), "r"(lo.y),
+               "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+               : "memory");
+}
+HM_DEV void ld_global_v8(const void* p, uint4& lo, uint4& hi) {
+  asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z),
+                 "=r"(hi.w)
+               : "l"(p));
+}
+
 // ---------------------------------------------------------------------------------------------
 // mbarrier
 

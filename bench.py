@@ -251,10 +251,17 @@ def run_ours(args, ws, rank, local):
         "frac_of_burst_peak": round(gemm_tflops / peaks["bf16_tflops"], 4),
         "frac_of_datasheet_2250": round(gemm_tflops / 2250.0, 4),
         "traffic": None,
+        "traffic_algorithmic_bytes_per_step": gemm_min_bytes(cfg),
         "peak_source": peaks["source"] + ", sustained bf16 (kernel timed inside a long step)",
         "algorithmic_flops_per_step": gemm_flop,
         "gemm_ms_per_step": round(gemm_ms, 3),
     }
+
+    tr = ncu_traffic(cfg.name, "grouped_gemm_kernel", 6)
+    if tr is not None:
+        roofline["traffic"] = tr["bytes"]
+        roofline["traffic_unit"] = "bytes of DRAM read+write per step (the 6 K3 launches)"
+        roofline["traffic_source"] = tr["source"]
 
     # ---- end-to-end through the public API with host buffers: every step copies its inputs
     # (x, dY) from pinned host memory and reads its result (the step's per-expert token
@@ -339,6 +346,34 @@ def run_ours(args, ws, rank, local):
         out["cpu_baseline"] = cpu_baseline(cfg, args.cpu_baseline_tokens)
     if rank == 0:
         _emit(out)
+
+
+def gemm_min_bytes(cfg) -> int:
+    """Compulsory HBM bytes of the six K3 GEMMs of one step (every operand read once, every
+    output written once): the floor roofline.traffic is compared with."""
+    R, d, f, E = cfg.T * cfg.k, cfg.d, cfg.f, cfg.E
+    x, h, act, w_ug, w_d = R * d * 2, R * 2 * f * 2, R * f * 2, E * 2 * f * d * 2, E * d * f * 2
+    return ((x + w_ug + h + act)          # fwd up+gate (SwiGLU epilogue stores h and act)
+            + (act + w_d + x)             # fwd down -> y
+            + (x + w_d + h + h)           # bwd dact: dY, W_d, saved h -> dH
+            + (h + w_ug + x)              # bwd dX
+            + (h + x + w_ug)              # wgrad dW_ug
+            + (x + act + w_d))            # wgrad dW_d
+
+
+def ncu_traffic(config_name: str, kernel_prefix: str, launches: int):
+    """DRAM bytes (read + write) of one step's launches of `kernel_prefix`, from the committed
+    `ncu --set full` capture summary profiles/ncu_traffic_<config>.json (tools/summarize_ncu.py),
+    or None when there is no capture for this config."""
+    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{config_name.split('-')[0]}.json")
+    if not os.path.exists(path):
+        return None
+    rec = json.load(open(path))
+    ls = [r for r in rec["launches"] if r["kernel"].startswith(kernel_prefix)][:launches]
+    if len(ls) < launches or any(r["dram_read_bytes"] is None for r in ls):
+        return None
+    return {"bytes": int(sum(r["dram_read_bytes"] + r["dram_write_bytes"] for r in ls)),
+            "source": os.path.relpath(path, ROOT) + " (" + rec["source"] + ")"}
 
 
 def cpu_baseline(cfg, tokens: int):

@@ -6,6 +6,8 @@
 
 import csv
 import io
+import json
+import os
 import re
 import subprocess
 import sys
@@ -77,6 +79,21 @@ def full(path, out):
         lines.append(f"| `{_short(r[idx['Kernel Name']])}` | " + " | ".join(cells) + " |")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
+    # JSON sidecar: per-launch DRAM bytes (bench.py reads it for roofline.traffic)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tscale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9}
+
+    def val(r, m, table):
+        i = idx.get(m)
+        if i is None or not r[i]:
+            return None
+        return float(r[i].replace(",", "")) * table.get(units[i], 1.0)
+
+    recs = [{"kernel": _short(r[idx["Kernel Name"]]),
+             "dram_read_bytes": val(r, "dram__bytes_read.sum", scale),
+             "dram_write_bytes": val(r, "dram__bytes_write.sum", scale),
+             "duration_s": val(r, "gpu__time_duration.sum", tscale)} for r in data]
+    json.dump({"source": path, "launches": recs}, open(os.path.splitext(out)[0] + ".json", "w"), indent=1)
 
 
 if __name__ == "__main__":

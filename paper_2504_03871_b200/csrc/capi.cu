@@ -165,12 +165,28 @@ int gemm_wide_mask();
 
 // CTA count / tile width dispatch for one GEMM kind: 1 CTA (HM_GEMM_CTAS=1), a CTA pair with
 // 256 x 256 tiles, or a CTA pair with 256 x 512 tiles (modes in the wide mask)
+int gemm_group_m(int mode);
+
 template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
-int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
+int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p0,
                 const TileBound& tb, int max_ctas, cudaStream_t st) {
+  hm::GroupedGemmParams p = p0;
+  p.group_m = gemm_group_m(mode);
   if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1>(ma, mb, p, tb, max_ctas, st);
   if ((gemm_wide_mask() >> mode) & 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
   return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1>(ma, mb, p, tb, max_ctas, st);
+}
+
+// raster group height per GEMM mode (HM_GEMM_GROUPM = one value for every mode)
+int g_group_m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+int gemm_group_m(int mode) {
+  if (mode < 0 || mode >= 8) return hm::kGroupM;
+  if (g_group_m[mode] <= 0) {
+    const char* s = getenv("HM_GEMM_GROUPM");
+    const int v = s ? atoi(s) : 0;
+    g_group_m[mode] = v > 0 ? v : hm::kGroupM;
+  }
+  return g_group_m[mode];
 }
 
 int gemm_stats_enabled() {
@@ -273,6 +289,14 @@ int hm_gemm_stats(unsigned long long* out) {
 int hm_debug_set_gemm_wide(int mask) {
   const int old = gemm_wide_mask();
   g_wide_mask = mask;
+  return old;
+}
+// tuning aid (not part of the ABI): raster group height of one GEMM mode (mode < 0: all modes;
+// value <= 0: back to the default); returns the previous value of `mode` (or of mode 0)
+int hm_debug_set_gemm_groupm(int mode, int value) {
+  const int old = gemm_group_m(mode < 0 ? 0 : mode);
+  for (int m = 0; m < 8; ++m)
+    if (mode < 0 || m == mode) g_group_m[m] = value;
   return old;
 }
 const char* hm_last_error(void) { return g_last_error.c_str(); }
@@ -449,7 +473,8 @@ int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, co
 
 size_t hm_router_bwd_part_elems(int T, int d, int E, int k) {
   // dlogit in permuted-row order (T*k) followed by the per-split dWg partials
-  return static_cast<size_t>(T) * k + static_cast<size_t>(hm::kWgSplit) * E * d;
+  const int splits = hm::kWgSplit > hm::kWgTokSplit ? hm::kWgSplit : hm::kWgTokSplit;
+  return static_cast<size_t>(T) * k + static_cast<size_t>(splits) * E * d;
 }
 
 int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
@@ -468,9 +493,26 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   auto dp = static_cast<const __nv_bfloat16*>(dx_perm);
   auto gt = static_cast<const __nv_bfloat16*>(wg_t);
   auto out = static_cast<__nv_bfloat16*>(dx);
-  float* dl_perm = dwg ? part : nullptr;
-  HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dlogit, dl_perm)));
+  // dWg: token-major (each token row read once) for E <= 8, k <= 3 and d % 64 == 0, else per
+  // expert over the permuted rows (each routed copy read once)
+  const bool tok = dwg && E <= 8 && k <= 3 && d % 64 == 0 && !getenv("HM_ROUTER_WGRAD_PERM");
+  float* dl_perm = (dwg && !tok) ? part : nullptr;
+  float* dl_tok = dlogit ? dlogit : (tok ? part : nullptr);
+  HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
   if (int rc = check_launch("unpermute_router_bwd")) return rc;
+  if (tok) {
+    float* partials = part + static_cast<size_t>(T) * k;
+    auto xp = static_cast<const __nv_bfloat16*>(x_perm);
+    const dim3 grid(d / 64, hm::kWgTokSplit);
+    if (k == 1) hm::router_wgrad_tok_kernel<1><<<grid, 256, 0, st>>>(xp, row_of, idx, dl_tok, T, d, E, partials);
+    else if (k == 2) hm::router_wgrad_tok_kernel<2><<<grid, 256, 0, st>>>(xp, row_of, idx, dl_tok, T, d, E, partials);
+    else hm::router_wgrad_tok_kernel<3><<<grid, 256, 0, st>>>(xp, row_of, idx, dl_tok, T, d, E, partials);
+    if (int rc = check_launch("router_wgrad_tok")) return rc;
+    const long n = static_cast<long>(d) * E;
+    hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+        partials, hm::kWgTokSplit, d, E, static_cast<__nv_bfloat16*>(dwg));
+    return check_launch("router_wgrad_reduce");
+  }
   if (dwg) {
     float* partials = part + static_cast<size_t>(T) * k;
     dim3 grid(E * hm::kWgSplit, (d + 2047) / 2048);
@@ -629,10 +671,6 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
       uint32_t box[3] = {64, 64, 1};
       if (int rc = make_map(&mb, b, 3, dims, str, box)) return rc;
     }
-    // raster: keep the larger operand outer so the smaller one is reused from L2
-    const double a_bytes = (double)rows / E * K;  // per-expert activation panel
-    const double b_bytes = (double)N * K;
-    p.n_fastest = (a_bytes > b_bytes) ? 1 : 0;
   } else {
     uint64_t dims_a[2] = {(uint64_t)M, (uint64_t)rows_m};
     uint64_t str_a[1] = {(uint64_t)M * 2};
@@ -641,7 +679,6 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
     uint64_t dims_b[2] = {(uint64_t)N, (uint64_t)rows_m};
     uint64_t str_b[1] = {(uint64_t)N * 2};
     if (int rc = make_map(&mb, b, 2, dims_b, str_b, box)) return rc;
-    p.n_fastest = (M >= N) ? 1 : 0;
     // per-expert views (device side, no host sync on the expert sizes)
     CUtensorMap* maps = static_cast<CUtensorMap*>(workspace);
     hm::SegBases bases{};
@@ -717,7 +754,6 @@ int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void
   p.out = static_cast<__nv_bfloat16*>(out);
   p.out_f32 = static_cast<float*>(out);
   p.ldo = ldo;
-  p.n_fastest = (M >= N) ? 1 : 0;
   p.expert_maps = maps;
   p.out_elems = static_cast<long>(E) * M * ldo;
   const TileBound tb{true, 0, M, N, E};

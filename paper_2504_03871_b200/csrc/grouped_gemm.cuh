@@ -44,7 +44,7 @@ constexpr int kTmemCols = 512;  // 2 accumulators x 256 columns
 //           each CTA stages its own 128 rows of A and half (128 columns) of B, the leader CTA
 //           issues the MMAs, each CTA's TMEM receives its 128 accumulator rows.
 constexpr int kBookkeepingBytes = 4096;  // GemmShared, placed first; tiles start 1024-aligned
-constexpr int kGroupM = 8;                // raster group height (tiles)
+constexpr int kGroupM = 8;                // default raster group height (tiles)
 constexpr int kMaxSegs = 16;              // wgrad: micro-batch segments per expert (K concatenation)
 
 // NSUB = 2 ("wide" tile, CTA pairs only): the tile is 256 x 512 — two UMMA N=256 sub-tiles
@@ -82,7 +82,7 @@ struct GroupedGemmParams {
   int ldo2;
   const __nv_bfloat16* aux;  // SWIGLU_BWD: h saved by the forward [rows, 2N]
   int ld_aux;
-  int n_fastest;  // raster: 1 = n-tile index varies fastest within an expert
+  int group_m;    // raster: m-tiles per group (m fastest inside a group, then n, then next group)
   const CUtensorMap* expert_maps;  // GROUP_K: per-(expert, segment) TMA views, [(e*R+j)*2] = A, +1 = B
   int R;                           // GROUP_K: segments per expert (seg_offsets is [R][E+1])
   float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
@@ -218,7 +218,7 @@ struct TileCoord {
 
 template <bool GROUP_K, int TILE_M>
 HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_fixed, int ntiles,
-                             int n_fastest) {
+                             int group_m) {
   // binary search: largest e with tile_prefix[e] <= tile
   int lo = 0, hi = E - 1;
   while (lo < hi) {
@@ -231,14 +231,14 @@ HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_f
   else mtiles = (sh.seg[lo + 1] - sh.seg[lo] + TILE_M - 1) / TILE_M;
   TileCoord c;
   c.e = lo;
-  // grouped raster: groups of kGroupM m-tiles, m fastest inside a group, then n, then the
-  // next group. The ~74-148 concurrently running tiles then form an ~8 x 9 block, so every
-  // A and B panel they stream is shared by ~8 concurrent tiles (L2 reuse along long K).
-  (void)n_fastest;
-  const int group = local / (kGroupM * ntiles);
-  const int rem = local - group * kGroupM * ntiles;
-  const int gm = min(kGroupM, mtiles - group * kGroupM);
-  c.mt = group * kGroupM + rem % gm;
+  // grouped raster: groups of group_m m-tiles, m fastest inside a group, then n, then the
+  // next group. With group_m = 8 the ~74 concurrently running tiles form an ~8 x 9 block, so
+  // every A and B panel they stream is shared by ~8 concurrent tiles (L2 reuse along long K).
+  const int gmax = group_m;
+  const int group = local / (gmax * ntiles);
+  const int rem = local - group * gmax * ntiles;
+  const int gm = min(gmax, mtiles - group * gmax);
+  c.mt = group * gmax + rem % gm;
   c.nt = rem / gm;
   return c;
 }
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
            tile = next_tile<CTAS, false>(sh, tile, tile_step, ci, true)) {
         if (tile >= total_tiles) continue;  // a stolen cluster index past the real tile count
-        const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+        const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.group_m);
         const int seg0 = sh.seg[tc.e];
         const int nk = GROUP_K ? sh.nk[tc.e] : (p.K + kBK - 1) / kBK;
         const CUtensorMap* mA = &map_a;
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
            tile = next_tile<CTAS, true>(sh, tile, tile_step, ci, lane == 0)) {
         if (tile >= total_tiles) continue;
-        const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+        const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.group_m);
         const int nk = GROUP_K ? sh.nk[tc.e] : (p.K + kBK - 1) / kBK;
         if (nk == 0) continue;  // epilogue writes zeros for this tile without touching TMEM
         const int acc = kAccBufs == 2 ? (tcount & 1) : 0;
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int tile = tile0; p.dynamic ? tile >= 0 : tile < total_tiles;
          tile = next_tile<CTAS, true>(sh, tile, tile_step, ci, lane == 0)) {
       if (tile >= total_tiles) continue;
-      const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.n_fastest);
+      const TileCoord tc = decode_tile<GROUP_K, kTileM>(sh, E, tile, mtiles_fixed, ntiles, p.group_m);
       const int seg0 = sh.seg[tc.e];
       const int me = sh.seg[tc.e + 1] - seg0;
       long grow;       // global output row

@@ -189,8 +189,15 @@ __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
 #pragma unroll
         for (int a = 0; a < TT; ++a) {
           const float xf = bf16_to_f32(reinterpret_cast<const uint16_t*>(&xv[a])[q]);
+          // packed fp32x2 FMAs (FFMA2): two independent IEEE fma.rn per instruction, so every
+          // accumulator sees exactly the scalar sequence (bit-identical logits)
 #pragma unroll
-          for (int e = 0; e < EG; ++e) acc[a][e] = __fmaf_rn(xf, wv[e], acc[a][e]);
+          for (int e = 0; e < EG; e += 2) {
+            const float2 r = __ffma2_rn(make_float2(xf, xf), make_float2(wv[e], wv[e + 1]),
+                                        make_float2(acc[a][e], acc[a][e + 1]));
+            acc[a][e] = r.x;
+            acc[a][e + 1] = r.y;
+          }
         }
       }
 #pragma unroll
@@ -646,6 +653,118 @@ __global__ void __launch_bounds__(256)
     float4* out = reinterpret_cast<float4*>(part + (static_cast<long>(split) * E + e) * d + col);
     out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// Token-major router weight gradient for E <= 8: dWg[i, e] = sum_t x[t, i] * dlogit_dense[t, e]
+// (dlogit_dense = the selected experts' dlogits, zeros elsewhere — the dense formula autograd
+// uses). Each token row is read ONCE (from its first routed copy, x_perm[row_of[t, 0]]) instead
+// of once per routed copy: T*d*2 bytes instead of T*k*d*2. grid = (d / 64, kWgTokSplit); thread
+// (tl, cg) = (tid / 8, tid % 8) owns columns [64*bx + 8*cg, +8) and tokens tl, tl + 32, ... of
+// its split; a warp load covers 4 tokens x 128 contiguous bytes. Partials: fixed-order butterfly
+// over the warp's 4 token lanes, then over the 8 warps in shared memory, then over the splits
+// (router_wgrad_reduce) — deterministic.
+constexpr int kWgTokSplit = 8;
+constexpr int kWgTokUnroll = 4;
+template <int K>
+__global__ void __launch_bounds__(256, 2)
+    router_wgrad_tok_kernel(const __nv_bfloat16* __restrict__ x_perm, const int32_t* __restrict__ row_of,
+                            const int32_t* __restrict__ idx, const float* __restrict__ dlogit, int T,
+                            int d, int E, float* __restrict__ part /*[kWgTokSplit][E][d]*/) {
+  __shared__ float red[8][8][64];  // [warp][cg][e * 8 + z]
+  const int tid = threadIdx.x;
+  const int cg = tid & 7, tl = tid >> 3;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int col = blockIdx.x * 64 + cg * 8;
+  const int split = blockIdx.y;
+  const int a = static_cast<int>((static_cast<long>(T) * split) / kWgTokSplit);
+  const int b = static_cast<int>((static_cast<long>(T) * (split + 1)) / kWgTokSplit);
+  constexpr int U = kWgTokUnroll;
+  float acc[8][8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int z = 0; z < 8; ++z) acc[e][z] = 0.f;
+  // software pipeline: the row index and (expert, dlogit) pairs of group g+1 are loaded while
+  // group g's rows are in flight, so each group costs one memory round trip, not two
+  int row[U], ex[U][K];
+  float dl[U][K];
+  auto load_meta = [&](int t0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = t0 + 32 * u;
+      const bool ok = t < b;
+      row[u] = ok ? __ldg(row_of + static_cast<long>(t) * K) : -1;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        ex[u][s] = ok ? __ldg(idx + static_cast<long>(t) * K + s) : -1;
+        dl[u][s] = ok ? __ldg(dlogit + static_cast<long>(t) * K + s) : 0.f;
+      }
+    }
+  };
+  load_meta(a + tl);
+  for (int t0 = a + tl; t0 < b; t0 += 32 * U) {
+    uint4 xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      xv[u] = row[u] >= 0 ? __ldg(reinterpret_cast<const uint4*>(x_perm + static_cast<long>(row[u]) * d + col))
+                          : make_uint4(0u, 0u, 0u, 0u);
+    int cex[U][K];
+    float cdl[U][K];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s = 0; s < K; ++s) { cex[u][s] = ex[u][s]; cdl[u][s] = dl[u][s]; }
+    load_meta(t0 + 32 * U);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float coef[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float c = 0.f;
+#pragma unroll
+        for (int s = 0; s < K; ++s) c = (cex[u][s] == e) ? cdl[u][s] : c;
+        coef[e] = c;
+      }
+      const uint16_t* h = reinterpret_cast<const uint16_t*>(&xv[u]);
+#pragma unroll
+      for (int z = 0; z < 8; z += 2) {
+        const float2 xf = make_float2(bf16_to_f32(h[z]), bf16_to_f32(h[z + 1]));
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float2 r = __ffma2_rn(make_float2(coef[e], coef[e]), xf, make_float2(acc[e][z], acc[e][z + 1]));
+          acc[e][z] = r.x;
+          acc[e][z + 1] = r.y;
+        }
+      }
+    }
+  }
+  // the warp's 4 token lanes (lane bits 3, 4) -> lanes 0..7
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int z = 0; z < 8; ++z) {
+      float v = acc[e][z];
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      acc[e][z] = v;
+    }
+  if (lane < 8) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int z = 0; z < 8; ++z) red[warp][lane][e * 8 + z] = acc[e][z];
+  }
+  __syncthreads();
+  // 8 cg x 64 (e, z) sums over the 8 warps; thread -> two of them
+  for (int i = tid; i < 8 * 64; i += 256) {
+    const int g = i >> 6, ez = i & 63;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][g][ez];
+    const int e = ez >> 3, z = ez & 7;
+    const int c = blockIdx.x * 64 + g * 8 + z;
+    if (e < E && c < d) part[(static_cast<long>(split) * E + e) * d + c] = s;
   }
 }
 

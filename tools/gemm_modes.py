@@ -2,7 +2,7 @@
 C2 layer, each run alone back to back (CUDA events, median of --reps). GPU box only.
 
     python tools/gemm_modes.py [C2|C3] [--reps 20]
-Environment knobs read by the library (HM_GEMM_WIDE, HM_GEMM_MC, HM_GEMM_STATS) select variants;
+Environment knobs read by the library (HM_GEMM_WIDE, HM_GEMM_GROUPM, HM_GEMM_STATS) select variants;
 run one process per setting."""
 import argparse
 import ctypes
@@ -22,7 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", nargs="?", default="C2")
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--ab", default="", help="comma-separated wide-tile masks timed interleaved")
+    ap.add_argument("--ab", default="", help="comma-separated variants 'WIDE_MASK[:GROUP_M]' timed "
+                    "interleaved (e.g. 0x3A:8,0x3A:16)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     dev = torch.device("cuda")
@@ -58,7 +59,12 @@ def main():
                        2 * rows * d * f),
     }
     out = {"config": args.config, "env": {k: v for k, v in os.environ.items() if k.startswith("HM_")}}
-    masks = [int(m, 0) for m in args.ab.split(",")] if args.ab else [None]
+    masks = args.ab.split(",") if args.ab else [None]
+
+    def select(m):
+        wide, _, gm = m.partition(":")
+        lib.hm_debug_set_gemm_wide(int(wide, 0))
+        lib.hm_debug_set_gemm_groupm(-1, int(gm) if gm else 0)
 
     def one(fn):
         a = torch.cuda.Event(enable_timing=True)
@@ -72,7 +78,7 @@ def main():
     for name, (fn, flops) in gemms.items():
         for m in masks:
             if m is not None:
-                lib.hm_debug_set_gemm_wide(m)
+                select(m)
             for _ in range(2):
                 fn()
         torch.cuda.synchronize()
@@ -80,7 +86,7 @@ def main():
         for _ in range(args.reps):  # variants interleaved so clock / power drift hits all alike
             for m in masks:
                 if m is not None:
-                    lib.hm_debug_set_gemm_wide(m)
+                    select(m)
                 ts[m].append(one(fn))
         for m in masks:
             t = sorted(ts[m])
@@ -89,7 +95,7 @@ def main():
                    "tflops_med": round(flops / med / 1e9, 1)}
             if stats:
                 if m is not None:
-                    lib.hm_debug_set_gemm_wide(m)
+                    select(m)
                 lib.hm_gemm_stats(buf)
                 fn()
                 lib.hm_gemm_stats(buf)
@@ -100,9 +106,10 @@ def main():
                 rec["head_share_of_tma_wait"] = round(v[6] / max(v[0], 1), 3)
                 rec["producer_wait_stage"] = round(v[3] / tot, 3)
                 rec["tiles"] = v[4]
-            out[name if m is None else f"{name}@{m:#x}"] = rec
+            out[name if m is None else f"{name}@{m}"] = rec
         if masks[0] is not None:
             lib.hm_debug_set_gemm_wide(-1)
+            lib.hm_debug_set_gemm_groupm(-1, 0)
     print(json.dumps(out))
 
 

@@ -1,0 +1,79 @@
+"""Router forward / backward timing on one config (GPU box): K1 (logits + top-k + scan) and the
+router backward with the token-major and the permuted-row weight-gradient kernels, interleaved.
+
+    python tools/router_bench.py [C2|C3] [--reps 30]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from bench import make_layer_tensors  # noqa: E402
+from paper_2504_03871_b200 import ops  # noqa: E402
+from paper_2504_03871_b200.configs import CONFIGS  # noqa: E402
+
+
+_BUSY = None
+
+
+def timed(fn, reps, inner=10):
+    """Median over `reps` of the device time of `inner` back-to-back calls, each batch queued
+    behind a ~5 ms matmul so host launch overhead never starves the GPU."""
+    global _BUSY
+    if _BUSY is None:
+        _BUSY = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        for _ in range(4):
+            _BUSY @ _BUSY
+        a.record()
+        for _ in range(inner):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / inner)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", nargs="?", default="C2")
+    ap.add_argument("--reps", type=int, default=30)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    x, wg, w_ug, w_d, dy = make_layer_tensors(cfg, 1, torch.device("cuda"))
+    r = ops.router_topk(x, wg, cfg.k)
+    xp, _, row_of = ops.dispatch_permute(x, r)
+    dxp = torch.randn_like(xp)
+    dw = torch.randn_like(r.w)
+    wg_t = ops.transpose_bf16(wg)
+    T, d, E, k = cfg.T, cfg.d, cfg.E, cfg.k
+    out = {"config": args.config}
+    out["router_fwd_ms"] = timed(lambda: ops.router_topk(x, wg, k), args.reps)
+    res = {}
+    for variant in ("tok", "perm", "tok", "perm"):
+        if variant == "perm":
+            os.environ["HM_ROUTER_WGRAD_PERM"] = "1"
+        else:
+            os.environ.pop("HM_ROUTER_WGRAD_PERM", None)
+        ms = timed(lambda: ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True), args.reps)
+        res.setdefault(variant, []).append(ms)
+        res.setdefault(variant + "_dwg", ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True)[2].float())
+    out["router_bwd_ms"] = {v: min(res[v]) for v in ("tok", "perm")}
+    a, b = res["tok_dwg"], res["perm_dwg"]
+    out["dwg_rel_diff_tok_vs_perm"] = float((a - b).norm() / b.norm())
+    fwd_bytes = T * d * 2 + d * E * 2 + T * k * 8 + 8 * E
+    bwd_bytes = 2 * T * k * d * 2 + T * d * 2  # unpermute + dlogit.Wg, dWg from x (token-major)
+    out["router_fwd_gbs"] = fwd_bytes / out["router_fwd_ms"] / 1e6
+    out["router_bwd_gbs"] = {v: bwd_bytes / ms / 1e6 for v, ms in out["router_bwd_ms"].items()}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -334,14 +334,26 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
       const int cap = (num_sms() + ngroups - 1) / ngroups;
       if (gx > cap) gx = cap;
       dim3 grid(gx, ngroups);
+      if (ngroups == 1 && !getenv("HM_ROUTER_UNFUSED")) {
+        // one expert group: top-k, softmax and chunk histogram fused into the logits kernel
+        auto kern = eg2 == 8 ? hm::router_logits2_kernel<8, tt, true> : hm::router_logits2_kernel<16, tt, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits, k, idx, w,
+                                                           chunk_base);
+        if (int rc = check_launch("router_logits2_topk")) return rc;
+        hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
+        return check_launch("router_scan");
+      }
       if (eg2 == 8) {
         auto kern = hm::router_logits2_kernel<8, tt>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits);
+        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
+                                                           nullptr, nullptr);
       } else {
         auto kern = hm::router_logits2_kernel<16, tt>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits);
+        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
+                                                           nullptr, nullptr);
       }
       if (int rc = check_launch("router_logits2")) return rc;
       hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);

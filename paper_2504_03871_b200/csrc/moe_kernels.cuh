@@ -126,11 +126,20 @@ HM_DEV int router2_row_off(int i, int eg) {  // float offset of row i in the pad
   return i * eg + (i >> 3) * 4;
 }
 
-template <int EG, int TT>
+// FUSE (one expert group, E == EG, kRouter2Warps * TT == kChunk): the top-k, softmax and
+// per-chunk histogram of router_topk_kernel run in the same kernel on the logits still in
+// registers (identical comparisons and arithmetic, so identical results), one chunk per CTA
+// iteration.
+template <int EG, int TT, bool FUSE = false>
 __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
     router_logits2_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
                           const float* __restrict__ bias, int T, int d, int E,
-                          float* __restrict__ logits) {
+                          float* __restrict__ logits, int k = 0, int32_t* __restrict__ idx = nullptr,
+                          float* __restrict__ w = nullptr,
+                          int32_t* __restrict__ chunk_counts = nullptr) {
+  static_assert(!FUSE || kRouter2Warps * TT == kChunk, "fused top-k: one chunk per CTA iteration");
+  __shared__ int hist[FUSE ? EG : 1];
+  if (FUSE && threadIdx.x < EG) hist[threadIdx.x] = 0;
   extern __shared__ __align__(16) uint8_t smem_r2[];
   float* ws = reinterpret_cast<float*>(smem_r2);
   const int e0 = blockIdx.y * EG;
@@ -156,7 +165,9 @@ __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nj = d / 256;
   const int per_iter = kRouter2Warps * TT;
-  for (int t0 = blockIdx.x * per_iter + warp * TT; t0 < T; t0 += gridDim.x * per_iter) {
+  // every warp runs every CTA iteration (the fused histogram synchronises the CTA per chunk)
+  for (int base = blockIdx.x * per_iter; base < T; base += gridDim.x * per_iter) {
+    const int t0 = base + warp * TT;
     float acc[TT][EG];
 #pragma unroll
     for (int a = 0; a < TT; ++a)
@@ -221,9 +232,54 @@ __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
       const int t = t0 + a;
 #pragma unroll
       for (int e = 0; e < EG; ++e) {
-        if (lane == ((a * EG + e) & 31) && t < T && e0 + e < E)
-          logits[static_cast<long>(t) * E + e0 + e] = bias ? acc[a][e] + bias[e0 + e] : acc[a][e];
+        if (bias) acc[a][e] = acc[a][e] + bias[e0 + e];
+        if (lane == ((a * EG + e) & 31) && t < T && e0 + e < E) logits[static_cast<long>(t) * E + e0 + e] = acc[a][e];
       }
+    }
+    if (FUSE) {
+      // lane a < TT selects for token t0 + a (the same comparisons as router_topk_kernel:
+      // strict >, ties -> lower expert id, NaN never selected, all-NaN -> lowest unselected id)
+#pragma unroll
+      for (int a = 0; a < TT; ++a) {
+        const int t = t0 + a;
+        if (lane != a || t >= T) continue;
+        float v[EG];
+#pragma unroll
+        for (int e = 0; e < EG; ++e) v[e] = acc[a][e];
+        float sel_l[kMaxTopK];
+        int sel_e[kMaxTopK];
+        for (int s2 = 0; s2 < k; ++s2) {
+          float bv = -INFINITY;
+          int be = 0x7fffffff;
+#pragma unroll
+          for (int e = 0; e < EG; ++e)
+            if (v[e] > bv || (v[e] == bv && e < be)) { bv = v[e]; be = e; }
+          if (be == 0x7fffffff) {
+            be = 0;
+            for (int q2 = 0; q2 < s2; ++q2)
+              if (sel_e[q2] == be) { ++be; q2 = -1; }
+          }
+          sel_l[s2] = bv;
+          sel_e[s2] = be;
+#pragma unroll
+          for (int e = 0; e < EG; ++e)
+            if (e == be) v[e] = -INFINITY;
+        }
+        float ex[kMaxTopK];
+        float sum = 0.f;
+        for (int s2 = 0; s2 < k; ++s2) { ex[s2] = expf(sel_l[s2] - sel_l[0]); sum += ex[s2]; }
+        for (int s2 = 0; s2 < k; ++s2) {
+          idx[static_cast<long>(t) * k + s2] = sel_e[s2];
+          w[static_cast<long>(t) * k + s2] = ex[s2] / sum;
+          atomicAdd(&hist[sel_e[s2]], 1);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < EG) {
+        chunk_counts[static_cast<long>(base / kChunk) * E + threadIdx.x] = hist[threadIdx.x];
+        hist[threadIdx.x] = 0;
+      }
+      __syncthreads();
     }
   }
 }

@@ -55,7 +55,16 @@ def main():
     wg_t = ops.transpose_bf16(wg)
     T, d, E, k = cfg.T, cfg.d, cfg.E, cfg.k
     out = {"config": args.config}
-    out["router_fwd_ms"] = timed(lambda: ops.router_topk(x, wg, k), args.reps)
+    fw = {}
+    for variant in ("fused", "unfused", "fused", "unfused"):
+        if variant == "unfused":
+            os.environ["HM_ROUTER_UNFUSED"] = "1"
+        else:
+            os.environ.pop("HM_ROUTER_UNFUSED", None)
+        fw.setdefault(variant, []).append(timed(lambda: ops.router_topk(x, wg, k), args.reps))
+    os.environ.pop("HM_ROUTER_UNFUSED", None)
+    out["router_fwd_ms_variants"] = {v: min(t) for v, t in fw.items()}
+    out["router_fwd_ms"] = min(fw["fused"])
     res = {}
     for variant in ("tok", "perm", "tok", "perm"):
         if variant == "perm":

@@ -166,12 +166,14 @@ int gemm_wide_mask();
 // CTA count / tile width dispatch for one GEMM kind: 1 CTA (HM_GEMM_CTAS=1), a CTA pair with
 // 256 x 256 tiles, or a CTA pair with 256 x 512 tiles (modes in the wide mask)
 int gemm_group_m(int mode);
+int g_early_release = getenv("HM_GEMM_NO_EARLY_RELEASE") ? 0 : 1;
 
 template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
 int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p0,
                 const TileBound& tb, int max_ctas, cudaStream_t st) {
   hm::GroupedGemmParams p = p0;
   p.group_m = gemm_group_m(mode);
+  p.early_release = g_early_release;
   if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1>(ma, mb, p, tb, max_ctas, st);
   if ((gemm_wide_mask() >> mode) & 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
   return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1>(ma, mb, p, tb, max_ctas, st);
@@ -297,6 +299,13 @@ int hm_debug_set_gemm_groupm(int mode, int value) {
   const int old = gemm_group_m(mode < 0 ? 0 : mode);
   for (int m = 0; m < 8; ++m)
     if (mode < 0 || m == mode) g_group_m[m] = value;
+  return old;
+}
+// tuning aid (not part of the ABI): wide plain-store epilogue releases its accumulator early (1)
+// or after every store (0); returns the previous setting
+int hm_debug_set_gemm_early_release(int on) {
+  const int old = g_early_release;
+  g_early_release = on;
   return old;
 }
 const char* hm_last_error(void) { return g_last_error.c_str(); }

@@ -91,6 +91,7 @@ struct GroupedGemmParams {
   const unsigned long long* out_rows;  // EPI_STORE: optional per-output-row destination pointer
                                        // (row r -> bf16* out_rows[r], may be a peer GPU's memory)
   long out_elems;  // elements of out (bounds checks in HM_BOUNDS_CHECK builds)
+  int early_release;  // wide plain-store epilogue: release the accumulator before the last stores
 };
 
 // HM_BOUNDS_CHECK builds record the first out-of-range access in g_hm_dbg (and skip it) so a
@@ -591,6 +592,70 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       const int acc = kAccBufs == 2 ? (tcount & 1) : 0;
       const uint32_t aph = (kAccBufs == 2 ? (tcount >> 1) : tcount) & 1;
+
+      if (EPI == EPI_STORE && NSUB == 2 && p.early_release) {
+        // Wide tile, plain store. The single accumulator (2 x 128 columns per thread) is drained
+        // in 16-column chunks: the first kStream chunks are stored straight from TMEM, the other
+        // kHeld are packed to bf16 in registers, then the accumulator is RELEASED and the held
+        // chunks are stored while the next tile's MMAs already run (12 of 16 chunks' stores
+        // leave the MMA critical path; holding all 16 would need 128 registers and spill).
+        constexpr int kChunks = 16, kStream = 8, kHeld = kChunks - kStream;
+        uint32_t pk[kHeld][8];
+        mbar_wait(&sh.tmem_full[acc], aph);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+        auto chunk_dst = [&](int ch, int& nv) -> __nv_bfloat16* {
+          const int u = ch >> 3;
+          const int n0 = (tc.nt * NSUB + u) * kBN;
+          const int c = half * 128 + (ch & 7) * 16;
+          nv = min(16, p.N - n0 - c);
+          return p.out_rows ? reinterpret_cast<__nv_bfloat16*>(p.out_rows[grow]) + n0 + c
+                            : p.out + grow * p.ldo + n0 + c;
+        };
+        auto store16 = [&](__nv_bfloat16* dst, int nv, const uint32_t (&v)[8]) {
+          if (nv == 16 && (reinterpret_cast<uintptr_t>(dst) & 31u) == 0) {
+            st_global_v8(dst, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]));
+          } else {
+            uint16_t* d16 = reinterpret_cast<uint16_t*>(dst);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nv) d16[j] = static_cast<uint16_t>(v[j >> 1] >> (16 * (j & 1)));
+          }
+        };
+        auto load16 = [&](int ch, uint32_t (&v)[8]) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(t_row + (acc + (ch >> 3)) * kBN + half * 128 + (ch & 7) * 16, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        };
+#pragma unroll
+        for (int ch = 0; ch < kStream; ++ch) {
+          uint32_t v[8];
+          load16(ch, v);
+          int nv;
+          __nv_bfloat16* dst = chunk_dst(ch, nv);
+          if (row_ok && nv > 0) store16(dst, nv, v);
+        }
+#pragma unroll
+        for (int ch = kStream; ch < kChunks; ++ch) load16(ch, pk[ch - kStream]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CTAS == 2) mbar_arrive_cluster(mapa_shared(&sh.tmem_empty[acc], 0));
+          else mbar_arrive(&sh.tmem_empty[acc]);
+        }
+        ++tcount;
+        if (row_ok) {
+#pragma unroll
+          for (int ch = kStream; ch < kChunks; ++ch) {
+            int nv;
+            __nv_bfloat16* dst = chunk_dst(ch, nv);
+            if (nv > 0) store16(dst, nv, pk[ch - kStream]);
+          }
+        }
+        continue;
+      }
 
 #pragma unroll 1
       for (int u = 0; u < NSUB; ++u) {

@@ -62,9 +62,11 @@ def main():
     masks = args.ab.split(",") if args.ab else [None]
 
     def select(m):
-        wide, _, gm = m.partition(":")
-        lib.hm_debug_set_gemm_wide(int(wide, 0))
-        lib.hm_debug_set_gemm_groupm(-1, int(gm) if gm else 0)
+        # WIDE_MASK[:GROUP_M[:EARLY_RELEASE]]
+        parts = m.split(":")
+        lib.hm_debug_set_gemm_wide(int(parts[0], 0))
+        lib.hm_debug_set_gemm_groupm(-1, int(parts[1]) if len(parts) > 1 and parts[1] else 0)
+        lib.hm_debug_set_gemm_early_release(int(parts[2]) if len(parts) > 2 else 1)
 
     def one(fn):
         a = torch.cuda.Event(enable_timing=True)
@@ -110,6 +112,7 @@ def main():
         if masks[0] is not None:
             lib.hm_debug_set_gemm_wide(-1)
             lib.hm_debug_set_gemm_groupm(-1, 0)
+            lib.hm_debug_set_gemm_early_release(1)
     print(json.dumps(out))
 
 

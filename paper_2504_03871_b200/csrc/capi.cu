@@ -203,7 +203,7 @@ int gemm_stats_enabled() {
 // GEMM modes (bit = HM_GEMM_* mode) that use the 256 x 512 "wide" pair tile; HM_GEMM_WIDE
 // overrides the default (measured per mode on B200)
 #ifndef HM_GEMM_WIDE_DEFAULT
-#define HM_GEMM_WIDE_DEFAULT 0x3A  // down, dX, both wgrads: plain-store epilogues, long K
+#define HM_GEMM_WIDE_DEFAULT 0x3B  // up+gate, down, dX, both wgrads (not the SwiGLU backward)
 #endif
 int g_wide_mask = -1;
 int gemm_wide_mask() {

@@ -791,21 +791,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int q = 0; q < 4; ++q) {
               const uint16_t* gs = reinterpret_cast<const uint16_t*>(&gcur[q]);
               const uint16_t* us = reinterpret_cast<const uint16_t*>(&ucur[q]);
-              float dg[8], du[8];
+              uint32_t pg[4], pu[4];
 #pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float g = bf16_to_f32(gs[j]);
-                const float u = bf16_to_f32(us[j]);
-                const float sg = sigmoid_f(g);
-                const float d = da[q * 8 + j];
-                du[j] = d * g * sg;
-                dg[j] = d * u * sg * (1.0f + g * (1.0f - sg));
+              for (int j = 0; j < 8; j += 2) {
+                // element pairs in packed fp32x2 arithmetic (FMUL2 / FFMA2): du = d*sg*g,
+                // dg = d*sg*u*(1 + g*(1 - sg)); the sigmoids stay scalar MUFU
+                const float2 g2 = make_float2(bf16_to_f32(gs[j]), bf16_to_f32(gs[j + 1]));
+                const float2 u2 = make_float2(bf16_to_f32(us[j]), bf16_to_f32(us[j + 1]));
+                const float2 sg2 = make_float2(sigmoid_f(g2.x), sigmoid_f(g2.y));
+                const float2 d2 = make_float2(da[q * 8 + j], da[q * 8 + j + 1]);
+                const float2 one2 = make_float2(1.0f, 1.0f);
+                const float2 t2 = __fmul2_rn(d2, sg2);
+                const float2 du2 = __fmul2_rn(t2, g2);
+                const float2 om2 = __ffma2_rn(sg2, make_float2(-1.0f, -1.0f), one2);
+                const float2 k2 = __ffma2_rn(g2, om2, one2);
+                const float2 dg2 = __fmul2_rn(__fmul2_rn(t2, u2), k2);
+                pg[j >> 1] = pack_bf16x2(dg2.x, dg2.y);
+                pu[j >> 1] = pack_bf16x2(du2.x, du2.y);
               }
               uint4 wg, wu;
-              wg.x = pack_bf16x2(dg[0], dg[1]); wg.y = pack_bf16x2(dg[2], dg[3]);
-              wg.z = pack_bf16x2(dg[4], dg[5]); wg.w = pack_bf16x2(dg[6], dg[7]);
-              wu.x = pack_bf16x2(du[0], du[1]); wu.y = pack_bf16x2(du[2], du[3]);
-              wu.z = pack_bf16x2(du[4], du[5]); wu.w = pack_bf16x2(du[6], du[7]);
+              wg.x = pg[0]; wg.y = pg[1]; wg.z = pg[2]; wg.w = pg[3];
+              wu.x = pu[0]; wu.y = pu[1]; wu.z = pu[2]; wu.w = pu[3];
               wgs[q] = wg;
               wus[q] = wu;
             }

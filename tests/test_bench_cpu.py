@@ -1,0 +1,32 @@
+"""CPU checks of bench.py's roofline bookkeeping (no GPU): the compulsory-bytes floor of the six
+K3 GEMMs and the DRAM traffic read back from the committed ncu capture summary."""
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+
+import bench  # noqa: E402
+from paper_2504_03871_b200.configs import CONFIGS  # noqa: E402
+
+
+def test_gemm_min_bytes_c2():
+    c = CONFIGS["C2"]
+    R, d, f, E = c.T * c.k, c.d, c.f, c.E
+    # per GEMM: operands read once, outputs written once (bf16)
+    want = 2 * (R * d + E * 2 * f * d + R * 2 * f + R * f          # up+gate -> h, act
+                + R * f + E * d * f + R * d                       # down -> y
+                + R * d + E * d * f + R * 2 * f + R * 2 * f       # SwiGLU bwd -> dH
+                + R * 2 * f + E * 2 * f * d + R * d               # dX
+                + R * 2 * f + R * d + E * 2 * f * d               # dW_ug
+                + R * d + R * f + E * d * f)                      # dW_d
+    assert bench.gemm_min_bytes(c) == want
+
+
+def test_ncu_traffic_reads_committed_capture():
+    tr = bench.ncu_traffic(CONFIGS["C2"].name, "grouped_gemm_kernel", 6)
+    assert tr is not None, "profiles/ncu_traffic_C2.json missing"
+    floor = bench.gemm_min_bytes(CONFIGS["C2"])
+    # measured DRAM bytes can only exceed the compulsory floor (L2 re-reads), within reason
+    assert floor <= tr["bytes"] < 4 * floor
+    assert bench.ncu_traffic("C9-none", "grouped_gemm_kernel", 6) is None

@@ -331,6 +331,28 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
   }
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(wg);
+  if (E % 8 == 0 && E > 16 && aligned16(wg) && !getenv("HM_ROUTER_V1") && !getenv("HM_ROUTER_EG16")) {
+    // many expert groups: 8 experts x 8 tokens per warp, 8 warps, 2 CTAs per SM (half the
+    // shared-memory weight traffic per FMA of the 16 x 4 shape); same order, same logits
+    const size_t smem3 = static_cast<size_t>(d) * 8 * 4 + static_cast<size_t>(d / 8) * 16;
+    if (smem3 <= 200 * 1024) {
+      const int ngroups = E / 8;
+      constexpr int tt = 8, nw = 8;
+      const int per_iter = nw * tt;
+      int gx = (T + per_iter - 1) / per_iter;
+      const int cap = (2 * num_sms() + ngroups - 1) / ngroups;
+      if (gx > cap) gx = cap;
+      auto kern = hm::router_logits2_kernel<8, tt, false, nw, 2, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
+      kern<<<dim3(gx, ngroups), nw * 32, smem3, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
+                                                       nullptr, nullptr);
+      if (int rc = check_launch("router_logits2(8x8)")) return rc;
+      hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+      if (int rc = check_launch("router_topk")) return rc;
+      hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
+      return check_launch("router_scan");
+    }
+  }
   if (E % 8 == 0 && aligned16(wg) && !getenv("HM_ROUTER_V1")) {
     // fp32-staged, bank-conflict-free variant (same summation order, bit-identical logits)
     const int eg2 = E == 8 ? 8 : 16;

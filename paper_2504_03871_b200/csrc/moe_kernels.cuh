@@ -130,14 +130,18 @@ HM_DEV int router2_row_off(int i, int eg) {  // float offset of row i in the pad
 // per-chunk histogram of router_topk_kernel run in the same kernel on the logits still in
 // registers (identical comparisons and arithmetic, so identical results), one chunk per CTA
 // iteration.
-template <int EG, int TT, bool FUSE = false>
-__global__ void __launch_bounds__(kRouter2Warps * 32, 1)
+// NW warps per CTA, MINB CTAs per SM: (16, 1) by default; the many-group case (E > 16) uses
+// EG = 8 experts x TT = 8 tokens per warp with (8, 2): every shared-memory weight load then
+// feeds twice the FMAs (the EG = 16 x TT = 4 kernel is shared-memory-bandwidth bound).
+template <int EG, int TT, bool FUSE = false, int NW = kRouter2Warps, int MINB = 1,
+          bool PREFETCH = true>
+__global__ void __launch_bounds__(NW * 32, MINB)
     router_logits2_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
                           const float* __restrict__ bias, int T, int d, int E,
                           float* __restrict__ logits, int k = 0, int32_t* __restrict__ idx = nullptr,
                           float* __restrict__ w = nullptr,
                           int32_t* __restrict__ chunk_counts = nullptr) {
-  static_assert(!FUSE || kRouter2Warps * TT == kChunk, "fused top-k: one chunk per CTA iteration");
+  static_assert(!FUSE || NW * TT == kChunk, "fused top-k: one chunk per CTA iteration");
   __shared__ int hist[FUSE ? EG : 1];
   if (FUSE && threadIdx.x < EG) hist[threadIdx.x] = 0;
   extern __shared__ __align__(16) uint8_t smem_r2[];
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nj = d / 256;
-  const int per_iter = kRouter2Warps * TT;
+  const int per_iter = NW * TT;
   // every warp runs every CTA iteration (the fused histogram synchronises the CTA per chunk)
   for (int base = blockIdx.x * per_iter; base < T; base += gridDim.x * per_iter) {
     const int t0 = base + warp * TT;
@@ -181,7 +185,14 @@ __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
     }
     for (int j = 0; j < nj; ++j) {
       const int ibase = j * 256 + lane * 8;
-      if (j + 1 < nj) {
+      if (!PREFETCH && j > 0) {  // no look-ahead registers: other warps hide the latency
+#pragma unroll
+        for (int a = 0; a < TT; ++a) {
+          const int t = min(t0 + a, T - 1);
+          xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase));
+        }
+      }
+      if (PREFETCH && j + 1 < nj) {
 #pragma unroll
         for (int a = 0; a < TT; ++a) {
           const int t = min(t0 + a, T - 1);
@@ -211,8 +222,10 @@ __global__ void __launch_bounds__(kRouter2Warps * 32, 1)
           }
         }
       }
+      if (PREFETCH) {
 #pragma unroll
-      for (int a = 0; a < TT; ++a) xv[a] = xn[a];
+        for (int a = 0; a < TT; ++a) xv[a] = xn[a];
+      }
     }
 #pragma unroll
     for (int a = 0; a < TT; ++a)

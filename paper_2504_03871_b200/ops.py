@@ -13,6 +13,7 @@ expert FFN -> EXP_F, ``costmodel.py:28-37``); their semantics come from the pape
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from dataclasses import dataclass
 
@@ -121,7 +122,12 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, bias: torch.Tensor | 
     )
     _end(_tk)
     _native.check(rc, "hm_router_topk")
-    _count(3)
+    # launches (mirrors hm_router_topk's dispatch): one expert group -> logits+top-k fused, scan
+    eg = 8 if E == 8 else 16
+    fused = (E % 8 == 0 and E <= 16 and wg.data_ptr() % 16 == 0
+             and d * eg * 4 + (d // 8) * 16 <= 200 * 1024
+             and not os.environ.get("HM_ROUTER_V1") and not os.environ.get("HM_ROUTER_UNFUSED"))
+    _count(0 if T == 0 else (2 if fused else 3))
     return Routing(idx, w, logits, counts, offsets, chunk_base)
 
 
@@ -245,7 +251,7 @@ def grouped_gemm(mode: int, a, b, seg_offsets, E: int, rows: int, M: int, N: int
     )
     _end(_tk)
     _native.check(rc, "hm_grouped_gemm")
-    _count(1)
+    _count(2 if nbytes else 1)  # the weight-gradient modes first build their per-expert TMA views
 
 
 def grouped_ffn_fwd(x_perm, seg_offsets, w_ug, w_d, max_ctas: int = 0):

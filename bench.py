@@ -397,10 +397,15 @@ def cpu_baseline(cfg, tokens: int):
             "sample": f"{tokens} tokens of {cfg.name} (fwd+bwd, fp32 CPU oracle, {dt:.1f}s)"}
 
 
-def stack_single_gpu(shape, layers: int, microbatches: int, dev, seed: int = 7):
-    """The ZP stack's work on ONE GPU with no pipeline (the scaling comparator for N > 1): every
-    micro-batch runs forward and backward through all layers — pre-norm attention block, then
-    the MoE layer through the same native kernels — with gradients accumulated. Returns
+def stack_single_gpu(shape, layers: int, microbatches: int, dev, seed: int = 7,
+                     chunk_tokens: int = 8192):
+    """The ZP stack's work on ONE GPU with no pipeline (the scaling comparator for N > 1): the
+    same tokens (microbatches x tokens_per_mb) and layers — pre-norm attention over the same
+    tokens_per_mb-token sequences, then the MoE layer through the same native kernels — forward
+    and backward, processed in chunks of `chunk_tokens` (8192: the bare layer's throughput there
+    equals the N = 1 bench's at 16384, with half the activation memory) so each chunk's
+    weight gradients are formed once per layer, like the ZP executor's (no per-micro-batch
+    gradient read-modify-write; a chunk's gradients replace the previous chunk's). Returns
     MoE-layer tokens/s (tokens x layers / time), CUDA-event timed, one iteration after warm-up."""
     from paper_2504_03871_b200.executor import attention_block, rms_norm
     from paper_2504_03871_b200.layer import moe_forward
@@ -408,23 +413,30 @@ def stack_single_gpu(shape, layers: int, microbatches: int, dev, seed: int = 7):
     g = torch.Generator(device=dev).manual_seed(seed)
     d, f, E, k, T = shape.d, shape.f, shape.E, shape.k, shape.tokens_per_mb
     heads = shape.heads or max(1, d // 128)
+    total = T * microbatches
+    C = max(T, (min(chunk_tokens, total) // T) * T)  # whole sequences per chunk
 
     def rnd(*sz, std=1.0):
         return (torch.randn(sz, generator=g, device=dev) * std).to(torch.bfloat16).requires_grad_()
 
     P = [dict(wqkv=rnd(d, 3 * d, std=d ** -0.5), wo=rnd(d, d, std=d ** -0.5), wg=rnd(d, E, std=d ** -0.5),
               w_ug=rnd(E, 2 * f, d, std=d ** -0.5), w_d=rnd(E, d, f, std=f ** -0.5)) for _ in range(layers)]
-    x = [torch.randn((T, d), generator=g, device=dev).to(torch.bfloat16) for _ in range(2)]
-    gy = [torch.randn((T, d), generator=g, device=dev).to(torch.bfloat16) for _ in range(2)]
+    x = [torch.randn((C, d), generator=g, device=dev).to(torch.bfloat16) for _ in range(2)]
+    gy = [torch.randn((C, d), generator=g, device=dev).to(torch.bfloat16) for _ in range(2)]
+    nchunks = (total + C - 1) // C
 
     def iteration():
-        for j in range(microbatches):
-            h = x[j & 1]
+        for j in range(nchunks):
+            n = min(C, total - j * C)
             for p in P:
-                u = attention_block(h, p["wqkv"], p["wo"], heads) if shape.attention else h * 1
+                for t in p.values():
+                    t.grad = None
+            h = x[j & 1][:n]
+            for p in P:
+                u = attention_block(h, p["wqkv"], p["wo"], heads, seq=T) if shape.attention else h * 1
                 y, _ = moe_forward(rms_norm(u), p["wg"], p["w_ug"], p["w_d"], k)
                 h = u + y
-            h.backward(gy[j & 1])
+            h.backward(gy[j & 1][:n])
 
     iteration()
     torch.cuda.synchronize(dev)
@@ -435,7 +447,7 @@ def stack_single_gpu(shape, layers: int, microbatches: int, dev, seed: int = 7):
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     del P
-    return T * microbatches * layers / (ms / 1e3), ms
+    return total * layers / (ms / 1e3), ms
 
 
 def run_zp(args, ws, rank, local):
@@ -567,7 +579,9 @@ def run_zp(args, ws, rank, local):
         v1, ms1 = stack_single_gpu(shape, args.layers, M * args.microbatches, dev)
         out["scaling_reference"] = {
             "value": v1, "unit": UNIT, "ms_per_iteration": round(ms1, 3),
-            "workload": "identical stack and token count on ONE GPU, no pipeline (rank 0, after the timed region)",
+            "workload": ("identical stack and token count on ONE GPU, no pipeline, in 8192-token chunks "
+                         "(weight gradients formed once per chunk and layer, as the "
+                         "executor forms them once per layer) — rank 0, after the timed region"),
             "per_gpu_efficiency": value / (ws * v1),
         }
     out["zp"]["simulated_makespan_ms"] = simulate(graph, default_orders(graph)).makespan / 1e6

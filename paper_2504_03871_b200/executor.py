@@ -231,14 +231,17 @@ def rms_norm(x):
     return torch.nn.functional.rms_norm(x, (x.shape[-1],), eps=1e-6)
 
 
-def attention_block(h, wqkv, wo, heads: int):
+def attention_block(h, wqkv, wo, heads: int, seq: int = 0):
     """u = h + Attn(RMSNorm(h)): fused QKV projection, causal SDPA, output projection (torch /
-    cuBLAS / flash attention; not one of the four hot-path kernels). Pre-norm, as in Mixtral."""
+    cuBLAS / flash attention; not one of the four hot-path kernels). Pre-norm, as in Mixtral.
+    The T rows are one causal sequence, or T / seq independent sequences of `seq` tokens."""
     T, d = h.shape
     hd = d // heads
-    qkv = (rms_norm(h) @ wqkv).view(1, T, 3, heads, hd).permute(2, 0, 3, 1, 4)  # [3, 1, H, T, hd]
+    S = seq if seq else T
+    B = T // S
+    qkv = (rms_norm(h) @ wqkv).view(B, S, 3, heads, hd).permute(2, 0, 3, 1, 4)  # [3, B, H, S, hd]
     o = torch.nn.functional.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True)
-    return h + o[0].permute(1, 0, 2).reshape(T, d) @ wo
+    return h + o.permute(0, 2, 1, 3).reshape(T, d) @ wo
 
 
 @dataclass

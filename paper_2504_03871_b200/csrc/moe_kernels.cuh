@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(256)
 //   dx[t]       = sum_s dx_perm[row_of[t,s]] + sum_s dlogit[t,s] * Wg[:, idx[t,s]]
 // wg_t is Wg transposed ([E][d]). Also writes dlogit (for the router weight gradient).
 template <int K>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
     unpermute_router_bwd_kernel(const __nv_bfloat16* __restrict__ dx_perm,
                                 const int32_t* __restrict__ row_of, const int32_t* __restrict__ idx,
                                 const float* __restrict__ w, const float* __restrict__ dw,

@@ -239,3 +239,19 @@ def test_load_balanced_placement():
         ow = expert_owners(E, M, N, o, loads)
         assert [sum(1 for x in ow if x == a) for a in range(M)] == [o * N // M] * M
         assert [sum(1 for x in ow if x == M + i) for i in range(N)] == [E // N - o] * N
+
+
+def test_attention_block_independent_sequences():
+    """attention_block(seq=S) treats the T rows as T/S independent causal sequences: identical to
+    running each S-row block alone (the single-GPU comparator relies on this)."""
+    from paper_2504_03871_b200.executor import attention_block
+
+    g = torch.Generator().manual_seed(0)
+    d, heads, S = 64, 4, 16
+    h = torch.randn(3 * S, d, generator=g)
+    wqkv = torch.randn(d, 3 * d, generator=g) * d ** -0.5
+    wo = torch.randn(d, d, generator=g) * d ** -0.5
+    joint = attention_block(h, wqkv, wo, heads, seq=S)
+    parts = torch.cat([attention_block(h[i * S:(i + 1) * S], wqkv, wo, heads) for i in range(3)])
+    assert torch.allclose(joint, parts, atol=1e-5, rtol=1e-5)
+    assert not torch.allclose(attention_block(h, wqkv, wo, heads), joint, atol=1e-3)

@@ -521,6 +521,10 @@ def run_zp(args, ws, rank, local):
     tl = execute(graph, ex)  # one more iteration, measured per task
     hw = torch.tensor([ex.host_wait_s], device=dev)
     dist.all_reduce(hw, op=dist.ReduceOp.MAX)
+    # peak device memory of the ZP run: per role (attention / expert ranks), max over ranks
+    mem = torch.zeros(2, device=dev)
+    mem[0 if rank < M else 1] = torch.cuda.max_memory_allocated(dev) / 2 ** 30
+    dist.all_reduce(mem, op=dist.ReduceOp.MAX)
     tokens_iter = args.mb_tokens * M * args.microbatches
     value = tokens_iter * args.layers * args.steps / (ms / 1e3)
     if rank != 0:
@@ -616,6 +620,9 @@ def run_zp(args, ws, rank, local):
                    graph.assignment, graph.forward_only)
     out["zp"]["resimulated_makespan_ms"] = simulate(g2, default_orders(g2)).makespan / 1e6
     out["zp"]["host_count_wait_ms_max_rank"] = round(float(hw) * 1e3, 3)
+    out["zp"]["peak_mem_gib"] = {"attention_ranks": round(float(mem[0]), 1),
+                                 "expert_ranks": round(float(mem[1]), 1),
+                                 "rank0_after_scaling_reference": round(torch.cuda.max_memory_allocated(dev) / 2 ** 30, 1)}
     _emit(out)
 
 

@@ -497,7 +497,13 @@ def run_zp(args, ws, rank, local):
         graph = build_distep_graph(spec, dur)
         assignment = graph.assignment
     else:
-        assignment = plan_assignment(spec, dur)
+        if args.offload:
+            # explicit per-layer offload (the reference CLI's explicit plan, cli.py:93-106)
+            from paper_2504_03871_b200 import ExpertAssignment
+
+            assignment = ExpertAssignment(tuple(int(v) for v in args.offload.split(",")))
+        else:
+            assignment = plan_assignment(spec, dur)
         graph = build_zp_graph(spec, dur, assignment, mode="zp-full")
     disp = dist.new_group(list(range(ws)))
     comb = dist.new_group(list(range(ws)))
@@ -705,6 +711,9 @@ def main():
                     help="ZP: zebra-parallel schedule, or the DistEP lockstep ablation")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="ZP: NVLink peer-memory transport fused into the kernels, or NCCL send/recv")
+    ap.add_argument("--offload", default="",
+                    help="ZP: explicit experts offloaded per expert rank, per layer (e.g. 2,2,2,2,2,2,2,2) "
+                         "instead of the Asym-EA plan")
     ap.add_argument("--expert-capacity", type=float, default=1.0,
                     help="ZP: capacity weight of expert ranks (grouped-GEMM grid = ceil(w*SMs))")
     args = ap.parse_args()

@@ -672,12 +672,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&sh.tmem_full[acc], aph);
         tc_fence_after();
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+        // the per-row destination table is only read for rows that exist (row_ok): past the
+        // last received row it has no entries
+        const unsigned long long row_base = (p.out_rows && row_ok) ? p.out_rows[grow] : 0ull;
         auto chunk_dst = [&](int ch, int& nv) -> __nv_bfloat16* {
           const int u = ch >> 3;
           const int n0 = (tc.nt * NSUB + u) * kBN;
           const int c = half * 128 + (ch & 7) * 16;
           nv = min(16, p.N - n0 - c);
-          return p.out_rows ? reinterpret_cast<__nv_bfloat16*>(p.out_rows[grow]) + n0 + c
+          return p.out_rows ? reinterpret_cast<__nv_bfloat16*>(row_base) + n0 + c
                             : p.out + grow * p.ldo + n0 + c;
         };
         auto store16 = [&](__nv_bfloat16* dst, int nv, const uint32_t (&v)[8]) {

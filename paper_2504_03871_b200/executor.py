@@ -457,6 +457,8 @@ class ZpExecutor:
 
     def _exp_f(self, l, j):
         st, be = self.st, self.be
+        if not st.own[l - 1]:  # every expert of this rank is offloaded at this layer
+            return
         seg = self.seg[(l, j)]
         self.seg_t[(l, j)] = seg_t = be.seg_tensor(seg)
         x = self.x_recv[(l, j)][: max(seg[-1], 1)]
@@ -488,6 +490,8 @@ class ZpExecutor:
         one grouped GEMM over all R micro-batches (K concatenation) instead of an fp32
         read-modify-write of every expert gradient per micro-batch."""
         st, be = self.st, self.be
+        if not st.own[l - 1]:
+            return
         seg = self.seg[(l, j)]
         n = max(seg[-1], 1)
         dy = self.dy_recv[(l, j)][:n]
@@ -813,6 +817,8 @@ class ZpP2PExecutor(ZpExecutor):
 
     def _exp_f(self, l, j):
         st, be = self.st, self.be
+        if not st.own[l - 1]:  # every expert of this rank is offloaded at this layer
+            return
         seg = self.seg[(l, j)]
         self.seg_t[(l, j)] = seg_t = be.seg_tensor(seg)
         x = self.x_recv[(l, j)]
@@ -845,6 +851,8 @@ class ZpP2PExecutor(ZpExecutor):
 
     def _exp_b(self, l, j):
         st, be, ar = self.st, self.be, self.arena
+        if not st.own[l - 1]:
+            return
         seg = self.seg[(l, j)]
         if (l, j) not in self.out_rows_dx:
             delta = ar.offset(l, j, "dx") - ar.offset(l, j, "y")

@@ -128,6 +128,7 @@ def _close(a, b, tol=1e-4):
     (2, 2, (1, 0), True),
     (1, 2, (0, 1), False),
     (4, 4, (1, 1), False),  # the 8-GPU layout of BASELINE C4 (2 experts per expert rank)
+    (4, 4, (2, 0), False),  # a layer whose expert ranks keep no expert at all (all offloaded)
     (2, 2, "distep", False),  # DistEP lockstep ablation on the same executor
 ])
 def test_executor_matches_single_process_reference(M, N, offload, attention):

@@ -320,7 +320,7 @@ def test_grouped_ffn_full_c2_sampled_rows():
         xr = x[r].float()
         gate = wg_[e].float() @ xr
         up = wu_[e].float() @ xr
-        hq_g, hq_u = ops.split_gate_up(h[r:r + 1].view(1, 1, 2 * f).float().reshape(1, 2 * f, 1))
+        hq_g, hq_u = ops.split_gate_up(h[r].float().view(1, 2 * f, 1))  # saved gate / up (bf16)
         assert orc.rel_err(hq_g.reshape(-1), gate) < TOL_ACT
         assert orc.rel_err(hq_u.reshape(-1), up) < TOL_ACT
         a_ref = torch.nn.functional.silu(gate) * up

@@ -285,6 +285,13 @@ class ZpExecutor:
         own = [sorted(e for e in range(shape.E) if ow[e] == rank) for ow in owners]
         self.st = RankState(owners=owners, own=own)
         self._init_params(seed)
+        # Initialise both communicators with one collective call by EVERY rank: NCCL requires the
+        # first operation on a group to involve all its ranks, and an exchange can involve only
+        # some (a layer whose experts all moved to the attention ranks leaves the expert ranks
+        # out of that layer's combine) — without this, that first exchange deadlocks.
+        for grp in {id(g_): g_ for g_ in (disp_group, comb_group)}.values():
+            t = backend.tensor((1,), torch.int32).zero_()
+            dist.all_reduce(t, group=grp)
 
     # ------------------------------------------------------------------ setup
     def _issue_order(self):

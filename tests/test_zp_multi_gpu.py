@@ -18,13 +18,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs 2 GPUs")
-@pytest.mark.parametrize("world", [2, 4])
-def test_transports_agree_on_gradients(world):
+@pytest.mark.parametrize("world,offload", [(2, ""), (4, ""), (4, "4,0")],
+                         ids=["2gpu", "4gpu", "4gpu-expert-ranks-empty-at-layer1"])
+def test_transports_agree_on_gradients(world, offload):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29400 + world),
+           "--master-addr", "127.0.0.1", "--master-port", str(29400 + world + (7 if offload else 0)),
            os.path.join(ROOT, "tools", "zp_transport_check.py")]
+    if offload:
+        cmd += ["--offload", offload]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stderr[-3000:]

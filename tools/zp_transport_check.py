@@ -55,9 +55,14 @@ def timed(ex, iters):
 
 
 def main():
+    if os.environ.get("HM_DUMP_AFTER"):  # debugging a hang: dump every thread's stack, then exit
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["HM_DUMP_AFTER"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="C2 shapes (d=4096, f=14336)")
-    ap.add_argument("--offload", type=int, default=-1)
+    ap.add_argument("--offload", default="",
+                    help="experts offloaded per expert rank: one value for every layer, or one per layer")
     ap.add_argument("--iters", type=int, default=3)
     args = ap.parse_args()
     os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
@@ -75,10 +80,14 @@ def main():
         E, k, d, f, T, L, R = 8, 2, 4096, 14336, 2048, 2, 4
     else:
         E, k, d, f, T, L, R = 8, 2, 512, 512, 512, 2, 3
-    off = args.offload if args.offload >= 0 else (1 if E // N > 1 else 0)
+    if args.offload:
+        off = [int(v) for v in args.offload.split(",")]
+        off = off * L if len(off) == 1 else off
+    else:
+        off = [1 if E // N > 1 else 0] * L
     spec = make_zp_spec(M, N, L, R, E, k, T, d, attn_fwd_ns=3000, expert_layer_fwd_ns=4000,
                         single_expert_fwd_ns=3000, dispatch_ns=100, combine_ns=100)
-    graph = build_zp_graph(spec, derive_task_durations(spec), ExpertAssignment(tuple([off] * L)),
+    graph = build_zp_graph(spec, derive_task_durations(spec), ExpertAssignment(tuple(off)),
                            mode="zp-full")
     shape = ZpLayerShape(E, k, d, f, T)
     disp = dist.new_group(list(range(W)))

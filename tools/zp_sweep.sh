@@ -10,7 +10,7 @@ run() {  # n name args...
   local devs=$(seq -s, 0 $((n - 1)))
   CUDA_VISIBLE_DEVICES=$devs timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n \
     --master-addr 127.0.0.1 --master-port $((29600 + RANDOM % 300)) bench.py --gpus $n --steps $STEPS \
-    --warmup 3 "$@" > gpurun_out/sweep/${n}gpu_${name}.json 2> gpurun_out/sweep/${n}gpu_${name}.err
+    --warmup 3 ${EXTRA:-} "$@" > gpurun_out/sweep/${n}gpu_${name}.json 2> gpurun_out/sweep/${n}gpu_${name}.err
   echo "$n $name rc=$?"
 }
 for n in ${NS:-4 2}; do

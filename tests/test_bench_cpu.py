@@ -30,3 +30,23 @@ def test_ncu_traffic_reads_committed_capture():
     # measured DRAM bytes can only exceed the compulsory floor (L2 re-reads), within reason
     assert floor <= tr["bytes"] < 4 * floor
     assert bench.ncu_traffic("C9-none", "grouped_gemm_kernel", 6) is None
+
+
+def test_reference_arm_prints_one_json_line():
+    """`bench.py --impl reference` (the driver's reference arm: the CPU oracle on the host) on a
+    tiny sample prints the contract's JSON line."""
+    import json
+    import subprocess
+
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "bench.py"), "--impl",
+                        "reference", "--config", "C1", "--steps", "1", "--warmup", "0",
+                        "--cpu-tokens", "64"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "impl", "cpu_baseline", "e2e", "config"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"

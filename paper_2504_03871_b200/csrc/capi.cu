@@ -541,7 +541,17 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   const bool tok = dwg && E <= 8 && k <= 3 && d % 64 == 0 && !getenv("HM_ROUTER_WGRAD_PERM");
   float* dl_perm = (dwg && !tok) ? part : nullptr;
   float* dl_tok = dlogit ? dlogit : (tok ? part : nullptr);
-  HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+  // k >= 4: metadata broadcast by shuffles, no row prefetch (C3, k = 6: 0.099 vs 0.121 ms);
+  // k <= 3: the v1 kernel (C2, k = 2: 0.080 vs 0.088 ms). Both produce bit-identical dx / dlogit
+  // (tools/router_bench.py). HM_UNPERMUTE_V1 / HM_UNPERMUTE_V2 force a variant for A/B runs.
+  const bool v1 = getenv("HM_UNPERMUTE_V1") || (k <= 3 && !getenv("HM_UNPERMUTE_V3"));
+  if (getenv("HM_UNPERMUTE_V2")) {
+    HM_K_SWITCH(k, (hm::unpermute_router_bwd2_kernel<K, true><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+  } else if (v1) {
+    HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+  } else {
+    HM_K_SWITCH(k, (hm::unpermute_router_bwd2_kernel<K, false><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+  }
   if (int rc = check_launch("unpermute_router_bwd")) return rc;
   if (tok) {
     float* partials = part + static_cast<size_t>(T) * k;

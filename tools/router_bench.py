@@ -75,6 +75,22 @@ def main():
         res.setdefault(variant, []).append(ms)
         res.setdefault(variant + "_dwg", ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True)[2].float())
     out["router_bwd_ms"] = {v: min(res[v]) for v in ("tok", "perm")}
+    # unpermute + dlogit.Wg kernel variants (HM_UNPERMUTE_V1/V2/V3), dx / dlogit compared bitwise
+    uv = {}
+    for variant in ("v1", "v2", "v3", "v1", "v2", "v3"):
+        for v in ("V1", "V2", "V3"):
+            os.environ.pop("HM_UNPERMUTE_" + v, None)
+        os.environ["HM_UNPERMUTE_" + variant.upper()] = "1"
+        uv.setdefault(variant, []).append(timed(lambda: ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=False), args.reps))
+        uv.setdefault(variant + "_out", ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True))
+    for v in ("V1", "V2", "V3"):
+        os.environ.pop("HM_UNPERMUTE_" + v, None)
+    out["unpermute_router_bwd_ms"] = {v: min(uv[v]) for v in ("v1", "v2", "v3")}
+    for v in ("v2", "v3"):
+        out[f"unpermute_{v}_bitwise_equal"] = all(
+            (a is None and b is None) or bool(torch.equal(a, b)) for a, b in zip(uv["v1_out"], uv[v + "_out"]))
+    ub = T * k * d * 2 + T * d * 2
+    out["unpermute_router_bwd_gbs"] = {v: ub / ms / 1e6 for v, ms in out["unpermute_router_bwd_ms"].items()}
     a, b = res["tok_dwg"], res["perm_dwg"]
     out["dwg_rel_diff_tok_vs_perm"] = float((a - b).norm() / b.norm())
     fwd_bytes = T * d * 2 + d * E * 2 + T * k * 8 + 8 * E

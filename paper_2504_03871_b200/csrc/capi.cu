@@ -226,6 +226,19 @@ int gemm_ctas() {
 
 }  // namespace
 
+// K1b: thread-per-token top-k for E % 4 == 0, E <= 64 (bit-identical to the warp-per-token
+// kernel, which stays for E > 64 and for A/B runs via HM_TOPK_WARP).
+static void launch_router_topk(int nchunk, cudaStream_t st, const float* logits, int T, int E, int k,
+                               int32_t* idx, float* w, int32_t* chunk_base) {
+  if (E % 4 == 0 && E <= 64 && !getenv("HM_TOPK_WARP")) {
+    if (E <= 16) hm::router_topk_lane_kernel<16><<<nchunk, hm::kChunk, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+    else if (E <= 32) hm::router_topk_lane_kernel<32><<<nchunk, hm::kChunk, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+    else hm::router_topk_lane_kernel<64><<<nchunk, hm::kChunk, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+  } else {
+    hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+  }
+}
+
 extern "C" {
 
 int hm_abi_version(void) { return HM_ABI_VERSION; }
@@ -347,7 +360,7 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
       kern<<<dim3(gx, ngroups), nw * 32, smem3, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
                                                        nullptr, nullptr);
       if (int rc = check_launch("router_logits2(8x8)")) return rc;
-      hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+      launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
       if (int rc = check_launch("router_topk")) return rc;
       hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
       return check_launch("router_scan");
@@ -387,7 +400,7 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
                                                            nullptr, nullptr);
       }
       if (int rc = check_launch("router_logits2")) return rc;
-      hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+      launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
       if (int rc = check_launch("router_topk")) return rc;
       hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
       return check_launch("router_scan");
@@ -417,7 +430,7 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
     kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
   }
   if (int rc = check_launch("router_logits")) return rc;
-  hm::router_topk_kernel<<<nchunk, 512, 0, st>>>(logits, T, E, k, idx, w, chunk_base);
+  launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
   if (int rc = check_launch("router_topk")) return rc;
   hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
   return check_launch("router_scan");

@@ -365,6 +365,64 @@ __global__ void __launch_bounds__(1024)
     chunk_counts[static_cast<long>(c) * E + e] = hist[e];
 }
 
+// K1b (v2, E % 4 == 0, E <= EP <= 64): one THREAD per token, one CTA of kChunk threads per
+// chunk. The token's E logits sit in registers (float4 loads); each of the k rounds scans them in
+// ascending expert order with router_topk_kernel's comparator (v > best, or v == best with a
+// lower id; NaN never wins). That comparator is a lexicographic max over the non-NaN values, so
+// the sequential scan selects exactly what the warp butterfly selects, including the all-NaN
+// fallback; softmax and histogram are the same code. No shuffles: C3 (E = 64, k = 6) spent
+// 32 us in the warp-per-token kernel's 60 dependent shuffles per token.
+template <int EP>
+__global__ void __launch_bounds__(kChunk)
+    router_topk_lane_kernel(const float* __restrict__ logits, int T, int E, int k,
+                            int32_t* __restrict__ idx, float* __restrict__ w,
+                            int32_t* __restrict__ chunk_counts /*[nchunk][E]*/) {
+  __shared__ int hist[EP];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int c = blockIdx.x;
+  const int t = c * kChunk + threadIdx.x;
+  if (t < T) {
+    float v[EP];
+#pragma unroll
+    for (int q = 0; q < EP / 4; ++q) {
+      float4 f = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (4 * q < E) f = __ldg(reinterpret_cast<const float4*>(logits + static_cast<long>(t) * E) + q);
+      v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+    }
+    float sel_l[kMaxTopK];
+    int sel_e[kMaxTopK];
+    for (int s = 0; s < k; ++s) {
+      float bv = -INFINITY;
+      int be = 0x7fffffff;
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (e < E && (v[e] > bv || (v[e] == bv && e < be))) { bv = v[e]; be = e; }
+      if (be == 0x7fffffff) {
+        be = 0;
+        for (int p = 0; p < s; ++p)
+          if (sel_e[p] == be) { ++be; p = -1; }
+      }
+      sel_l[s] = bv;
+      sel_e[s] = be;
+#pragma unroll
+      for (int e = 0; e < EP; ++e)
+        if (e == be) v[e] = -INFINITY;
+    }
+    float ex[kMaxTopK];
+    float sum = 0.f;
+    for (int s = 0; s < k; ++s) { ex[s] = expf(sel_l[s] - sel_l[0]); sum += ex[s]; }
+    for (int s = 0; s < k; ++s) {
+      idx[static_cast<long>(t) * k + s] = sel_e[s];
+      w[static_cast<long>(t) * k + s] = ex[s] / sum;
+      atomicAdd(&hist[sel_e[s]], 1);
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    chunk_counts[static_cast<long>(c) * E + e] = hist[e];
+}
+
 // ------------------------------------------------------------------------------------------
 // K1c: counts / offsets / chunk bases. Single CTA of 1024 threads; warp w owns experts
 // w, w+32, ...: (1) per-expert totals with warp reductions over the chunks, (2) exclusive scan

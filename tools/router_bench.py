@@ -63,6 +63,27 @@ def main():
             os.environ.pop("HM_ROUTER_UNFUSED", None)
         fw.setdefault(variant, []).append(timed(lambda: ops.router_topk(x, wg, k), args.reps))
     os.environ.pop("HM_ROUTER_UNFUSED", None)
+    # top-k kernel: thread-per-token (default, E <= 64) vs warp-per-token (HM_TOPK_WARP), on the
+    # unfused path, every routing output compared bitwise (incl. ties and a NaN/-inf row)
+    xt = x.clone()
+    xt[1] = 0  # all-zero logits: every expert ties
+    xt[2] = float("nan")
+    os.environ["HM_ROUTER_UNFUSED"] = "1"
+    rt = {}
+    for variant in ("lane", "warp", "lane", "warp"):
+        if variant == "warp":
+            os.environ["HM_TOPK_WARP"] = "1"
+        else:
+            os.environ.pop("HM_TOPK_WARP", None)
+        fw.setdefault("unfused_topk_" + variant, []).append(timed(lambda: ops.router_topk(x, wg, k), args.reps))
+        rr = ops.router_topk(xt, wg, k)
+        rt[variant] = [rr.idx, rr.w, rr.counts, rr.offsets, rr.chunk_base]
+    os.environ.pop("HM_TOPK_WARP", None)
+    os.environ.pop("HM_ROUTER_UNFUSED", None)
+    bits = [(a.view(torch.int32) if a.dtype == torch.float32 else a) for a in rt["lane"]]
+    bits_w = [(a.view(torch.int32) if a.dtype == torch.float32 else a) for a in rt["warp"]]
+    out["topk_lane_bitwise_equal"] = {n: bool(torch.equal(a, b)) for n, a, b in
+                                      zip(("idx", "w", "counts", "offsets", "chunk_base"), bits, bits_w)}
     out["router_fwd_ms_variants"] = {v: min(t) for v, t in fw.items()}
     out["router_fwd_ms"] = min(fw["fused"])
     res = {}

@@ -527,10 +527,16 @@ int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, co
   return check_launch("combine_bwd");
 }
 
+// the dlogit region of the router-backward workspace, padded to 64 floats so the dWg partials
+// after it stay 16-byte aligned (router_wgrad_perm_kernel stores float4; T*k % 4 != 0 faulted)
+static size_t router_bwd_dl_elems(int T, int k) {
+  return (static_cast<size_t>(T) * k + 63) & ~static_cast<size_t>(63);
+}
+
 size_t hm_router_bwd_part_elems(int T, int d, int E, int k) {
   // dlogit in permuted-row order (T*k) followed by the per-split dWg partials
   const int splits = hm::kWgSplit > hm::kWgTokSplit ? hm::kWgSplit : hm::kWgTokSplit;
-  return static_cast<size_t>(T) * k + static_cast<size_t>(splits) * E * d;
+  return router_bwd_dl_elems(T, k) + static_cast<size_t>(splits) * E * d;
 }
 
 int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
@@ -567,7 +573,7 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   }
   if (int rc = check_launch("unpermute_router_bwd")) return rc;
   if (tok) {
-    float* partials = part + static_cast<size_t>(T) * k;
+    float* partials = part + router_bwd_dl_elems(T, k);
     auto xp = static_cast<const __nv_bfloat16*>(x_perm);
     const dim3 grid(d / 64, hm::kWgTokSplit);
     if (k == 1) hm::router_wgrad_tok_kernel<1><<<grid, 256, 0, st>>>(xp, row_of, idx, dl_tok, T, d, E, partials);
@@ -580,7 +586,7 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
     return check_launch("router_wgrad_reduce");
   }
   if (dwg) {
-    float* partials = part + static_cast<size_t>(T) * k;
+    float* partials = part + router_bwd_dl_elems(T, k);
     dim3 grid(E * hm::kWgSplit, (d + 2047) / 2048);
     hm::router_wgrad_perm_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x_perm),
                                                        dl_perm, offsets, d, E, partials);

@@ -353,3 +353,58 @@ def test_grouped_ffn_full_c2_sampled_rows():
             dcol = da * gq * sg if is_up else da * uq * sg * (1 + gq * (1 - sg))
             ref = dcol @ x[a:b].float()
             assert orc.rel_err(dw_ug[e, j].float(), ref) < TOL_W
+
+
+def _with_env(name, fn):
+    import os
+
+    os.environ[name] = "1"
+    try:
+        return fn()
+    finally:
+        os.environ.pop(name, None)
+
+
+def _bits(t):
+    return t.view(torch.int32) if t.dtype == torch.float32 else t
+
+
+@pytest.mark.parametrize("cfg", [with_tokens(C3, 1000), LayerConfig("E32", E=32, k=4, d=256, f=128, T=333),
+                                 with_tokens(C1, 999)], ids=lambda c: c.name)
+def test_topk_thread_per_token_matches_warp_kernel(cfg):
+    """router_topk_lane_kernel (E <= 64) vs router_topk_kernel (HM_TOPK_WARP): every routing
+    output bitwise equal, including an all-tie row (zero input) and an all-NaN row."""
+    import os
+
+    inp = make_inputs(cfg, seed=7)
+    x = inp.x.cuda().clone()
+    x[1] = 0
+    x[2] = float("nan")
+    wg = inp.wg.cuda()
+    os.environ["HM_ROUTER_UNFUSED"] = "1"
+    try:
+        a = ops.router_topk(x, wg, cfg.k)
+        b = _with_env("HM_TOPK_WARP", lambda: ops.router_topk(x, wg, cfg.k))
+    finally:
+        os.environ.pop("HM_ROUTER_UNFUSED", None)
+    for name in ("idx", "w", "counts", "offsets", "chunk_base"):
+        assert torch.equal(_bits(getattr(a, name)), _bits(getattr(b, name))), name
+
+
+@pytest.mark.parametrize("cfg", [with_tokens(C3, 777), with_tokens(C1, 500)], ids=lambda c: c.name)
+def test_unpermute_router_bwd_variants_bitwise_equal(cfg):
+    """unpermute_router_bwd_kernel (v1) and unpermute_router_bwd2_kernel (v2 prefetch / v3):
+    dx, dlogit and dWg bitwise equal."""
+    inp = make_inputs(cfg, seed=8)
+    x, wg = inp.x.cuda(), inp.wg.cuda()
+    r = ops.router_topk(x, wg, cfg.k)
+    xp, _, row_of = ops.dispatch_permute(x, r)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    dxp = torch.randn(xp.shape, generator=g, device="cuda").to(xp.dtype)
+    dw = torch.randn(r.w.shape, generator=g, device="cuda")
+    wg_t = ops.transpose_bf16(wg)
+    outs = {v: _with_env("HM_UNPERMUTE_" + v, lambda: ops.router_bwd(dxp, row_of, r, dw, xp, wg_t))
+            for v in ("V1", "V2", "V3")}
+    for v in ("V2", "V3"):
+        for a, b in zip(outs["V1"], outs[v]):
+            assert torch.equal(_bits(a), _bits(b)), v

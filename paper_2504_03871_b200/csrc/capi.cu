@@ -448,9 +448,13 @@ int hm_dispatch_permute(const void* x, const int32_t* idx, const int32_t* chunk_
   const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
   auto xb = static_cast<const __nv_bfloat16*>(x);
   auto xp = static_cast<__nv_bfloat16*>(x_perm);
+  const char* split_env = getenv("HM_PERMUTE_SPLIT");
+  // 4 CTAs per 64-token chunk: C2 0.077 -> 0.069 ms (89 % of HBM), C3 0.097 -> 0.094 ms
+  // (tools/permute_bench.py); HM_PERMUTE_SPLIT overrides for A/B runs
+  const int split = split_env ? (atoi(split_env) < 1 ? 1 : (atoi(split_env) > 8 ? 8 : atoi(split_env))) : 4;
 #define HM_PERMUTE_CASE(V)                                                                      \
   case V:                                                                                       \
-    hm::dispatch_permute_kernel<V><<<nchunk, 256, 0, st>>>(xb, idx, chunk_base, T, d, E, k, xp, \
+    hm::dispatch_permute_kernel<V><<<dim3(nchunk, split), 256, 0, st>>>(xb, idx, chunk_base, T, d, E, k, xp, \
                                                             row_src, row_of);                   \
     break;
   if (d % 256 == 0 && d / 256 <= 16) {

@@ -520,14 +520,17 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   assign_rows_ballot(s_idx, s_row, chunk_base + static_cast<long>(c) * E, nt * k, E);
   __syncthreads();
-  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
-    const int r = s_row[i];
-    row_of[static_cast<long>(tbeg) * k + i] = r;
-    row_src[r] = tbeg + i / k;
+  if (blockIdx.y == 0) {
+    for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+      const int r = s_row[i];
+      row_of[static_cast<long>(tbeg) * k + i] = r;
+      row_src[r] = tbeg + i / k;
+    }
   }
-  // row copies
+  // row copies; with gridDim.y = S > 1 the S CTAs of a chunk (each re-deriving the chunk's
+  // rows, a few hundred shared-memory operations) copy every S-th group of 8 tokens
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int tt = warp; tt < nt; tt += 8) {
+  for (int tt = warp + 8 * blockIdx.y; tt < nt; tt += 8 * gridDim.y) {
     const long t = tbeg + tt;
     const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
     uint4 v[VPL];

@@ -615,9 +615,13 @@ int hm_dispatch_permute_p2p(const void* x, const int32_t* idx, const int32_t* ch
   const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
   auto xb = static_cast<const __nv_bfloat16*>(x);
   auto xp = static_cast<__nv_bfloat16*>(x_perm);
+  const char* split_env = getenv("HM_PERMUTE_SPLIT");
+  // default 1 CTA per chunk here: with 4 the ZP stack measured 0.689M / 1.432M tok/s at 2 / 4
+  // GPUs against 0.695M / 1.447M with 1 (within box noise, not a gain); HM_PERMUTE_SPLIT overrides
+  const int split = split_env ? (atoi(split_env) < 1 ? 1 : (atoi(split_env) > 8 ? 8 : atoi(split_env))) : 1;
 #define HM_P2P_CASE(V)                                                                        \
   case V:                                                                                     \
-    hm::dispatch_permute_p2p_kernel<V><<<nchunk, 256, 0, st>>>(xb, idx, chunk_base, offsets, T, d, \
+    hm::dispatch_permute_p2p_kernel<V><<<dim3(nchunk, split), 256, 0, st>>>(xb, idx, chunk_base, offsets, T, d, \
                                                                 E, k, xp, row_src, row_of,    \
                                                                 dest_base, dest_start);       \
     break;

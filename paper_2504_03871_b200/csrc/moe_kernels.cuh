@@ -1027,13 +1027,16 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   assign_rows_ballot(s_idx, s_row, chunk_base + static_cast<long>(c) * E, nt * k, E);
   __syncthreads();
-  for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
-    const int r = s_row[i];
-    row_of[static_cast<long>(tbeg) * k + i] = r;
-    if (row_src) row_src[r] = tbeg + i / k;
+  if (blockIdx.y == 0) {
+    for (int i = threadIdx.x; i < nt * k; i += blockDim.x) {
+      const int r = s_row[i];
+      row_of[static_cast<long>(tbeg) * k + i] = r;
+      if (row_src) row_src[r] = tbeg + i / k;
+    }
   }
+  // gridDim.y CTAs per chunk, as in dispatch_permute_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int tt = warp; tt < nt; tt += 8) {
+  for (int tt = warp + 8 * blockIdx.y; tt < nt; tt += 8 * gridDim.y) {
     const long t = tbeg + tt;
     const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
     uint4 v[VPL];

@@ -24,7 +24,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
+if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    # NCCL's communicator lines (INFO) go to stderr: main() points fd 1 at stderr and writes
+    # the one JSON line to a duplicate of the original stdout
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
@@ -168,6 +171,9 @@ def hbm_bytes(cfg):
         "combine": T * k * d * 2 + T * d * 2 + 8 * T * k,
         "combine_bwd": T * d * 2 + 2 * T * k * d * 2 + 8 * T * k,
         "router_bwd": T * k * d * 2 + T * d * 2 + 4 * T * k + T * d * 2,
+        # fused peer-memory variants (ZP): the routed rows are also written to the owners' slots
+        "dispatch_permute_p2p": T * d * 2 + 2 * T * k * d * 2 + 8 * T * k,
+        "combine_bwd_p2p": T * d * 2 + 2 * T * k * d * 2 + 8 * T * k,
     }
 
 
@@ -264,15 +270,19 @@ def run_ours(args, ws, rank, local):
         roofline["traffic_source"] = tr["source"]
 
     # ---- end-to-end through the public API with host buffers: every step copies its inputs
-    # (x, dY) from pinned host memory and reads its result (the step's per-expert token
-    # histogram) back; the H2D copy of step i+1 runs on a copy stream under step i's compute
-    # (double-buffered device inputs), all inside the timed region.
+    # (x, dY) from pinned host memory and its results (the layer output y and the input gradient
+    # dX) back to pinned host memory. The H2D copy of step i+1 runs on a copy stream under step
+    # i's compute (double-buffered device inputs); the D2H copies of step i run on a second copy
+    # stream under step i+1's compute. Everything is inside the timed region, which ends when the
+    # last D2H copy has landed.
     x_host = x.detach().cpu().pin_memory()
     dy_host = dy.detach().cpu().pin_memory()
-    counts_host = torch.empty((cfg.E,), dtype=torch.int32).pin_memory()
+    y_host = [torch.empty(x_host.shape, dtype=x_host.dtype).pin_memory() for _ in range(2)]
+    dx_host = [torch.empty(x_host.shape, dtype=x_host.dtype).pin_memory() for _ in range(2)]
     x_dev = [torch.empty_like(x.detach()) for _ in range(2)]
     dy_dev = [torch.empty_like(dy) for _ in range(2)]
     copy_stream = torch.cuda.Stream(dev)
+    d2h_stream = torch.cuda.Stream(dev)
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     consumed = [torch.cuda.Event(), torch.cuda.Event()]
 
@@ -295,8 +305,12 @@ def run_ours(args, ws, rank, local):
         y, idx = moe_forward(xin, params[0], params[1], params[2], cfg.k, args.max_ctas)
         y.backward(dy_dev[b])
         consumed[b].record(stream)
-        counts = torch.bincount(idx.reshape(-1), minlength=cfg.E)
-        counts_host.copy_(counts.to(torch.int32), non_blocking=True)
+        d2h_stream.wait_event(consumed[b])
+        with torch.cuda.stream(d2h_stream):
+            y.record_stream(d2h_stream)
+            xin.grad.record_stream(d2h_stream)
+            y_host[b].copy_(y.detach(), non_blocking=True)
+            dx_host[b].copy_(xin.grad, non_blocking=True)
 
     for ev in consumed:
         ev.record(stream)
@@ -307,15 +321,17 @@ def run_ours(args, ws, rank, local):
     e0.record(stream)
     for i in range(1, args.steps + 1):
         e2e_step(i)
+    stream.wait_stream(d2h_stream)  # the last step's results are on the host
     e1.record(stream)
     barrier(ws)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), ws)
     e2e = {"value": tokens_total / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": x_host.numel() * 2 + dy_host.numel() * 2,
-           "d2h_bytes_per_step": cfg.E * 4,
+           "d2h_bytes_per_step": y_host[0].numel() * 2 + dx_host[0].numel() * 2,
            "ms_per_step": round(e2e_ms / args.steps, 3),
-           "note": "pinned H2D of each step's x and dY (prefetched one step ahead on a copy stream) "
-                   "+ D2H of the step's expert histogram, through moe_forward/backward"}
+           "note": "through moe_forward/backward: pinned H2D of each step's x and dY (prefetched one "
+                   "step ahead on a copy stream) and pinned D2H of its y and dX (on a second copy "
+                   "stream, overlapping the next step)"}
 
     out = {
         "metric": METRIC,
@@ -516,14 +532,20 @@ def run_zp(args, ws, rank, local):
     barrier(ws)
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timer = ops.KernelTimer()  # per-kernel device time, on each task's own stream
+    ops.set_timer(timer)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             ex.run()
         ev1.record(stream)
         barrier(ws)
+    ops.set_timer(None)
     ms = max_over_ranks(ev0.elapsed_time(ev1), ws)
     launches = (ops.LAUNCHES[0] - l0) // args.steps
+    tokens_iter = args.mb_tokens * M * args.microbatches
+    roofline, kernels = zp_roofline(timer.summary(), c, args, ws, rank, tokens_iter)
+    e2e = zp_e2e(ex, args, ws, rank, dev, tokens_iter)
     tl = execute(graph, ex)  # one more iteration, measured per task
     hw = torch.tensor([ex.host_wait_s], device=dev)
     dist.all_reduce(hw, op=dist.ReduceOp.MAX)
@@ -531,7 +553,6 @@ def run_zp(args, ws, rank, local):
     mem = torch.zeros(2, device=dev)
     mem[0 if rank < M else 1] = torch.cuda.max_memory_allocated(dev) / 2 ** 30
     dist.all_reduce(mem, op=dist.ReduceOp.MAX)
-    tokens_iter = args.mb_tokens * M * args.microbatches
     value = tokens_iter * args.layers * args.steps / (ms / 1e3)
     if rank != 0:
         return
@@ -577,6 +598,9 @@ def run_zp(args, ws, rank, local):
             "timeline_violations": len(viol),
             "task_durations": task_ms,
         },
+        "roofline": roofline,
+        "kernels": kernels,
+        "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -629,7 +653,93 @@ def run_zp(args, ws, rank, local):
     out["zp"]["peak_mem_gib"] = {"attention_ranks": round(float(mem[0]), 1),
                                  "expert_ranks": round(float(mem[1]), 1),
                                  "rank0_after_scaling_reference": round(torch.cuda.max_memory_allocated(dev) / 2 ** 30, 1)}
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(c, args.cpu_baseline_tokens)
     _emit(out)
+
+
+GEMM_NAMES = ("gemm_fwd_upgate", "gemm_fwd_down", "gemm_fwd_down_p2p", "gemm_bwd_dact", "gemm_bwd_dx",
+              "gemm_bwd_dx_p2p", "gemm_wgrad_ug", "gemm_wgrad_down")
+
+
+def zp_roofline(summ, c, args, ws, rank, tokens_iter):
+    """N > 1: K3 (every rank's grouped-GEMM launches) against the sustained tensor peak, and the
+    attention-side HBM kernels of rank 0. `summ` is this rank's KernelTimer summary over the
+    timed steps (CUDA events on each launch's own stream). Collective: every rank calls it."""
+    peaks = load_peaks()
+    gemm_ms = sum(summ[n][1] for n in GEMM_NAMES if n in summ)
+    t = torch.tensor([gemm_ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)  # sum of K3 device time over all ranks
+    flop = 18.0 * tokens_iter * c.k * c.d * c.f * args.layers * args.steps  # fwd 6 + bwd 12 per row
+    per_gpu = flop / (float(t) / 1e3) / 1e12 if float(t) > 0 else 0.0
+    peak_t = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    roofline = {
+        "kernel": "grouped_gemm_kernel (K3) on every rank: expert ranks' experts and the Asym-EA "
+                  "offloaded experts on attention ranks",
+        "bound": "tensor", "achieved": round(per_gpu, 1), "peak": peak_t, "unit": "TFLOP/s",
+        "frac": round(per_gpu / peak_t, 4),
+        "frac_of_burst_peak": round(per_gpu / peaks["bf16_tflops"], 4),
+        "traffic": None,
+        "achieved_definition": "algorithmic FLOP of all K3 launches of the job (18*tokens*k*d*f per "
+                               "layer) / the sum over ranks of their K3 device time: the per-GPU "
+                               "rate while K3 runs",
+        "peak_source": peaks["source"] + ", sustained bf16",
+        "gemm_ms_per_step_all_ranks": round(float(t) / args.steps, 3),
+    }
+    kernels = {}
+    if rank == 0:
+        from paper_2504_03871_b200.configs import with_tokens
+
+        hb = hbm_bytes(with_tokens(c, args.mb_tokens))
+        for n, (cnt, tot) in summ.items():
+            per = tot / cnt
+            ent = {"launches_per_step": cnt // args.steps, "ms_per_launch": round(per, 4)}
+            if n in hb:
+                ent["gbs"] = round(hb[n] / (per / 1e3) / 1e9, 1)
+                ent["frac_hbm"] = round(ent["gbs"] / peaks["hbm_gbs"], 3)
+            kernels[n] = ent
+        kernels["_note"] = "rank 0 (an attention rank); per-launch device time of each native op"
+    return roofline, kernels
+
+
+def zp_e2e(ex, args, ws, rank, dev, tokens_iter):
+    """N > 1 end to end through the executor: every iteration the attention ranks copy each
+    micro-batch's input and output gradient from pinned host memory into the executor's input
+    buffers (H2D) and read each micro-batch's input gradient back (D2H), all inside the timed
+    region; time = max over ranks. Collective."""
+    ex.keep_input_grads = True
+    hin = {j: t.detach().cpu().pin_memory() for j, t in ex.inputs.items()}
+    hgo = {j: t.detach().cpu().pin_memory() for j, t in ex.out_grads.items()}
+    hdx = {j: torch.empty(t.shape, dtype=t.dtype).pin_memory() for j, t in ex.inputs.items()}
+    stream = torch.cuda.current_stream()
+
+    def iteration():
+        for j in hin:
+            ex.inputs[j].copy_(hin[j], non_blocking=True)
+            ex.out_grads[j].copy_(hgo[j], non_blocking=True)
+        ex.run()
+        for j in hdx:
+            hdx[j].copy_(ex.input_grads[j], non_blocking=True)
+
+    iteration()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        iteration()
+    e1.record(stream)
+    barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    ex.keep_input_grads = False
+    nb = torch.tensor([sum(t.numel() * 2 for t in hin.values()) * 2, sum(t.numel() * 2 for t in hdx.values())],
+                      dtype=torch.int64, device="cuda")
+    dist.all_reduce(nb)  # whole-job bytes per step (attention ranks hold the batches)
+    return {"value": tokens_iter * args.layers * args.steps / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": int(nb[0]), "d2h_bytes_per_step": int(nb[1]),
+            "ms_per_step": round(ms / args.steps, 3),
+            "note": "through ZpExecutor.run(): per iteration, pinned H2D of every micro-batch's input "
+                    "and output gradient and pinned D2H of its input gradient on the attention "
+                    "ranks (bytes summed over ranks)"}
 
 
 def run_reference(args, ws, rank):
@@ -672,6 +782,22 @@ def run_reference(args, ws, rank):
 _OUT = sys.stdout
 
 
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this command under torch.distributed.run
+    with N ranks on this node (one per GPU, rendezvous on 127.0.0.1). Rank 0's JSON line reaches
+    our stdout unchanged; returns the launcher's exit code."""
+    import socket
+    import subprocess
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def _emit(obj) -> None:
     """Print the one JSON result line on the original stdout."""
     _OUT.write(json.dumps(obj) + "\n")
@@ -693,8 +819,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-ctas", type=int, default=0)
-    ap.add_argument("--cpu-tokens", type=int, default=512, help="tokens per --impl reference step")
-    ap.add_argument("--cpu-baseline-tokens", type=int, default=1024)
+    ap.add_argument("--cpu-tokens", type=int, default=2048, help="tokens per --impl reference step")
+    ap.add_argument("--cpu-baseline-tokens", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--layers", type=int, default=8, help="ZP (N>1): MoE transformer layers")
     ap.add_argument("--microbatches", type=int, default=8, help="ZP (N>1): micro-batches R")
@@ -717,6 +843,11 @@ def main():
     ap.add_argument("--expert-capacity", type=float, default=1.0,
                     help="ZP: capacity weight of expert ranks (grouped-GEMM grid = ceil(w*SMs))")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
+    ws_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_setup() if args.impl == "ours" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)

@@ -129,16 +129,37 @@ def route_c(x_bf16: torch.Tensor, wg_bf16: torch.Tensor, k: int, bias=None) -> "
 
 
 def topk_softmax(logits: np.ndarray, k: int):
-    """Top-k with ties -> lower expert id; w = softmax over the selected logits (fp32)."""
+    """Top-k with ties -> lower expert id; w = softmax over the selected logits (fp32).
+
+    Non-finite logits follow one total order, (isnan, -logit, expert id): every number (-inf
+    included) ranks before every NaN, equal numbers and NaNs go to the lower id, and each
+    expert is selected at most once, so the k indices of a row are always distinct (an all-NaN
+    row selects experts 0..k-1 and gets NaN weights; an all -inf row gets NaN weights from
+    exp(-inf - -inf)). numpy's lexsort already sorts NaN last; ``router_ref.c`` states the same
+    comparator explicitly, and the CUDA kernels reach it by marking selected experts NaN."""
     T, E = logits.shape
     order = np.lexsort((np.broadcast_to(np.arange(E), (T, E)), -logits), axis=-1)
     idx = order[:, :k].astype(np.int32)
     sel = np.take_along_axis(logits, idx, axis=1).astype(np.float32)
-    ex = np.exp((sel - sel[:, :1]).astype(np.float32)).astype(np.float32)
-    s = np.zeros((T,), dtype=np.float32)
-    for j in range(k):
-        s = (s + ex[:, j]).astype(np.float32)
-    w = (ex / s[:, None]).astype(np.float32)
+    with np.errstate(invalid="ignore", over="ignore"):
+        ex = np.exp((sel - sel[:, :1]).astype(np.float32)).astype(np.float32)
+        s = np.zeros((T,), dtype=np.float32)
+        for j in range(k):
+            s = (s + ex[:, j]).astype(np.float32)
+        w = (ex / s[:, None]).astype(np.float32)
+    return idx, w
+
+
+def topk_softmax_c(logits: np.ndarray, k: int):
+    """``topk_softmax`` through the C restatement (the numpy version when it is not built)."""
+    lib = _clib()
+    logits = np.ascontiguousarray(logits, dtype=np.float32)
+    if lib is None:
+        return topk_softmax(logits, k)
+    T, E = logits.shape
+    idx = np.empty((T, k), dtype=np.int32)
+    w = np.empty((T, k), dtype=np.float32)
+    lib.hm_ref_topk_softmax(logits.ctypes.data, T, E, k, idx.ctypes.data, w.ctypes.data)
     return idx, w
 
 

@@ -46,7 +46,17 @@ void hm_ref_router_logits(const uint16_t* x, const uint16_t* wg, int T, int d, i
   }
 }
 
-/* top-k (ties -> lower expert id) and softmax over the selected logits */
+/* ranking of the top-k: larger logit first, ties -> lower expert id, NaN after every number
+ * (including -inf), NaN ties -> lower id; a selected expert is never selected again. This is the
+ * total order (isnan, -logit, id) that numpy's lexsort in moe_oracle.topk_softmax also applies. */
+static int ranks_before(float a, int ea, float b, int eb) {
+  const int na = isnan(a), nb = isnan(b);
+  if (na != nb) return nb;           /* a number ranks before NaN */
+  if (!na && a != b) return a > b;   /* both numbers: larger first */
+  return ea < eb;                    /* equal numbers, or both NaN: lower id first */
+}
+
+/* top-k and softmax over the selected logits */
 void hm_ref_topk_softmax(const float* logits, int T, int E, int k, int32_t* idx, float* w) {
 #pragma omp parallel for schedule(static)
   for (int t = 0; t < T; ++t) {
@@ -58,7 +68,7 @@ void hm_ref_topk_softmax(const float* logits, int T, int E, int k, int32_t* idx,
         int used = 0;
         for (int p = 0; p < s; ++p) used |= (sel[p] == e);
         if (used) continue;
-        if (best < 0 || l[e] > l[best]) best = e;
+        if (best < 0 || ranks_before(l[e], e, l[best], best)) best = e;
       }
       sel[s] = best;
     }

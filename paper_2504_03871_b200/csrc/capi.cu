@@ -47,6 +47,22 @@ int check_launch(const char* what) {
   return 0;
 }
 
+// HM_PERMUTE_SPLIT (CTAs per 64-token permute chunk, 1..8), parsed once; 0 = not set. A value
+// that is not an integer in range is reported on stderr once and ignored.
+int permute_split_override() {
+  static int v = -1;
+  if (v < 0) {
+    v = 0;
+    if (const char* s = getenv("HM_PERMUTE_SPLIT")) {
+      char* end = nullptr;
+      const long n = strtol(s, &end, 10);
+      if (end != s && *end == '\0' && n >= 1 && n <= 8) v = static_cast<int>(n);
+      else fprintf(stderr, "hetermoe: ignoring HM_PERMUTE_SPLIT=%s (want 1..8)\n", s);
+    }
+  }
+  return v;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -448,10 +464,9 @@ int hm_dispatch_permute(const void* x, const int32_t* idx, const int32_t* chunk_
   const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
   auto xb = static_cast<const __nv_bfloat16*>(x);
   auto xp = static_cast<__nv_bfloat16*>(x_perm);
-  const char* split_env = getenv("HM_PERMUTE_SPLIT");
   // 4 CTAs per 64-token chunk: C2 0.077 -> 0.069 ms (89 % of HBM), C3 0.097 -> 0.094 ms
   // (tools/permute_bench.py); HM_PERMUTE_SPLIT overrides for A/B runs
-  const int split = split_env ? (atoi(split_env) < 1 ? 1 : (atoi(split_env) > 8 ? 8 : atoi(split_env))) : 4;
+  const int split = permute_split_override() ? permute_split_override() : 4;
 #define HM_PERMUTE_CASE(V)                                                                      \
   case V:                                                                                       \
     hm::dispatch_permute_kernel<V><<<dim3(nchunk, split), 256, 0, st>>>(xb, idx, chunk_base, T, d, E, k, xp, \
@@ -615,10 +630,9 @@ int hm_dispatch_permute_p2p(const void* x, const int32_t* idx, const int32_t* ch
   const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
   auto xb = static_cast<const __nv_bfloat16*>(x);
   auto xp = static_cast<__nv_bfloat16*>(x_perm);
-  const char* split_env = getenv("HM_PERMUTE_SPLIT");
   // default 1 CTA per chunk here: with 4 the ZP stack measured 0.689M / 1.432M tok/s at 2 / 4
   // GPUs against 0.695M / 1.447M with 1 (within box noise, not a gain); HM_PERMUTE_SPLIT overrides
-  const int split = split_env ? (atoi(split_env) < 1 ? 1 : (atoi(split_env) > 8 ? 8 : atoi(split_env))) : 1;
+  const int split = permute_split_override() ? permute_split_override() : 1;
 #define HM_P2P_CASE(V)                                                                        \
   case V:                                                                                     \
     hm::dispatch_permute_p2p_kernel<V><<<dim3(nchunk, split), 256, 0, st>>>(xb, idx, chunk_base, offsets, T, d, \

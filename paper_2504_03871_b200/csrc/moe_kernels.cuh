@@ -22,6 +22,13 @@ constexpr int kChunk = 64;          // tokens per dispatch chunk (one permute CT
 constexpr int kMaxTopK = 8;
 constexpr int kRouterWarps = 8;
 
+// Top-k marks an already-selected expert with NaN: the comparator (v > best, or v == best with a
+// lower id) never picks a NaN, so a selected expert cannot be chosen again even when the row's
+// remaining logits are all -inf (a -inf mark would tie with the -inf start value and win on its
+// lower id). When every unselected logit is NaN the fallback takes the lowest UNSELECTED id.
+// Net rule (oracle/router_ref.c, moe_oracle.topk_softmax): rank by (isnan, -logit, expert id).
+#define kSelectedMark __int_as_float(0x7fc00000)
+
 // ------------------------------------------------------------------------------------------
 // K1a: router logits. grid = (token blocks, expert groups). EG experts per group staged in
 // shared memory as [d][EG] bf16. Each warp handles TT tokens at a time.
@@ -267,8 +274,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 #pragma unroll
           for (int e = 0; e < EG; ++e)
             if (v[e] > bv || (v[e] == bv && e < be)) { bv = v[e]; be = e; }
-          if (be == 0x7fffffff) {
+          if (be == 0x7fffffff) {  // every unselected logit is NaN: lowest unselected id
             be = 0;
+            bv = kSelectedMark;
             for (int q2 = 0; q2 < s2; ++q2)
               if (sel_e[q2] == be) { ++be; q2 = -1; }
           }
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
           sel_e[s2] = be;
 #pragma unroll
           for (int e = 0; e < EG; ++e)
-            if (e == be) v[e] = -INFINITY;
+            if (e == be) v[e] = kSelectedMark;
         }
         float ex[kMaxTopK];
         float sum = 0.f;
@@ -339,6 +347,7 @@ __global__ void __launch_bounds__(1024)
       if (be == 0x7fffffff) {
         // every remaining logit is NaN: take the lowest unselected expert so indices stay valid
         be = 0;
+        bv = kSelectedMark;  // the selected logit is NaN (the softmax sees it)
         for (int p = 0; p < s; ++p)
           if (sel_e[p] == be) { ++be; p = -1; }
       }
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(1024)
       sel_e[s] = be;
 #pragma unroll
       for (int q = 0; q < kPer; ++q)
-        if (q * 32 + lane == be) v[q] = -INFINITY;
+        if (q * 32 + lane == be) v[q] = kSelectedMark;
     }
     if (lane == 0) {
       // softmax over the k selected logits (sel_l[0] is the max)
@@ -400,6 +409,7 @@ __global__ void __launch_bounds__(kChunk)
         if (e < E && (v[e] > bv || (v[e] == bv && e < be))) { bv = v[e]; be = e; }
       if (be == 0x7fffffff) {
         be = 0;
+        bv = kSelectedMark;  // the selected logit is NaN (the softmax sees it)
         for (int p = 0; p < s; ++p)
           if (sel_e[p] == be) { ++be; p = -1; }
       }
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(kChunk)
       sel_e[s] = be;
 #pragma unroll
       for (int e = 0; e < EP; ++e)
-        if (e == be) v[e] = -INFINITY;
+        if (e == be) v[e] = kSelectedMark;
     }
     float ex[kMaxTopK];
     float sum = 0.f;

@@ -284,6 +284,9 @@ class ZpExecutor:
         owners = [expert_owners(shape.E, M, N, o, expert_loads) for o in graph.assignment.offload]
         own = [sorted(e for e in range(shape.E) if ow[e] == rank) for ow in owners]
         self.st = RankState(owners=owners, own=own)
+        self.wg_t = {}
+        self.keep_input_grads = False  # keep dL/d(input) of every micro-batch (input_grads[j])
+        self.input_grads = {}
         self._init_params(seed)
         # Initialise both communicators with one collective call by EVERY rank: NCCL requires the
         # first operation on a group to involve all its ranks, and an exchange can involve only
@@ -528,10 +531,11 @@ class ZpExecutor:
         st, be = self.st, self.be
         r = self.route[(l, j)]
         u, z = self.u[(l, j)], self.z[(l, j)]
-        if l not in self.wg_t:
-            self.wg_t[l] = be.transpose(st.wg[l])
+        key = (st.wg[l]._version, st.wg[l].data_ptr())  # Wg^T kept across iterations until Wg changes
+        if self.wg_t.get(l, (None,))[0] != key:
+            self.wg_t[l] = (key, be.transpose(st.wg[l]))
         dz, dwg = be.router_bwd(self.dx_perm[(l, j)], self.row_of[(l, j)], r, self.dw[(l, j)],
-                                self.x_perm[(l, j)], self.wg_t[l])
+                                self.x_perm[(l, j)], self.wg_t[l][1])
         st.gwg[l] += dwg.float()
         h = self.h_in[(l, j)]
         with torch.enable_grad():
@@ -541,6 +545,8 @@ class ZpExecutor:
         if l > 1:
             self.dh_next[(l - 1, j)] = dh
             self._attn_combine_bwd(l - 1, j, dh)
+        elif self.keep_input_grads:  # the iteration's result for a caller that reads it back
+            self.input_grads[j] = dh
         # free the layer's activations early
         self.u.pop((l, j), None)
         self.z.pop((l, j), None)
@@ -646,7 +652,6 @@ class ZpExecutor:
                      "recv_pos", "seg", "seg_t", "x_recv", "y_recv", "h_save", "act", "y_perm",
                      "dy_perm", "dw", "dh_next", "dy_recv", "dx_recv", "dx_perm", "dh"):
             setattr(self, name, {})
-        self.wg_t = {}
         self.host_wait_s = 0.0
         for gdict in (self.st.gw_ug, self.st.gw_d, self.st.gwg):
             for t in gdict.values():
@@ -803,6 +808,11 @@ class ZpP2PExecutor(ZpExecutor):
         pos_by = {o: self._recv_layout(l, counts_all, o)[1] for o in self.owner_sets[l - 1]}
         seg, pos = self._recv_layout(l, counts_all)
         self.seg[(l, j)], self.recv_pos[(l, j)] = seg, pos
+        for o, pos_o in pos_by.items():  # the peer stores must stay inside each owner's slot
+            need = sum(c for _, c in pos_o.values())
+            if need > ar.cap:
+                raise RuntimeError(f"layer {l} micro-batch {j}: owner rank {o} would receive {need} rows, "
+                                   f"more than its receive slot holds ({ar.cap})")
         if self.is_attn:
             dest_rank, dest_start = p2p_dispatch_dest(owners, pos_by, self.rank, s.E)
             self.dest_start[(l, j)] = st_t = be.h2d(dest_start, torch.int32)
@@ -892,21 +902,35 @@ class ZpP2PExecutor(ZpExecutor):
         return super().run()
 
 
-def merge_rank_intervals(graph: TaskGraph, per_rank: list, M: int) -> Timeline:
+def merge_rank_intervals(graph: TaskGraph, per_rank: list, M: int) -> MeasuredTimeline:
     """Timeline of the representative devices (the reference's one-device-per-role model,
-    ``taskgraph.py:6-7``): a task's interval on its home role spans the earliest start and the
-    latest end over that role's ranks."""
+    ``taskgraph.py:6-7``). Each role is represented by ONE rank — its critical rank, the one whose
+    last task ends latest — so every lane of the Timeline holds one real stream's intervals and
+    never overlaps itself (an envelope over several ranks' intervals would, and would push
+    ``compute_metrics``' utilisation above 1 for M > 1). A task the representative did not take
+    part in takes its interval from the role's other ranks, or from any rank that ran it (e.g. a
+    communication task whose home role had nothing to send). The makespan is the latest end on
+    any rank."""
+    W = len(per_rank)
+    roles = {"attn": list(range(0, M)), "exp": list(range(M, W))}
+
+    def last_end(r):
+        return max((b for _, b in per_rank[r].values()), default=-1)
+
+    rep = {role: max(rs, key=lambda r: (last_end(r), -r)) for role, rs in roles.items() if rs}
     starts, ends = {}, {}
     for t in graph.tasks:
-        ranks = range(0, M) if t.device == "attn" else range(M, len(per_rank))
-        iv = [per_rank[r][t.id] for r in ranks if t.id in per_rank[r]]
-        if not iv:  # e.g. a comm task whose home role had nothing to send
-            iv = [per_rank[r][t.id] for r in range(len(per_rank)) if t.id in per_rank[r]]
-        starts[t.id] = min(a for a, _ in iv)
-        ends[t.id] = max(b for _, b in iv)
+        home = roles[t.device]
+        cands = ([rep[t.device]] if t.device in rep else []) + [r for r in home if r != rep.get(t.device)]
+        cands += [r for r in range(W) if r not in home]
+        r = next((r for r in cands if t.id in per_rank[r]), None)
+        if r is None:
+            raise KeyError(f"task {t.id} ({t.kind.value}) ran on no rank")
+        starts[t.id], ends[t.id] = per_rank[r][t.id]
     orders = default_orders(graph)
-    return MeasuredTimeline(starts, ends, max(ends.values(), default=0),
-                            {k: list(v) for k, v in orders.items()}, per_rank=list(per_rank))
+    makespan = max((b for iv in per_rank for _, b in iv.values()), default=0)
+    return MeasuredTimeline(starts, ends, makespan, {k: list(v) for k, v in orders.items()},
+                            per_rank=list(per_rank), representative_ranks=rep)
 
 
 def execute(graph: TaskGraph, executor: ZpExecutor, world_group=None) -> MeasuredTimeline:

@@ -8,14 +8,32 @@ when attention and experts share one device: no all-to-all, one expert group of 
 
 from __future__ import annotations
 
+import weakref
+
 import torch
 
 from . import ops
+
+# Wg^T ([E, d], the router backward's layout) per router weight tensor, rebuilt only when the
+# weight changes (its version counter moves on every in-place update, e.g. an optimizer step)
+_WG_T: "weakref.WeakKeyDictionary[torch.Tensor, tuple]" = weakref.WeakKeyDictionary()
+
+
+def router_weight_t(wg: torch.Tensor) -> torch.Tensor:
+    ent = _WG_T.get(wg)
+    key = (wg._version, wg.data_ptr())
+    if ent is None or ent[0] != key:
+        ent = (key, ops.transpose_bf16(wg.detach()))
+        _WG_T[wg] = ent
+    return ent[1]
 
 
 class _MoEFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, wg, w_ug, w_down, k, max_ctas):
+        # idx is an output without a gradient: do not let autograd materialise a zero int32
+        # gradient for it (an eager fill kernel per backward)
+        ctx.set_materialize_grads(False)
         r = ops.router_topk(x, wg, k)
         x_perm, row_src, row_of = ops.dispatch_permute(x, r)
         y_perm, h, act = ops.grouped_ffn_fwd(x_perm, r.offsets, w_ug, w_down, max_ctas)
@@ -23,6 +41,7 @@ class _MoEFunction(torch.autograd.Function):
         ctx.save_for_backward(x, wg, w_ug, w_down, x_perm, row_of, y_perm, h, act)
         ctx.routing = r
         ctx.max_ctas = max_ctas
+        ctx.wg_obj = wg  # the caller's router weight object: key of the cached Wg^T
         ctx.mark_non_differentiable(r.idx)
         return y, r.idx
 
@@ -30,12 +49,14 @@ class _MoEFunction(torch.autograd.Function):
     def backward(ctx, dy, _didx):
         x, wg, w_ug, w_down, x_perm, row_of, y_perm, h, act = ctx.saved_tensors
         r = ctx.routing
+        if dy is None:  # y did not reach the loss
+            return None, None, None, None, None, None
         dy = dy.contiguous()
         dy_perm, dw = ops.combine_bwd(dy, y_perm, row_of, r.w)
         dx_perm, dw_ug, dw_down = ops.grouped_ffn_bwd(
             dy_perm, x_perm, h, act, r.offsets, w_ug, w_down, ctx.max_ctas
         )
-        wg_t = ops.transpose_bf16(wg)
+        wg_t = router_weight_t(ctx.wg_obj)
         dx, _dlogit, dwg = ops.router_bwd(dx_perm, row_of, r, dw, x_perm, wg_t, want_dwg=True)
         return dx, dwg, dw_ug, dw_down, None, None
 

@@ -50,3 +50,31 @@ def test_reference_arm_prints_one_json_line():
         assert key in d, key
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "port"
+
+
+def test_gpus_flag_relaunches_under_torchrun():
+    """`bench.py --gpus 2` without WORLD_SIZE re-executes itself under torch.distributed.run with
+    two ranks (the driver may call it either way); rank 0 alone prints one line with n_gpus 2.
+    Exercised through the reference arm, which needs no GPU."""
+    import json
+    import subprocess
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "bench.py"), "--impl",
+                        "reference", "--gpus", "2", "--config", "C1", "--steps", "1", "--warmup", "0",
+                        "--cpu-tokens", "64"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+
+
+def test_world_size_must_match_gpus():
+    import subprocess
+
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "bench.py"), "--impl",
+                        "reference", "--gpus", "4", "--config", "C1", "--steps", "1"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr

@@ -256,3 +256,34 @@ def test_attention_block_independent_sequences():
     parts = torch.cat([attention_block(h[i * S:(i + 1) * S], wqkv, wo, heads) for i in range(3)])
     assert torch.allclose(joint, parts, atol=1e-5, rtol=1e-5)
     assert not torch.allclose(attention_block(h, wqkv, wo, heads), joint, atol=1e-3)
+
+
+def test_merged_timeline_uses_one_rank_per_role():
+    """M > 1: two attention ranks whose compute intervals interleave. The merged Timeline carries
+    one (critical) rank per role, so no lane overlaps itself, utilisation stays <= 1 and
+    validate_measured_timeline accepts it; an envelope over both ranks would overlap."""
+    from paper_2504_03871_b200 import compute_metrics
+    from paper_2504_03871_b200.executor import merge_rank_intervals
+
+    M, N = 2, 2
+    g = _build(M, N, 2, 2, 4, 2, 16, 256, 128, [0, 0])
+    per_rank = []
+    for r in range(M + N):
+        iv, clock = {}, 0
+        for t in g.tasks:  # a per-rank serial walk in id order (valid on every stream)
+            if (t.device == "attn") == (r < M) or t.lane[1] != "compute":
+                a = clock + (5 if r % 2 else 0)  # rank-dependent skew: envelopes would overlap
+                b = a + 10 + 3 * r
+                iv[t.id] = (a, b)
+                clock = b + 1
+        per_rank.append(iv)
+    tl = merge_rank_intervals(g, per_rank, M)
+    assert set(tl.representative_ranks) == {"attn", "exp"}
+    assert tl.representative_ranks["attn"] < M <= tl.representative_ranks["exp"]
+    met = compute_metrics(g, tl)
+    for dev in ("attn", "exp"):
+        assert met.devices[dev].utilization_of_makespan <= 1
+        assert met.devices[dev].utilization <= 1
+    spans = sorted((tl.starts[t.id], tl.ends[t.id]) for t in g.tasks if t.device == "attn" and t.lane[1] == "compute")
+    assert all(b[0] >= a[1] for a, b in zip(spans, spans[1:]))
+    assert tl.makespan == max(b for iv in per_rank for _, b in iv.values())

@@ -116,3 +116,62 @@ def test_c_restatement_matches_numpy_oracle():
         for f in ("idx", "counts", "offsets", "row_src", "row_of"):
             assert np.array_equal(getattr(a, f), getattr(b, f)), f
         assert np.abs(a.w - b.w).max() < 1e-6
+
+
+def _adversarial_logits(E: int, seed: int = 0) -> np.ndarray:
+    """Rows that stress the top-k ordering: all ties, all NaN, a single number among NaNs,
+    -inf / +inf mixes, NaN next to -inf, and ordinary rows with planted ties."""
+    rng = np.random.default_rng(seed)
+    nan, inf = np.float32("nan"), np.float32("inf")
+    rows = [np.zeros(E), np.full(E, nan), np.full(E, -inf), np.full(E, inf)]
+    r = np.full(E, nan); r[E // 2] = 1.0; rows.append(r)
+    r = np.full(E, -inf); r[E - 1] = 0.5; rows.append(r)
+    r = np.full(E, nan); r[1::3] = -inf; rows.append(r)
+    r = rng.standard_normal(E); r[::2] = inf; rows.append(r)
+    r = rng.standard_normal(E); r[0] = nan; r[E - 1] = -inf; rows.append(r)
+    r = np.round(rng.standard_normal(E) * 2) / 2; rows.append(r)  # many exact ties
+    rows += [rng.standard_normal(E) for _ in range(6)]
+    return np.asarray(rows, dtype=np.float32)
+
+
+def _kernel_topk_emulation(logits: np.ndarray, k: int):
+    """Pure-Python restatement of the CUDA top-k loop (moe_kernels.cuh router_topk_lane_kernel):
+    scan with `v > best or (v == best and e < best_e)` from best = -inf, mark the winner NaN,
+    fall back to the lowest unselected id when nothing but NaN is left."""
+    T, E = logits.shape
+    idx = np.zeros((T, k), dtype=np.int32)
+    for t in range(T):
+        v = [np.float32(x) for x in logits[t]]
+        sel = []
+        for _ in range(k):
+            bv, be = np.float32(-np.inf), None
+            for e in range(E):
+                if v[e] > bv or (v[e] == bv and (be is None or e < be)):
+                    bv, be = v[e], e
+            if be is None:
+                be = min(set(range(E)) - set(sel))
+            sel.append(be)
+            v[be] = np.float32("nan")
+        idx[t] = sel
+    return idx
+
+
+def test_topk_non_finite_rows_total_order():
+    for E, k in ((8, 2), (8, 8), (16, 4), (64, 6), (5, 3)):
+        lg = _adversarial_logits(E, seed=E)
+        idx_np, w_np = orc.topk_softmax(lg, k)
+        idx_c, w_c = orc.topk_softmax_c(lg, k)
+        idx_k = _kernel_topk_emulation(lg, k)
+        assert np.array_equal(idx_np, idx_c), (E, k)
+        assert np.array_equal(idx_np, idx_k), (E, k)
+        np.testing.assert_allclose(w_np, w_c, rtol=0, atol=1e-6)  # NaN positions equal too
+        for row in idx_np:
+            assert len(set(row.tolist())) == k  # distinct experts, always
+    # the cases of the round-1 review: a single number among NaNs and a -inf-biased row
+    nan, inf = np.float32("nan"), np.float32("inf")
+    idx, w = orc.topk_softmax(np.array([[1.0, nan, nan, nan]], dtype=np.float32), 2)
+    assert idx.tolist() == [[0, 1]] and np.isnan(w).all()
+    idx, w = orc.topk_softmax(np.array([[-inf, 3.0, -inf, -inf]], dtype=np.float32), 3)
+    assert idx.tolist() == [[1, 0, 2]] and w.tolist() == [[1.0, 0.0, 0.0]]
+    idx, _ = orc.topk_softmax(np.full((1, 8), nan, dtype=np.float32), 2)
+    assert idx.tolist() == [[0, 1]]

@@ -1,0 +1,147 @@
+"""GPU parity against the CPU oracle at the BASELINE layer shapes and on adversarial routing rows
+(run on a B200). Complements test_kernels_gpu.py.
+
+Bars, written here as in the sibling file: routing indices, counts, offsets, row
+maps and permuted rows BIT-EXACT; gate weights within 1e-5 abs (NaN where the oracle has NaN);
+layer output and dX within relative Frobenius error 1e-2 of the fp32 oracle fed the same bf16
+inputs; weight gradients within 2e-2.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as orc
+from paper_2504_03871_b200 import ops
+from paper_2504_03871_b200.configs import C2, C3, LayerConfig, make_inputs, with_tokens
+
+pytestmark = pytest.mark.gpu
+
+TOL_ACT = 1e-2
+TOL_W = 2e-2
+TOL_GATE = 1e-5
+
+
+def _same_float(a: np.ndarray, b: np.ndarray) -> bool:
+    """Bitwise equal where finite or infinite; NaN where the other is NaN (payloads may differ)."""
+    na, nb = np.isnan(a), np.isnan(b)
+    if not np.array_equal(na, nb):
+        return False
+    return np.array_equal(a[~na].view(np.uint32), b[~nb].view(np.uint32))
+
+
+# one config per top-k kernel: fused logits+top-k (E=8, E=16), thread-per-token (E=64, C3 shape),
+# warp-per-token (E=256); T not a multiple of the 64-token chunk
+ADV_CASES = [
+    LayerConfig("E8k2", E=8, k=2, d=4096, f=128, T=203),
+    LayerConfig("E16k4", E=16, k=4, d=512, f=128, T=130),
+    LayerConfig("E64k6", E=64, k=6, d=2048, f=128, T=257),
+    LayerConfig("E256k8", E=256, k=8, d=256, f=128, T=99),
+    LayerConfig("E8k8", E=8, k=8, d=256, f=128, T=65),
+]
+
+
+def _adversarial_x(x: torch.Tensor) -> torch.Tensor:
+    x = x.clone()
+    x[1] = 0  # all logits 0 (+ bias): an all-tie row
+    x[2] = float("nan")  # all-NaN row
+    x[3] = 0
+    x[3, 5] = float("inf")  # +inf / -inf logits by the sign of Wg[5, e]
+    x[4, 7] = float("nan")  # NaN in one element -> all-NaN logits too
+    x[5] = 0
+    x[5, 0] = float("-inf")
+    x[-1] = 0  # last (ragged) chunk gets a tie row
+    return x
+
+
+def _bias_variants(E):
+    nan_free = np.zeros(E, dtype=np.float32)
+    half_ninf = np.zeros(E, dtype=np.float32)
+    half_ninf[1::2] = -np.inf  # more -inf experts than k -> -inf ties must still pick distinct ids
+    one_left = np.full(E, -np.inf, dtype=np.float32)
+    one_left[E - 1] = 0.0  # only the last expert finite
+    return {"none": None, "zero": nan_free, "half_-inf": half_ninf, "one_finite": one_left}
+
+
+@pytest.mark.parametrize("bias_name", ["none", "zero", "half_-inf", "one_finite"])
+@pytest.mark.parametrize("cfg", ADV_CASES, ids=lambda c: c.name)
+def test_router_nonfinite_and_tie_rows_vs_oracle(cfg, bias_name):
+    inp = make_inputs(cfg, seed=13)
+    x = _adversarial_x(inp.x)
+    bias = _bias_variants(cfg.E)[bias_name]
+    ref = orc.route(x.float().numpy(), inp.wg.float().numpy(), cfg.k, bias=bias)
+    xc = x.cuda()
+    r = ops.router_topk(xc, inp.wg.cuda(), cfg.k, None if bias is None else torch.from_numpy(bias).cuda())
+    x_perm, row_src, row_of = ops.dispatch_permute(xc, r)
+    torch.cuda.synchronize()
+    assert _same_float(r.logits.cpu().numpy(), ref.logits), "logits"
+    idx = r.idx.cpu().numpy()
+    assert np.array_equal(idx, ref.idx), np.nonzero((idx != ref.idx).any(1))
+    for row in idx:
+        assert len(set(row.tolist())) == cfg.k  # never the same expert twice
+    np.testing.assert_allclose(r.w.cpu().numpy(), ref.w, rtol=0, atol=TOL_GATE)  # NaN == NaN
+    assert np.array_equal(r.counts.cpu().numpy(), ref.counts)
+    assert np.array_equal(r.offsets.cpu().numpy(), ref.offsets)
+    assert int(r.offsets[-1]) == cfg.T * cfg.k
+    assert np.array_equal(row_src.cpu().numpy(), ref.row_src)
+    assert np.array_equal(row_of.cpu().numpy(), ref.row_of)
+    got = x_perm.cpu().view(torch.int16)
+    want = x[torch.from_numpy(ref.row_src.astype(np.int64))].view(torch.int16)
+    assert torch.equal(got, want)  # bitwise, NaN/inf rows included
+
+
+def _layer_vs_oracle(cfg, seed, expert_bias=None, check_empty=None):
+    from paper_2504_03871_b200.layer import moe_forward
+
+    inp = make_inputs(cfg, seed=seed, expert_bias=expert_bias)
+    w_ug = ops.interleave_gate_up(inp.w_gate, inp.w_up)
+    x = inp.x.cuda().requires_grad_()
+    wg = inp.wg.cuda().requires_grad_()
+    wug = w_ug.cuda().requires_grad_()
+    wd = inp.w_down.cuda().requires_grad_()
+    y, idx = moe_forward(x, wg, wug, wd, cfg.k)
+    y.backward(inp.dy.cuda())
+    torch.cuda.synchronize()
+    got = {"y": y.cpu(), "dx": x.grad.cpu(), "dwg": wg.grad.cpu(), "dw_down": wd.grad.cpu()}
+    got["dw_gate"], got["dw_up"] = ops.split_gate_up(wug.grad.cpu())
+    idx = idx.cpu().numpy()
+    del x, wg, wug, wd, y
+    torch.cuda.empty_cache()
+    ref = orc.moe_layer(inp.x, inp.wg, w_ug, inp.w_down, cfg.k, dy=inp.dy)
+    assert np.array_equal(idx, ref["routing"].idx)
+    errs = {
+        "y": orc.rel_err(got["y"], ref["y"]),
+        "dx": orc.rel_err(got["dx"], ref["dx"]),
+        "dwg": orc.rel_err(got["dwg"], ref["dwg"]),
+        "dw_gate": orc.rel_err(got["dw_gate"], ref["dw_gate"]),
+        "dw_up": orc.rel_err(got["dw_up"], ref["dw_up"]),
+        "dw_down": orc.rel_err(got["dw_down"], ref["dw_down"]),
+    }
+    tol = {"y": TOL_ACT, "dx": TOL_ACT}
+    bad = {k: v for k, v in errs.items() if not v < tol.get(k, TOL_W)}
+    assert not bad, (bad, errs)
+    if check_empty is not None:
+        counts = ref["routing"].counts
+        assert counts[check_empty] == 0
+        assert torch.count_nonzero(got["dw_gate"][check_empty]) == 0
+        assert torch.count_nonzero(got["dw_down"][check_empty]) == 0
+    return errs
+
+
+def test_moe_layer_c3_shape_vs_oracle():
+    """C3 (E=64, top-6, d=2048, f=1408: partial N tiles in the wide GEMMs, 64 ragged experts)."""
+    _layer_vs_oracle(with_tokens(C3, 2048), seed=31)
+
+
+def test_moe_layer_c2_shape_vs_oracle():
+    """C2 (E=8, top-2, d=4096, f=14336): the Mixtral layer at T=2048."""
+    _layer_vs_oracle(with_tokens(C2, 2048), seed=32)
+
+
+def test_moe_layer_with_empty_expert_vs_oracle():
+    """An expert that receives no token (router bias -30): zero rows in K3's variable-K weight
+    gradient, an empty segment in every GEMM, zero gradient rows for that expert."""
+    cfg = LayerConfig("empty-expert", E=8, k=2, d=512, f=384, T=1000)
+    bias = [0.0] * 8
+    bias[3] = -30.0
+    _layer_vs_oracle(cfg, seed=33, expert_bias=bias, check_empty=3)

@@ -194,9 +194,10 @@ class RoutingRef:
 
 
 def route(x: np.ndarray, wg: np.ndarray, k: int, bias=None) -> RoutingRef:
-    logits = router_logits(x, wg)
-    if bias is not None:
-        logits = (logits + np.asarray(bias, dtype=np.float32)[None, :]).astype(np.float32)
+    with np.errstate(invalid="ignore", over="ignore"):  # non-finite rows follow IEEE, as on the GPU
+        logits = router_logits(x, wg)
+        if bias is not None:
+            logits = (logits + np.asarray(bias, dtype=np.float32)[None, :]).astype(np.float32)
     idx, w = topk_softmax(logits, k)
     E = wg.shape[1]
     counts, offsets = counts_offsets(idx, E)

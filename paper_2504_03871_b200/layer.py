@@ -8,23 +8,20 @@ when attention and experts share one device: no all-to-all, one expert group of 
 
 from __future__ import annotations
 
-import weakref
-
 import torch
 
 from . import ops
 
-# Wg^T ([E, d], the router backward's layout) per router weight tensor, rebuilt only when the
-# weight changes (its version counter moves on every in-place update, e.g. an optimizer step)
-_WG_T: "weakref.WeakKeyDictionary[torch.Tensor, tuple]" = weakref.WeakKeyDictionary()
-
 
 def router_weight_t(wg: torch.Tensor) -> torch.Tensor:
-    ent = _WG_T.get(wg)
+    """Wg^T ([E, d], the router backward's layout), kept on the weight tensor itself and rebuilt
+    only when the weight changes (its version counter moves on every in-place update, e.g. an
+    optimizer step)."""
     key = (wg._version, wg.data_ptr())
+    ent = getattr(wg, "_hm_wg_t", None)
     if ent is None or ent[0] != key:
         ent = (key, ops.transpose_bf16(wg.detach()))
-        _WG_T[wg] = ent
+        wg._hm_wg_t = ent
     return ent[1]
 
 

@@ -483,7 +483,16 @@ def run_zp(args, ws, rank, local):
     N = ws - M
     dev = torch.device("cuda", local)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    exp_ctas = 0 if args.expert_capacity >= 1.0 else int(math.ceil(args.expert_capacity * sms))
+    caps = [float(v) for v in str(args.expert_capacity).split(",")]
+    caps = caps * N if len(caps) == 1 else caps
+    if len(caps) != N or min(caps) <= 0 or max(caps) > 1:
+        raise SystemExit(f"--expert-capacity: need 1 or {N} weights in (0, 1], got {args.expert_capacity}")
+
+    def ctas(w):  # capacity weight -> grouped-GEMM grid cap (0 = the whole GPU)
+        return 0 if w >= 1.0 else int(math.ceil(w * sms))
+
+    exp_ctas = ctas(caps[rank - M]) if rank >= M else 0
+    hetero = len(set(caps)) > 1
     shape = ZpLayerShape(c.E, c.k, c.d, c.f, args.mb_tokens, attention=not args.no_attention,
                          router_skew=args.router_skew)
     loads = None
@@ -492,20 +501,41 @@ def run_zp(args, ws, rank, local):
         # expert placement and the busiest-rank expert timing
         from paper_2504_03871_b200.profiler import measure_loads
 
-        lt = torch.tensor(measure_loads(shape, device=dev), dtype=torch.int64, device=dev)
+        lt = torch.tensor(measure_loads(shape, device=dev), dtype=torch.int64, device=dev)  # noqa: E501
         dist.broadcast(lt, 0)
         loads = [int(v) for v in lt.tolist()]
-    durs = measure_durations(shape, M, N, expert_max_ctas=exp_ctas, device=dev, loads=loads)
+    # the planner's expert GPU is the slowest expert rank (Algorithm 1 models one expert class)
+    durs = measure_durations(shape, M, N, expert_max_ctas=ctas(min(caps)), device=dev, loads=loads,
+                             capacity=caps if hetero else None)
+    # profiler -> planner, memory and transport: measured bytes per expert,
+    # activation bytes per role and the device capacity become the spec's memory model (n_min /
+    # n_max bounds of Algorithm 1); the (layer, micro-batch) exchange is timed on NCCL
+    from paper_2504_03871_b200.executor import PeerArena
+    from paper_2504_03871_b200.profiler import measure_exchange, measure_memory, memory_spec_fields
+
+    mem = measure_memory(shape, device=dev)
+    comm_ns = measure_exchange(M, N, args.mb_tokens, c.k, c.d)
+    mt = torch.tensor([mem[k_] for k_ in sorted(mem)] + [comm_ns], dtype=torch.int64, device=dev)
+    dist.broadcast(mt, 0)  # every rank plans with rank 0's probe
+    mem = dict(zip(sorted(mem), (int(v) for v in mt[:-1].tolist())))
+    comm_ns = int(mt[-1])
+    arena = PeerArena.bytes_needed(args.layers, args.microbatches, args.mb_tokens * M * c.k,
+                                   args.mb_tokens * c.k, c.d) if args.transport == "p2p" else 0
+    mem_fields = memory_spec_fields(mem, M, N, args.layers, args.microbatches, args.mb_tokens, c.k, arena)
     # every rank must plan identically: use rank 0's measurement
     t = torch.tensor([durs[k] for k in sorted(durs)], dtype=torch.int64, device=dev)
     dist.broadcast(t, 0)
     durs = dict(zip(sorted(durs), (int(v) for v in t.tolist())))
     from fractions import Fraction
 
+    durs["dispatch_ns"] = durs["combine_ns"] = comm_ns
     plan_durs = {k_: v for k_, v in durs.items() if k_ != "gamma_x100"}
     spec = make_zp_spec(M, N, args.layers, args.microbatches, c.E, c.k, args.mb_tokens, c.d,
                         asym_ea=not args.no_asym_ea, gamma=Fraction(durs["gamma_x100"], 100),
-                        **plan_durs)
+                        **plan_durs, **mem_fields)
+    from paper_2504_03871_b200.costmodel import memory_bounds
+
+    bounds = memory_bounds(spec)
     dur = derive_task_durations(spec)
     from paper_2504_03871_b200 import build_distep_graph
 
@@ -525,7 +555,8 @@ def run_zp(args, ws, rank, local):
     comb = dist.new_group(list(range(ws)))
     be = NativeBackend(dev, max_ctas=exp_ctas if rank >= M else 0)
     ex_cls = ZpP2PExecutor if args.transport == "p2p" else ZpExecutor
-    ex = ex_cls(graph, shape, M, N, rank, be, disp, comb, seed=1234, expert_loads=loads)
+    ex = ex_cls(graph, shape, M, N, rank, be, disp, comb, seed=1234, expert_loads=loads,
+                expert_capacity=caps if hetero else None)
     for _ in range(args.warmup):
         ex.run()
     l0 = ops.LAUNCHES[0]
@@ -583,9 +614,18 @@ def run_zp(args, ws, rank, local):
             "microbatches": args.microbatches, "tokens_per_microbatch": args.mb_tokens,
             "attention_block": not args.no_attention, "parallelism": f"zp{M}+{N}",
             "asym_ea_offload": list(assignment.offload),
-            "transport": args.transport, "schedule": args.schedule, "expert_capacity": args.expert_capacity,
+            "transport": args.transport, "schedule": args.schedule, "expert_capacity": caps,
+            "expert_grid_ctas": [ctas(w) or sms for w in caps],
             "router_skew_zipf": args.router_skew,
-            "expert_placement": "contiguous" if loads is None else "load-balanced (LPT over measured loads)",
+            "expert_placement": ("contiguous" if loads is None and not hetero else
+                                 "load-balanced (LPT over measured loads / capacity weights)"),
+            "memory_probe_bytes": mem,
+            "memory_bounds": {"n_min": bounds.n_min, "n_max": bounds.n_max,
+                              "expert_mem": mem_fields["expert_mem"],
+                              "non_expert_mem_attention": mem_fields["non_expert_mem_attention"],
+                              "non_expert_mem_expert": mem_fields["non_expert_mem_expert"],
+                              "capacity": mem_fields["exp_capacity"]},
+            "measured_exchange_ns": comm_ns,
             "expert_loads_per_mb": loads,
             "measured_durations_ns": durs,
             "l2": "activations and weights exceed the 126 MB L2; no flush",
@@ -840,8 +880,9 @@ def main():
     ap.add_argument("--offload", default="",
                     help="ZP: explicit experts offloaded per expert rank, per layer (e.g. 2,2,2,2,2,2,2,2) "
                          "instead of the Asym-EA plan")
-    ap.add_argument("--expert-capacity", type=float, default=1.0,
-                    help="ZP: capacity weight of expert ranks (grouped-GEMM grid = ceil(w*SMs))")
+    ap.add_argument("--expert-capacity", default="1.0",
+                    help="ZP: capacity weight of the expert ranks, one value or one per expert rank "
+                         "(e.g. 1,0.5); grouped-GEMM grid = ceil(w*SMs) on that rank")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch(args.gpus))

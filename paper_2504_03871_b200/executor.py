@@ -56,24 +56,33 @@ K = TaskKind
 # placement
 
 
-def expert_owners(E: int, M: int, N: int, offload: int, loads=None) -> list:
+def expert_owners(E: int, M: int, N: int, offload: int, loads=None, capacity=None) -> list:
     """Owner rank of every expert of one layer. Base: expert rank M+i owns experts
     [i*E/N, (i+1)*E/N). With offload o, the last o local experts of each expert rank move to
     the attention ranks, dealt in (expert rank, local id) order, o*N/M per attention rank.
 
     ``loads`` (expected routed rows per expert, e.g. under a skewed router) switches to a
-    load-balanced placement: experts by decreasing load go to the least-loaded expert rank
-    with room (E/N each), and the o experts each rank offloads are the ones whose loads are closest to the
-    rank's mean (the planner prices an offloaded expert at an average share, R4)."""
+    load-balanced placement: experts by decreasing load go to the expert rank with room (E/N
+    each) whose load after taking it, divided by its capacity weight (``capacity[i]``, default 1:
+    the per-rank heterogeneity of BASELINE C5), is smallest (LPT), and the o experts each rank
+    offloads are the ones whose loads are closest to the rank's mean (the planner prices an
+    offloaded expert at an average share, R4). Every expert rank keeps E/N experts, so the
+    offload shares of ``offload_scaling`` (``taskgraph.py:178-194``) hold unchanged."""
     per = E // N
+    cap = [1.0] * N if capacity is None else [float(c) for c in capacity]
+    if len(cap) != N or min(cap) <= 0:
+        raise ValueError(f"need {N} positive expert-rank capacity weights, got {capacity}")
+    if loads is None and capacity is not None and len(set(cap)) > 1:
+        loads = [1] * E  # uniform router: LPT still spreads experts by capacity (ties -> rank order)
     if loads is None:
         local = [[i * per + q for q in range(per)] for i in range(N)]
     else:
         order = sorted(range(E), key=lambda e: (-loads[e], e))
         local = [[] for _ in range(N)]
         tot = [0] * N
-        for e in order:  # largest load first, to the least-loaded rank with room (LPT)
-            i = min((i for i in range(N) if len(local[i]) < per), key=lambda i: (tot[i], i))
+        for e in order:  # largest load first, to the rank it loads least (capacity-weighted LPT)
+            i = min((i for i in range(N) if len(local[i]) < per),
+                    key=lambda i: ((tot[i] + loads[e]) / cap[i], tot[i], i))
             local[i].append(e)
             tot[i] += loads[e]
         if offload:
@@ -266,7 +275,7 @@ class ZpExecutor:
 
     def __init__(self, graph: TaskGraph, shape: ZpLayerShape, M: int, N: int, rank: int,
                  backend, disp_group=None, comb_group=None, seed: int = 0,
-                 durations_hint: Optional[dict] = None, expert_loads=None):
+                 durations_hint: Optional[dict] = None, expert_loads=None, expert_capacity=None):
         if graph.mode not in ("zp-full", "distep"):
             raise ValueError("the executor runs zp-full graphs (layer-L experts + loss turnaround) "
                              "or their DistEP lockstep ablation")
@@ -281,7 +290,7 @@ class ZpExecutor:
         self.heads = shape.heads or max(1, shape.d // 128)
         self.orders = default_orders(graph)
         self.issue_order = self._issue_order()
-        owners = [expert_owners(shape.E, M, N, o, expert_loads) for o in graph.assignment.offload]
+        owners = [expert_owners(shape.E, M, N, o, expert_loads, expert_capacity) for o in graph.assignment.offload]
         own = [sorted(e for e in range(shape.E) if ow[e] == rank) for ow in owners]
         self.st = RankState(owners=owners, own=own)
         self.wg_t = {}
@@ -736,6 +745,10 @@ class PeerArena:
         torch.cuda.synchronize(device)
         dist.barrier(group=group)
 
+    @classmethod
+    def bytes_needed(cls, L: int, R: int, cap: int, tk: int, d: int) -> int:
+        return cls.FLAG_BYTES + L * R * (2 * cap + 2 * tk) * d * 2
+
     def offset(self, l: int, j: int, which: str) -> int:
         base = self.FLAG_BYTES + ((l - 1) * self.R + (j - 1)) * self.slot_bytes
         cap, tk, rb = self.cap, self.tk, self.rb
@@ -770,9 +783,9 @@ class ZpP2PExecutor(ZpExecutor):
     the NCCL path) stays a collective. Same task graph, streams and issue order as ZpExecutor."""
 
     def __init__(self, graph, shape, M, N, rank, backend, disp_group=None, comb_group=None,
-                 seed: int = 0, durations_hint=None, expert_loads=None):
+                 seed: int = 0, durations_hint=None, expert_loads=None, expert_capacity=None):
         super().__init__(graph, shape, M, N, rank, backend, disp_group, comb_group, seed, durations_hint,
-                         expert_loads)
+                         expert_loads, expert_capacity)
         if self.W > 8:
             raise ValueError("p2p transport supports at most 8 ranks (one NVSwitch domain)")
         s = shape

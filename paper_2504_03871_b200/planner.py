@@ -62,15 +62,19 @@ def make_zp_spec(M: int, N: int, layers: int, microbatches: int, experts: int, t
                  tokens_per_mb: int, hidden: int, attn_fwd_ns: int, expert_layer_fwd_ns: int,
                  single_expert_fwd_ns: int, dispatch_ns: int = 0, combine_ns: int = 0,
                  gamma=Fraction(2), asym_ea: bool = False, squeeze: str = "verbatim",
-                 expert_mem: int = 0, attn_capacity: int = 10**12, exp_capacity: int = 10**12) -> Spec:
-    """Spec with a duration table (measured B200 times enter here, costmodel.py:88-104)."""
+                 expert_mem: int = 0, attn_capacity: int = 10**12, exp_capacity: int = 10**12,
+                 non_expert_mem_attention: int = 0, non_expert_mem_expert: int = 0) -> Spec:
+    """Spec with a duration table (measured B200 times enter here, costmodel.py:88-104) and,
+    optionally, the measured memory model (``profiler.memory_spec_fields``) that
+    ``costmodel.memory_bounds`` turns into the offload bounds n_min / n_max."""
     from .core import GpuClass, HardwareProfile, ModelSpec, RunOptions, ZpGroupSpec
 
     a = GpuClass("b200-attention", attn_capacity)
     e = GpuClass("b200-expert", exp_capacity)
     prof = HardwareProfile(a, e, {"attn_fwd": int(attn_fwd_ns), "single_expert_fwd": int(single_expert_fwd_ns)},
                            {"expert_layer_fwd": int(expert_layer_fwd_ns)},
-                           {"dispatch": int(dispatch_ns), "combine": int(combine_ns)})
+                           {"dispatch": int(dispatch_ns), "combine": int(combine_ns)},
+                           int(non_expert_mem_attention), int(non_expert_mem_expert))
     model = ModelSpec(layers, experts, top_k, hidden, tokens_per_mb, microbatches, 1, expert_mem, 0)
     return Spec(ZpGroupSpec(M, N, a, e, 900 * 10**9, 2 * hidden), model, prof,
                 RunOptions(mode="zp-full", gamma=Fraction(gamma), asym_ea=asym_ea, squeeze=squeeze))

@@ -9,14 +9,22 @@ them as the reference's duration table (``profile.attention_gpu.durations`` /
   expert_layer_fwd     grouped SwiGLU FFN of the B = s*M*k/N rows an expert rank receives,
                        over its E/N experts, with the rank's capacity cap (max_ctas)
   single_expert_fwd    one expert over B rows on an attention GPU
-  dispatch / combine   bytes per attention rank over the measured NVLink peer bandwidth
+  dispatch / combine   one (layer, micro-batch) exchange, timed on the real communicator
+                       (``measure_exchange``: NCCL all-to-all with the ZP split sizes)
+
+and the memory side of the paper's profiler (``PAPER.md:364``; the reference turns it into
+offload bounds in ``costmodel.memory_bounds``, ``costmodel.py:124-161``): ``measure_memory``
+measures bytes per expert (weights + the executor's fp32 gradient accumulators), the activation
+bytes an expert rank keeps per routed row and an attention rank per token and layer, attention
+parameters per layer, and the device capacity, which ``memory_spec_fields`` folds into the
+spec's ``expert_mem`` / ``memory_capacity`` / ``non_expert_mem_*`` fields.
 """
 
 from __future__ import annotations
 
 import torch
 
-NVLINK_GBS = 770.0  # measured peer copy bandwidth per direction (B200_PROFILING.md)
+NVLINK_GBS = 770.0  # peer copy bandwidth per direction (B200_PROFILING.md); fallback only
 
 
 def _time_ms(fn, reps: int = 5, warmup: int = 2) -> float:
@@ -56,11 +64,13 @@ def measure_loads(shape, device="cuda", seed: int = 0) -> list:
 
 
 def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_ctas: int = 0,
-                      device="cuda", seed: int = 0, loads=None) -> dict:
+                      device="cuda", seed: int = 0, loads=None, capacity=None) -> dict:
     """Duration table (ns) for ``planner.make_zp_spec`` measured with the native kernels.
     With ``loads`` (``measure_loads``) the expert layer is timed on the busiest expert rank of
     the load-balanced placement (the reference's ``load_factor`` for skew, costmodel.py:54-63),
-    with that rank's real per-expert row counts."""
+    with that rank's real per-expert row counts; with per-rank ``capacity`` weights the busiest
+    rank is the one with the largest load / capacity, and ``expert_max_ctas`` should be that
+    rank's grid cap (the caller passes the slowest rank's)."""
     from . import ops
     from .executor import attention_block, rms_norm
 
@@ -94,10 +104,12 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
     if loads is not None:
         from .executor import expert_owners
 
-        owners = expert_owners(E, M, N, 0, loads)
+        owners = expert_owners(E, M, N, 0, loads, capacity)
         tot = sum(loads)
+        cap = list(capacity) if capacity is not None else [1.0] * N
         per_rank = [[e for e in range(E) if owners[e] == M + i] for i in range(N)]
-        busiest = max(per_rank, key=lambda es: sum(loads[e] for e in es))
+        busiest = max(range(N), key=lambda i: sum(loads[e] for e in per_rank[i]) / cap[i])
+        busiest = per_rank[busiest]
         rows = [T * M * k * loads[e] // tot for e in busiest]
         seg_l = [0]
         for r_ in rows:
@@ -128,3 +140,117 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
         "dispatch_ns": int(comm_ns),
         "combine_ns": int(comm_ns),
     }
+
+
+def measure_memory(shape, device="cuda", seed: int = 0) -> dict:
+    """Memory probe with the native kernels on this GPU. Returns bytes:
+
+      capacity              total device memory (cudaMemGetInfo)
+      outside_torch         memory in use that torch did not allocate (CUDA context, NCCL)
+      expert_mem            one expert: bf16 W_ug + W_d and the fp32 gradient accumulators the
+                            executor keeps per owned expert (optimizer state is not held)
+      expert_act_per_row    what an expert rank keeps per routed row and layer between the
+                            forward and the backward (y, h, act of the grouped FFN)
+      attn_act_per_token    what an attention rank keeps per token and layer (attention block
+                            autograd state, pre-norm input, routing, permuted rows)
+      attn_params_per_layer attention block + router weights of one layer and their gradients
+    """
+    from . import ops
+    from .executor import attention_block, rms_norm
+
+    dev = torch.device(device)
+    torch.cuda.synchronize(dev)
+    free, total = torch.cuda.mem_get_info(dev)
+    outside = total - free - torch.cuda.memory_reserved(dev)
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d, f, E, k, T = shape.d, shape.f, shape.E, shape.k, shape.tokens_per_mb
+    heads = shape.heads or max(1, d // 128)
+
+    def rnd(*s, std=1.0):
+        return (torch.randn(s, generator=g, device=dev) * std).to(torch.bfloat16)
+
+    def alloc():
+        torch.cuda.synchronize(dev)
+        return torch.cuda.memory_allocated(dev)
+
+    m0 = alloc()
+    w_ug = rnd(1, 2 * f, d, std=d ** -0.5)
+    w_d = rnd(1, d, f, std=f ** -0.5)
+    gw_ug = torch.zeros(w_ug.shape, dtype=torch.float32, device=dev)
+    gw_d = torch.zeros(w_d.shape, dtype=torch.float32, device=dev)
+    expert_mem = alloc() - m0
+
+    rows = max(T * k // max(E, 1), 256)  # one expert's share of a micro-batch
+    xb = rnd(rows, d)
+    seg = torch.tensor([0, rows], dtype=torch.int32, device=dev)
+    m1 = alloc()
+    kept = ops.grouped_ffn_fwd(xb, seg, w_ug, w_d)
+    expert_act = (alloc() - m1) / rows
+    del kept, xb, w_ug, w_d, gw_ug, gw_d
+
+    m2 = alloc()
+    wqkv = rnd(d, 3 * d, std=d ** -0.5).requires_grad_()
+    wo = rnd(d, d, std=d ** -0.5).requires_grad_()
+    wg = rnd(d, E, std=d ** -0.5)
+    attn_params = 2 * (alloc() - m2) + d * E * 4  # + their gradients (same size) + fp32 router grad
+    x = rnd(T, d).requires_grad_()
+    m3 = alloc()
+    with torch.enable_grad():
+        u = attention_block(x, wqkv, wo, heads) if shape.attention else x * 1
+        z = rms_norm(u)
+    r = ops.router_topk(z.detach(), wg, k)
+    x_perm, _, row_of = ops.dispatch_permute(z.detach(), r)
+    attn_act = (alloc() - m3) / T
+    del u, z, r, x_perm, row_of, x, wqkv, wo, wg
+    torch.cuda.empty_cache()
+    return {"capacity": int(total), "outside_torch": int(max(outside, 0)), "expert_mem": int(expert_mem),
+            "expert_act_per_row": int(round(expert_act)), "attn_act_per_token": int(round(attn_act)),
+            "attn_params_per_layer": int(attn_params)}
+
+
+def memory_spec_fields(mem: dict, M: int, N: int, layers: int, microbatches: int, tokens_per_mb: int,
+                       k: int, arena_bytes: int = 0) -> dict:
+    """The measured probe as the reference's memory model (``costmodel.memory_bounds``): per role,
+    ``non_expert_mem_*`` = memory outside torch + the transport arena + the activations resident
+    at the ZP peak (all L layers x R micro-batches in flight before the first backward) + (attention)
+    its parameters; ``activation_mem_per_token`` stays 0 because the per-role activation bytes
+    differ and are folded into the per-role terms."""
+    rows_per_mb = tokens_per_mb * M * k // N  # routed rows one expert rank receives (R6's B)
+    exp_non = mem["outside_torch"] + arena_bytes + mem["expert_act_per_row"] * rows_per_mb * microbatches * layers
+    attn_non = (mem["outside_torch"] + arena_bytes + mem["attn_params_per_layer"] * layers
+                + mem["attn_act_per_token"] * tokens_per_mb * microbatches * layers)
+    return {"expert_mem": mem["expert_mem"], "attn_capacity": mem["capacity"], "exp_capacity": mem["capacity"],
+            "non_expert_mem_attention": int(attn_non), "non_expert_mem_expert": int(exp_non)}
+
+
+def measure_exchange(M: int, N: int, tokens_per_mb: int, k: int, d: int, group=None, reps: int = 5) -> int:
+    """One (layer, micro-batch) dispatch exchange timed on the real communicator (collective: every
+    rank calls it): each attention rank sends tokens_per_mb*k/N routed bf16 rows to every expert
+    rank through NCCL all_to_all_single with the ZP split sizes (the combine is the mirror
+    image). CUDA events, max over ranks, ns."""
+    import torch.distributed as dist
+
+    W = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per = tokens_per_mb * k // N
+    send = [per if (rank < M and q >= M) else 0 for q in range(W)]
+    recv = [per if (rank >= M and q < M) else 0 for q in range(W)]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sb = torch.empty((max(sum(send), 1), d), dtype=torch.bfloat16, device=dev)
+    rb = torch.empty((max(sum(recv), 1), d), dtype=torch.bfloat16, device=dev)
+
+    def once():
+        dist.all_to_all_single(rb[: sum(recv)], sb[: sum(send)], recv, send, group=group)
+
+    once()
+    torch.cuda.synchronize(dev)
+    dist.barrier(group=group)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        once()
+    b.record()
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(float(t) * 1e6)

@@ -287,3 +287,56 @@ def test_merged_timeline_uses_one_rank_per_role():
     spans = sorted((tl.starts[t.id], tl.ends[t.id]) for t in g.tasks if t.device == "attn" and t.lane[1] == "compute")
     assert all(b[0] >= a[1] for a, b in zip(spans, spans[1:]))
     assert tl.makespan == max(b for iv in per_rank for _, b in iv.values())
+
+
+def test_capacity_weighted_placement():
+    """Per-rank capacity weights (BASELINE C5): the LPT placement divides each rank's load by its
+    weight, so under a skewed router the heavy experts go to the fast rank; every rank keeps E/N
+    experts (offload shares unchanged), and uniform weights reproduce the unweighted placement."""
+    from paper_2504_03871_b200.executor import expert_owners
+
+    E, M, N = 8, 2, 2
+    loads = [int(1000 / (e + 1)) for e in range(E)]
+    assert expert_owners(E, M, N, 0, loads, [1.0, 1.0]) == expert_owners(E, M, N, 0, loads)
+    ow = expert_owners(E, M, N, 0, loads, [1.0, 0.5])
+    rank_load = [sum(l for l, o in zip(loads, ow) if o == M + i) for i in range(N)]
+    assert rank_load[0] > rank_load[1]  # the full-capacity rank carries more rows
+    ratio = lambda ow_: max(sum(l for l, o in zip(loads, ow_) if o == M + i) / c  # noqa: E731
+                            for i, c in enumerate((1.0, 0.5)))
+    assert ratio(ow) < ratio(expert_owners(E, M, N, 0, loads))  # better balanced per capacity
+    assert [sum(1 for x in ow if x == M + i) for i in range(N)] == [E // N] * N
+    for o in (1, 2):
+        owo = expert_owners(E, M, N, o, loads, [1.0, 0.5])
+        assert [sum(1 for x in owo if x == a) for a in range(M)] == [o * N // M] * M
+    # uniform router + unequal weights: still E/N experts per rank
+    owu = expert_owners(E, M, N, 1, None, [1.0, 0.5])
+    assert sorted(owu) == sorted(expert_owners(E, M, N, 1))
+    import pytest as _pt
+
+    with _pt.raises(ValueError):
+        expert_owners(E, M, N, 0, loads, [1.0])
+
+
+def test_memory_spec_fields_drive_memory_bounds():
+    """The profiler's measured memory model reaches Algorithm 1's bounds through the reference's
+    own memory_bounds (costmodel.py:124-161): a capacity that cannot hold every expert's weights
+    forces n_min > 0; an ample one gives n_min = 0 and a finite n_max."""
+    from paper_2504_03871_b200.costmodel import memory_bounds
+    from paper_2504_03871_b200.planner import make_zp_spec
+    from paper_2504_03871_b200.profiler import memory_spec_fields
+
+    mem = {"capacity": 180 * 2**30, "outside_torch": 2**30, "expert_mem": 2**30,
+           "expert_act_per_row": 96 * 1024, "attn_act_per_token": 200 * 1024, "attn_params_per_layer": 200 * 2**20}
+    M = N = 4
+    L, R, T, k, E = 8, 8, 4096, 2, 8
+    fields = memory_spec_fields(mem, M, N, L, R, T, k, arena_bytes=40 * 2**30)
+    spec = make_zp_spec(M, N, L, R, E, k, T, 4096, 10**6, 2 * 10**6, 10**6, **fields)
+    b = memory_bounds(spec)
+    assert b.n_min == 0 and b.n_max is not None and b.n_max > 0
+    # 60 GiB devices, no arena: an expert rank keeps ~48 GiB of activations, so 11 of its 16
+    # experts fit (n_min = 5); an attention rank has ~7.4 GiB left -> 7 experts each (n_max = 7)
+    tight = dict(mem, capacity=60 * 2**30)
+    spec2 = make_zp_spec(M, N, L, R, E, k, T, 4096, 10**6, 2 * 10**6, 10**6,
+                         **memory_spec_fields(tight, M, N, L, R, T, k, arena_bytes=0))
+    b2 = memory_bounds(spec2)
+    assert (b2.n_min, b2.n_max) == (5, 7)

@@ -513,15 +513,15 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200.executor import PeerArena
     from paper_2504_03871_b200.profiler import measure_exchange, measure_memory, memory_spec_fields
 
-    mem = measure_memory(shape, device=dev)
+    memp = measure_memory(shape, device=dev)
     comm_ns = measure_exchange(M, N, args.mb_tokens, c.k, c.d)
-    mt = torch.tensor([mem[k_] for k_ in sorted(mem)] + [comm_ns], dtype=torch.int64, device=dev)
+    mt = torch.tensor([memp[k_] for k_ in sorted(memp)] + [comm_ns], dtype=torch.int64, device=dev)
     dist.broadcast(mt, 0)  # every rank plans with rank 0's probe
-    mem = dict(zip(sorted(mem), (int(v) for v in mt[:-1].tolist())))
+    memp = dict(zip(sorted(memp), (int(v) for v in mt[:-1].tolist())))
     comm_ns = int(mt[-1])
     arena = PeerArena.bytes_needed(args.layers, args.microbatches, args.mb_tokens * M * c.k,
                                    args.mb_tokens * c.k, c.d) if args.transport == "p2p" else 0
-    mem_fields = memory_spec_fields(mem, M, N, args.layers, args.microbatches, args.mb_tokens, c.k, arena)
+    mem_fields = memory_spec_fields(memp, M, N, args.layers, args.microbatches, args.mb_tokens, c.k, arena)
     # every rank must plan identically: use rank 0's measurement
     t = torch.tensor([durs[k] for k in sorted(durs)], dtype=torch.int64, device=dev)
     dist.broadcast(t, 0)
@@ -619,7 +619,7 @@ def run_zp(args, ws, rank, local):
             "router_skew_zipf": args.router_skew,
             "expert_placement": ("contiguous" if loads is None and not hetero else
                                  "load-balanced (LPT over measured loads / capacity weights)"),
-            "memory_probe_bytes": mem,
+            "memory_probe_bytes": memp,
             "memory_bounds": {"n_min": bounds.n_min, "n_max": bounds.n_max,
                               "expert_mem": mem_fields["expert_mem"],
                               "non_expert_mem_attention": mem_fields["non_expert_mem_attention"],
@@ -838,9 +838,21 @@ def relaunch(n: int) -> int:
     return subprocess.run(cmd).returncode
 
 
+def _plain(obj, path="$"):
+    """JSON-ready copy of obj; a stray tensor is converted and reported on stderr with its path."""
+    if isinstance(obj, dict):
+        return {k: _plain(v, f"{path}.{k}") for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_plain(v, f"{path}[{i}]") for i, v in enumerate(obj)]
+    if isinstance(obj, torch.Tensor):
+        print(f"bench.py: tensor at {path} in the result line", file=sys.stderr)
+        return obj.tolist()
+    return obj
+
+
 def _emit(obj) -> None:
     """Print the one JSON result line on the original stdout."""
-    _OUT.write(json.dumps(obj) + "\n")
+    _OUT.write(json.dumps(_plain(obj)) + "\n")
     _OUT.flush()
 
 

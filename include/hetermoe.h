@@ -54,13 +54,17 @@ int hm_gemm_stats(unsigned long long* out);
 /* ---- K1 router: logits (fixed-order fp32), top-k, softmax over the k, histogram, offsets ----
  * x[T,d] bf16, wg[d,E] bf16, bias[E] fp32 or NULL (logits = x . wg + bias). Outputs: idx[T,k] int32, w[T,k] fp32,
  * logits[T,E] fp32 (required scratch, also a result), counts[E], offsets[E+1] int32,
- * chunk_base[hm_router_chunk_elems(T,E)] int32 (consumed by hm_dispatch_permute).
- * Requires d % 256 == 0, 1 <= k <= 8, k <= E <= 256.
+ * chunk_base[hm_router_chunk_elems(T,E)] int32 (per-chunk row bases, consumed by
+ * hm_dispatch_permute; its last element is the fused kernel's completion counter).
+ * Requires d = 256 * 2^m <= 16384, 1 <= k <= 8, k <= E <= 256.
  * Replaces: the router/gate folded into ATTN_F (taskgraph.py:220-246). */
 int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
                    int32_t* idx, float* w, float* logits, int32_t* counts, int32_t* offsets,
                    int32_t* chunk_base, void* stream);
 size_t hm_router_chunk_elems(int T, int E);
+/* kernel launches hm_router_topk issues for this shape (1 when logits, top-k, histogram and
+ * scan run fused: E <= 8 for d <= 4096), 0 for an unsupported shape or T = 0 */
+int hm_router_launches(int T, int d, int E);
 
 /* ---- K2 dispatch permute: x[T,d] -> x_perm[T*k,d] grouped by expert, stable in token order --
  * row_src[T*k] = source token of each permuted row, row_of[T,k] = permuted row of (t, slot).

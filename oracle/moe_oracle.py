@@ -20,9 +20,10 @@ The only reference-pinned quantities at this boundary are aggregate token counts
 ``tests/test_oracle.py``.
 
 Router logits use the SAME fixed fp32 summation order as the CUDA kernel
-(``paper_2504_03871_b200/csrc/moe_kernels.cuh``): lane L of 32 accumulates
-i = 256*j + 8*L + q (j ascending, q = 0..7) with single-rounding multiply-adds (bf16 x bf16
-products are exact in fp32), then an xor butterfly over lanes with offsets 16, 8, 4, 2, 1.
+(``paper_2504_03871_b200/csrc/moe_kernels.cuh``): per 256-wide block j, lane L of 32 accumulates
+i = 256*j + 8*L + q (q = 0..7) with single-rounding multiply-adds (bf16 x bf16 products are
+exact in fp32), an xor butterfly over lanes with offsets 16, 8, 4, 2, 1 gives the block
+partial, and the block partials are added in block order.
 Everything that derives from the logits (indices, counts, offsets, row maps) is therefore
 bit-exact; floating outputs are compared with the tolerances written in the tests.
 """
@@ -47,7 +48,12 @@ def bf16_round(a: torch.Tensor) -> torch.Tensor:
 
 
 def router_logits(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
-    """Fixed-order fp32 logits. x [T,d] and wg [d,E] hold bf16-representable float32 values."""
+    """Fixed-order fp32 logits. x [T,d] and wg [d,E] hold bf16-representable float32 values.
+
+    Blocked order (the CUDA kernel's, ``csrc/moe_kernels.cuh``): d splits into blocks of 256;
+    inside block j lane L accumulates i = 256*j + 8*L + q for q = 0..7 from 0 with one rounding
+    per step, the 32 lanes are combined by an xor butterfly (16, 8, 4, 2, 1) into the block
+    partial P_j, and the logit is ((P_0 + P_1) + P_2) + ... in block order."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     wg = np.ascontiguousarray(wg, dtype=np.float32)
     T, d = x.shape
@@ -56,15 +62,18 @@ def router_logits(x: np.ndarray, wg: np.ndarray) -> np.ndarray:
     nj = d // 256
     xr = x.reshape(T, nj, 32, 8)
     wr = wg.reshape(nj, 32, 8, E)
-    acc = np.zeros((T, 32, E), dtype=np.float32)
-    for j in range(nj):
-        for q in range(8):
-            prod = xr[:, j, :, q, None] * wr[None, j, :, q, :]  # exact in fp32
-            acc = acc + prod  # one rounding == fused multiply-add
+    acc = np.zeros((T, nj, 32, E), dtype=np.float32)
+    for q in range(8):
+        prod = xr[:, :, :, q, None] * wr[None, :, :, q, :]  # exact in fp32
+        acc = acc + prod  # one rounding == fused multiply-add
     lanes = np.arange(32)
     for off in (16, 8, 4, 2, 1):
-        acc = acc + acc[:, lanes ^ off, :]
-    return acc[:, 0, :].copy()
+        acc = acc + acc[:, :, lanes ^ off, :]
+    part = acc[:, :, 0, :]
+    out = part[:, 0, :].copy()
+    for j in range(1, nj):
+        out = out + part[:, j, :]
+    return out
 
 
 _CLIB = None

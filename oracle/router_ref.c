@@ -18,30 +18,35 @@ static inline float bf16(uint16_t h) {
   return f;
 }
 
-/* logits[t,e]: lane L accumulates i = 256*j + 8*L + q (j ascending, q = 0..7) with one rounding
- * per step (bf16 products are exact in fp32), then an xor butterfly 16, 8, 4, 2, 1. */
+/* logits[t,e], blocked order: for each 256-wide block j, lane L accumulates i = 256*j + 8*L + q
+ * (q = 0..7) from 0 with one rounding per step (bf16 products are exact in fp32), an xor
+ * butterfly 16, 8, 4, 2, 1 combines the 32 lanes into the block partial P_j, and the logit is
+ * ((P_0 + P_1) + P_2) + ... in block order. */
 void hm_ref_router_logits(const uint16_t* x, const uint16_t* wg, int T, int d, int E, float* out) {
   const int nj = d / 256;
 #pragma omp parallel for schedule(static)
   for (int t = 0; t < T; ++t) {
     float lane[32];
     for (int e = 0; e < E; ++e) {
-      for (int L = 0; L < 32; ++L) {
-        float acc = 0.0f;
-        for (int j = 0; j < nj; ++j)
+      float total = 0.0f;
+      for (int j = 0; j < nj; ++j) {
+        for (int L = 0; L < 32; ++L) {
+          float acc = 0.0f;
           for (int q = 0; q < 8; ++q) {
             const int i = 256 * j + 8 * L + q;
             volatile float prod = bf16(x[(long)t * d + i]) * bf16(wg[(long)i * E + e]);
             acc = acc + prod;
           }
-        lane[L] = acc;
+          lane[L] = acc;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+          float nxt[32];
+          for (int L = 0; L < 32; ++L) nxt[L] = lane[L] + lane[L ^ off];
+          memcpy(lane, nxt, sizeof(lane));
+        }
+        total = (j == 0) ? lane[0] : total + lane[0];
       }
-      for (int off = 16; off > 0; off >>= 1) {
-        float nxt[32];
-        for (int L = 0; L < 32; ++L) nxt[L] = lane[L] + lane[L ^ off];
-        memcpy(lane, nxt, sizeof(lane));
-      }
-      out[(long)t * E + e] = lane[0];
+      out[(long)t * E + e] = total;
     }
   }
 }

@@ -34,6 +34,7 @@ SIGNATURES = {
     "hm_num_sms": (_I, []),
     "hm_gemm_stats": (_I, [_P]),
     "hm_router_chunk_elems": (ctypes.c_size_t, [_I, _I]),
+    "hm_router_launches": (_I, [_I, _I, _I]),
     "hm_router_topk": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "hm_dispatch_permute": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "hm_unpermute_sum": (_I, [_P, _P, _I, _I, _I, _P, _P]),

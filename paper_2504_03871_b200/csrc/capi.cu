@@ -341,15 +341,67 @@ const char* hm_last_error(void) { return g_last_error.c_str(); }
 int hm_num_sms(void) { return num_sms(); }
 
 // ---------------------------------------------------------------------------------------------
-size_t hm_router_chunk_elems(int T, int E) {
-  return static_cast<size_t>((T + hm::kChunk - 1) / hm::kChunk) * static_cast<size_t>(E);
+// Router plan for d (blocks of 256, a power of two up to 64): EGW experts per CTA group and BPW
+// blocks per warp keep 64 fp32 router weights per thread in registers.
+static bool router_shape(int d, int* egw, int* bpw) {
+  if (d <= 0 || d % 256 != 0) return false;
+  const int nj = d / 256;
+  if (nj & (nj - 1)) return false;
+  if (nj <= 16) { *egw = 8; *bpw = 1; }
+  else if (nj == 32) { *egw = 4; *bpw = 2; }
+  else if (nj == 64) { *egw = 2; *bpw = 4; }
+  else return false;
+  return true;
 }
+
+// HM_ROUTER_UNFUSED: logits kernel + separate top-k + scan even for one expert group (read on
+// every call: tests switch it at run time to compare the two paths)
+static bool router_unfused_forced() { return getenv("HM_ROUTER_UNFUSED") != nullptr; }
+
+int hm_router_launches(int T, int d, int E) {
+  int egw, bpw;
+  if (T <= 0 || !router_shape(d, &egw, &bpw)) return 0;
+  return (E <= egw && !router_unfused_forced()) ? 1 : 3;
+}
+
+size_t hm_router_chunk_elems(int T, int E) {
+  // per-chunk counts / row bases, then the fused kernel's CTA completion counter
+  const size_t nchunk = (static_cast<size_t>(T) + hm::kChunk - 1) / hm::kChunk;
+  return nchunk * E + 1;
+}
+
+}  // extern "C"
+
+template <int EGW, int BPW, bool FUSE>
+static int launch_router_fused(int groups, cudaStream_t st, const __nv_bfloat16* xb, const __nv_bfloat16* wb,
+                               const float* bias, int T, int d, int E, float* logits, int k, int32_t* idx,
+                               float* w, int32_t* chunk_base, int32_t* counts, int32_t* offsets) {
+  auto kern = hm::router_fused_kernel<EGW, BPW, FUSE>;
+  const size_t smem = hm::router_fused_smem_bytes(EGW);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return fail(static_cast<int>(e), "router smem attr: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  const int TG = hm::kRouterItems / (d / 256);
+  const int units = (T + TG - 1) / TG;
+  int ranges = num_sms() / groups;  // one persistent CTA per SM over all (range, group) pairs
+  if (ranges < 1) ranges = 1;
+  if (ranges > units) ranges = units;
+  kern<<<ranges * groups, hm::kRouterThreads, smem, st>>>(xb, wb, bias, T, d, E, ranges, logits, k, idx, w,
+                                                          chunk_base, counts, offsets);
+  return check_launch("router_fused");
+}
+
+extern "C" {
 
 int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
                    int32_t* idx, float* w, float* logits, int32_t* counts, int32_t* offsets,
                    int32_t* chunk_base, void* stream) {
-  if (T < 0 || d <= 0 || d % 256 != 0 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK || k > E)
-    return fail(HM_E_SHAPE, "router: unsupported shape T=%d d=%d E=%d k=%d", T, d, E, k);
+  int egw = 0, bpw = 0;
+  if (T < 0 || !router_shape(d, &egw, &bpw) || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK || k > E)
+    return fail(HM_E_SHAPE, "router: unsupported shape T=%d d=%d E=%d k=%d (d = 256 * 2^m <= 16384)", T, d, E, k);
   if (!aligned16(x)) return fail(HM_E_ALIGN, "router: x not 16-byte aligned");
   cudaStream_t st = S(stream);
   const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;
@@ -360,94 +412,22 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
   }
   const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
   const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(wg);
-  if (E % 8 == 0 && E > 16 && aligned16(wg) && !getenv("HM_ROUTER_V1") && !getenv("HM_ROUTER_EG16")) {
-    // many expert groups: 8 experts x 8 tokens per warp, 8 warps, 2 CTAs per SM (half the
-    // shared-memory weight traffic per FMA of the 16 x 4 shape); same order, same logits
-    const size_t smem3 = static_cast<size_t>(d) * 8 * 4 + static_cast<size_t>(d / 8) * 16;
-    if (smem3 <= 200 * 1024) {
-      const int ngroups = E / 8;
-      constexpr int tt = 8, nw = 8;
-      const int per_iter = nw * tt;
-      int gx = (T + per_iter - 1) / per_iter;
-      const int cap = (2 * num_sms() + ngroups - 1) / ngroups;
-      if (gx > cap) gx = cap;
-      auto kern = hm::router_logits2_kernel<8, tt, false, nw, 2, false>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3);
-      kern<<<dim3(gx, ngroups), nw * 32, smem3, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
-                                                       nullptr, nullptr);
-      if (int rc = check_launch("router_logits2(8x8)")) return rc;
-      launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
-      if (int rc = check_launch("router_topk")) return rc;
-      hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
-      return check_launch("router_scan");
-    }
+  const int groups = (E + egw - 1) / egw;
+  if (groups == 1 && !router_unfused_forced()) {
+    // logits, top-k, softmax, chunk histogram and scan in one kernel (the histogram accumulates
+    // with atomics into the zeroed chunk table; the last CTA scans it)
+    cudaMemsetAsync(chunk_base, 0, sizeof(int32_t) * hm_router_chunk_elems(T, E), st);
+    if (egw == 8) return launch_router_fused<8, 1, true>(1, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets);
+    if (egw == 4) return launch_router_fused<4, 2, true>(1, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets);
+    return launch_router_fused<2, 4, true>(1, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets);
   }
-  if (E % 8 == 0 && aligned16(wg) && !getenv("HM_ROUTER_V1")) {
-    // fp32-staged, bank-conflict-free variant (same summation order, bit-identical logits)
-    const int eg2 = E == 8 ? 8 : 16;
-    const size_t smem2 = static_cast<size_t>(d) * eg2 * 4 + static_cast<size_t>(d / 8) * 16;
-    if (smem2 <= 200 * 1024) {
-      const int ngroups = (E + eg2 - 1) / eg2;
-      constexpr int tt = 4;
-      const int per_iter = hm::kRouter2Warps * tt;
-      int gx = (T + per_iter - 1) / per_iter;
-      const int cap = (num_sms() + ngroups - 1) / ngroups;
-      if (gx > cap) gx = cap;
-      dim3 grid(gx, ngroups);
-      if (ngroups == 1 && !getenv("HM_ROUTER_UNFUSED")) {
-        // one expert group: top-k, softmax and chunk histogram fused into the logits kernel
-        auto kern = eg2 == 8 ? hm::router_logits2_kernel<8, tt, true> : hm::router_logits2_kernel<16, tt, true>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits, k, idx, w,
-                                                           chunk_base);
-        if (int rc = check_launch("router_logits2_topk")) return rc;
-        hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
-        return check_launch("router_scan");
-      }
-      if (eg2 == 8) {
-        auto kern = hm::router_logits2_kernel<8, tt>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
-                                                           nullptr, nullptr);
-      } else {
-        auto kern = hm::router_logits2_kernel<16, tt>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-        kern<<<grid, hm::kRouter2Warps * 32, smem2, st>>>(xb, wb, bias, T, d, E, logits, 0, nullptr,
-                                                           nullptr, nullptr);
-      }
-      if (int rc = check_launch("router_logits2")) return rc;
-      launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
-      if (int rc = check_launch("router_topk")) return rc;
-      hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
-      return check_launch("router_scan");
-    }
-  }
-  int eg = E <= 8 ? 8 : (E <= 16 ? 16 : 32);
-  const size_t smem = static_cast<size_t>(d) * eg * 2;
-  if (smem > 200 * 1024) return fail(HM_E_SHAPE, "router: d*EG too large for shared memory");
-  const int ngroups = (E + eg - 1) / eg;
-  const int tt = (eg == 32) ? 2 : 4;
-  const int tok_per_iter = hm::kRouterWarps * tt;
-  int gx = (T + tok_per_iter - 1) / tok_per_iter;
-  const int cap = (2 * num_sms() + ngroups - 1) / ngroups;
-  if (gx > cap) gx = cap;
-  dim3 grid(gx, ngroups);
-  if (eg == 8) {
-    auto kern = hm::router_logits_kernel<8, 4>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
-  } else if (eg == 16) {
-    auto kern = hm::router_logits_kernel<16, 4>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
-  } else {
-    auto kern = hm::router_logits_kernel<32, 2>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, hm::kRouterWarps * 32, smem, st>>>(xb, wb, bias, T, d, E, logits);
-  }
-  if (int rc = check_launch("router_logits")) return rc;
+  int rc;
+  if (egw == 8) rc = launch_router_fused<8, 1, false>(groups, st, xb, wb, bias, T, d, E, logits, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
+  else if (egw == 4) rc = launch_router_fused<4, 2, false>(groups, st, xb, wb, bias, T, d, E, logits, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
+  else rc = launch_router_fused<2, 4, false>(groups, st, xb, wb, bias, T, d, E, logits, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
+  if (rc) return rc;
   launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
-  if (int rc = check_launch("router_topk")) return rc;
+  if (int rc2 = check_launch("router_topk")) return rc2;
   hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);
   return check_launch("router_scan");
 }

@@ -105,6 +105,16 @@ HM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// 1-D bulk copy global -> shared (TMA engine, no tensor map), completion counted in bytes on an
+// mbarrier of this CTA; bytes and both addresses multiples of 16
+HM_DEV void bulk_load_1d(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ---------------------------------------------------------------------------------------------
 // TMA
 

@@ -1,14 +1,17 @@
 // moe_kernels.cuh — K1 router/top-k, K2 dispatch permute (+ unpermute), K4 combine (+ bwd).
 //
-// Semantics fixed by the CPU oracle (oracle/moe_oracle.py):
-//  * router logits l[t,e] = sum_i x[t,i] * Wg[i,e] in fp32 with a FIXED order: lane L of a warp
-//    accumulates i = 256*j + 8*L + q (j ascending, then q = 0..7) with fused multiply-adds
-//    (bf16*bf16 products are exact in fp32, so FMA == mul-then-add), then the 32 lane partials
-//    are combined by an xor butterfly (offsets 16, 8, 4, 2, 1). Indices, counts and the
-//    permutation therefore reproduce bit-for-bit on the CPU.
+// Semantics fixed by the CPU oracle (oracle/moe_oracle.py, oracle/router_ref.c):
+//  * router logits l[t,e] = sum_i x[t,i] * Wg[i,e] in fp32 with a FIXED "blocked" order. d is
+//    split into blocks of 256 (j = 0 .. d/256-1). Inside block j, lane L of 32 accumulates
+//    i = 256*j + 8*L + q for q = 0..7 with fused multiply-adds starting from 0 (bf16*bf16
+//    products are exact in fp32, so FMA == mul-then-add), then the 32 lane partials are combined
+//    by an xor butterfly (offsets 16, 8, 4, 2, 1) into the block partial P_j; finally
+//    l = ((P_0 + P_1) + P_2) + ... in block order. Indices, counts and the permutation
+//    therefore reproduce bit-for-bit on the CPU.
 //  * an optional per-expert bias is added last (one fp32 rounding): l[t,e] = dot + bias[e]
 //    (router skew for the Asym-EA sweep; bias-based load balancing).
-//  * top-k: k largest logits, ties -> lower expert id; w = softmax over the k selected logits.
+//  * top-k: k largest logits, ties -> lower expert id, NaN after every number, each expert at
+//    most once; w = softmax over the k selected logits.
 //  * dispatch order: stable by (expert, token); a token appears at most once per expert.
 //    Tokens are processed in chunks of kChunk; chunk c's rows for expert e start at
 //    chunk_base[c][e] = offsets[e] + sum_{c'<c} count[c'][e].
@@ -20,7 +23,6 @@ namespace hm {
 
 constexpr int kChunk = 64;          // tokens per dispatch chunk (one permute CTA)
 constexpr int kMaxTopK = 8;
-constexpr int kRouterWarps = 8;
 
 // Top-k marks an already-selected expert with NaN: the comparator (v > best, or v == best with a
 // lower id) never picks a NaN, so a selected expert cannot be chosen again even when the row's
@@ -30,279 +32,297 @@ constexpr int kRouterWarps = 8;
 #define kSelectedMark __int_as_float(0x7fc00000)
 
 // ------------------------------------------------------------------------------------------
-// K1a: router logits. grid = (token blocks, expert groups). EG experts per group staged in
-// shared memory as [d][EG] bf16. Each warp handles TT tokens at a time.
-template <int EG, int TT>
-__global__ void __launch_bounds__(kRouterWarps * 32)
-    router_logits_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                         const float* __restrict__ bias, int T, int d, int E,
-                         float* __restrict__ logits) {
-  extern __shared__ __align__(16) uint8_t smem_r[];
-  __nv_bfloat16* ws = reinterpret_cast<__nv_bfloat16*>(smem_r);  // [d][EG]
-  const int e0 = blockIdx.y * EG;
-  // stage Wg[:, e0:e0+EG]
-  for (int idx = threadIdx.x; idx < d * EG; idx += blockDim.x) {
-    const int i = idx / EG, e = idx % EG;
-    ws[idx] = (e0 + e < E) ? wg[static_cast<long>(i) * E + e0 + e] : __float2bfloat16(0.f);
+// K1a: router logits (+ fused top-k, softmax, chunk histogram and scan when the experts form one
+// group). Persistent: one CTA of 16 warps per SM (per expert group), each over a contiguous
+// token range. Token rows stream into a shared-memory ring by 1-D bulk copies (TMA engine;
+// 32 KB stages of 64 / nj tokens, nj = d / 256 blocks). The router weight never touches shared
+// memory: warp w owns block(s) j and keeps Wg[256 j + 8 L + q, e0 .. e0 + EGW) in registers
+// (lane L, q = 0..7: 8 x EGW fp32). Per (token, block) item a lane does 8 x EGW FMAs (packed
+// FFMA2: two IEEE fma.rn per instruction, the scalar per-accumulator sequence) and the warp
+// reduces its EGW lane partials with a reduce-scatter butterfly (offsets 16, 8, ... halving the
+// vector; then the plain xor steps): log2(EGW) + (5 - log2(EGW)) shuffle rounds of
+// EGW/2 + ... + 1 values — 9 shuffles for EGW = 8 instead of 40 — and, because fp32 addition is
+// commutative, every expert's value is the same tree as the full butterfly's. The block partials
+// go to shared memory and 8 x TG threads add them in block order (+ bias).
+constexpr int kRouterThreads = 512;
+constexpr int kRouterStages = 4;
+constexpr int kRouterStageBytes = 32768;  // 64 (token, block) items of 512 bytes
+constexpr int kRouterItems = 64;
+
+// reduce-scatter butterfly of EGW values over the 32 lanes; returns the value of expert
+// router_lane_expert<EGW>(lane), identical on the 32 / EGW lanes that share it
+template <int EGW>
+HM_DEV float router_reduce_scatter(const float (&v)[EGW], int lane) {
+  float cur[EGW];
+#pragma unroll
+  for (int e = 0; e < EGW; ++e) cur[e] = v[e];
+  int off = 16;
+#pragma unroll
+  for (int h = EGW / 2; h >= 1; h >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int m = 0; m < h; ++m) {
+      const float keep = up ? cur[m + h] : cur[m];
+      const float send = up ? cur[m] : cur[m + h];
+      cur[m] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+    off >>= 1;
+  }
+  float r = cur[0];
+#pragma unroll
+  for (int o = 32 / EGW / 2; o >= 1; o >>= 1) r = r + __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
+template <int EGW>
+HM_DEV int router_lane_expert(int lane) {
+  int e = 0, off = 16;
+#pragma unroll
+  for (int h = EGW / 2; h >= 1; h >>= 1) {
+    if (lane & off) e += h;
+    off >>= 1;
+  }
+  return e;
+}
+
+// Per-expert totals, exclusive offsets and per-chunk row bases (in place) from per-chunk counts.
+// Threads (g, e) of the CTA: chunk group g of G = blockDim / Epad, expert e; loads coalesced
+// over e. part: blockDim ints of shared memory, off: 257 ints.
+HM_DEV void router_scan_block(int32_t* __restrict__ chunk_counts /*in: counts, out: bases*/, int nchunk,
+                              int E, int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                              int* part, int* off) {
+  int epad = 1;
+  while (epad < E) epad <<= 1;
+  const int G = blockDim.x / epad;
+  const int g = threadIdx.x / epad, e = threadIdx.x % epad;
+  const int c_lo = static_cast<int>((static_cast<long>(nchunk) * g) / G);
+  const int c_hi = static_cast<int>((static_cast<long>(nchunk) * (g + 1)) / G);
+  int s = 0;
+  if (e < E && g < G) {
+#pragma unroll 8
+    for (int c = c_lo; c < c_hi; ++c) s += __ldcg(chunk_counts + static_cast<long>(c) * E + e);
+  }
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < epad) {  // exclusive prefix over the chunk groups of expert e = threadIdx.x
+    int a = 0;
+    for (int gg = 0; gg < G; ++gg) {
+      const int v = part[gg * epad + threadIdx.x];
+      part[gg * epad + threadIdx.x] = a;
+      a += v;
+    }
+    if (threadIdx.x < E) off[threadIdx.x] = a;  // expert total, scanned below
   }
   __syncthreads();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nj = d / 256;
-  const int tokens_per_block_iter = kRouterWarps * TT;
-  for (int t0 = blockIdx.x * tokens_per_block_iter + warp * TT; t0 < T;
-       t0 += gridDim.x * tokens_per_block_iter) {
-    float acc[TT][EG];
-#pragma unroll
-    for (int a = 0; a < TT; ++a)
-#pragma unroll
-      for (int e = 0; e < EG; ++e) acc[a][e] = 0.f;
-
-    // x rows are streamed with one 16-byte load per token per j, prefetched one j ahead
-    uint4 xv[TT], xn[TT];
-#pragma unroll
-    for (int a = 0; a < TT; ++a) {
-      const int t = min(t0 + a, T - 1);
-      xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + lane * 8));
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int i = 0; i < E; ++i) {
+      const int t = off[i];
+      off[i] = a;
+      counts[i] = t;
+      offsets[i] = a;
+      a += t;
     }
-    for (int j = 0; j < nj; ++j) {
-      const int ibase = j * 256 + lane * 8;
-      if (j + 1 < nj) {
-#pragma unroll
-        for (int a = 0; a < TT; ++a) {
-          const int t = min(t0 + a, T - 1);
-          xn[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase + 256));
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const __nv_bfloat16* wrow = ws + (ibase + q) * EG;
-        float wv[EG];
-#pragma unroll
-        for (int e = 0; e < EG; e += 8) {
-          uint4 w8 = *reinterpret_cast<const uint4*>(wrow + e);
-          const uint16_t* ws16 = reinterpret_cast<const uint16_t*>(&w8);
-#pragma unroll
-          for (int z = 0; z < 8; ++z) wv[e + z] = bf16_to_f32(ws16[z]);
-        }
-#pragma unroll
-        for (int a = 0; a < TT; ++a) {
-          const float xf = bf16_to_f32(reinterpret_cast<const uint16_t*>(&xv[a])[q]);
-#pragma unroll
-          for (int e = 0; e < EG; ++e) acc[a][e] = __fmaf_rn(xf, wv[e], acc[a][e]);
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < TT; ++a) xv[a] = xn[a];
-    }
-    // xor butterfly across lanes (fixed order 16, 8, 4, 2, 1)
-#pragma unroll
-    for (int a = 0; a < TT; ++a)
-#pragma unroll
-      for (int e = 0; e < EG; ++e) {
-        float v = acc[a][e];
-        v = v + __shfl_xor_sync(0xffffffffu, v, 16);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 8);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 4);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 2);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 1);
-        acc[a][e] = v;
-      }
-    // lane e writes expert e (EG <= 32)
-#pragma unroll
-    for (int a = 0; a < TT; ++a) {
-      const int t = t0 + a;
-      if (t < T) {
-#pragma unroll
-        for (int e = 0; e < EG; ++e)
-          if (lane == e && e0 + e < E)
-            logits[static_cast<long>(t) * E + e0 + e] = bias ? acc[a][e] + bias[e0 + e] : acc[a][e];
-      }
+    off[E] = a;
+    offsets[E] = a;
+  }
+  __syncthreads();
+  if (e < E && g < G) {
+    int base = off[e] + part[threadIdx.x];
+#pragma unroll 8
+    for (int c = c_lo; c < c_hi; ++c) {
+      int32_t* p = chunk_counts + static_cast<long>(c) * E + e;
+      const int v = __ldcg(p);
+      *p = base;
+      base += v;
     }
   }
 }
 
-// K1a (v2, fp32-staged): same summation order as router_logits_kernel — lane L owns
-// i = 256 j + 8 L + q, accumulates over (j, q) in order, then the xor butterfly — so the logits
-// are bit-identical, but Wg[:, e0:e0+EG] is staged ONCE per CTA as fp32 (no per-token bf16
-// unpacking), rows padded by 16 bytes every 8 rows so that the 8 lanes of each LDS.128 phase
-// (rows 8 apart) hit disjoint banks, with 16 warps per CTA and TT tokens per warp.
-constexpr int kRouter2Warps = 16;
-
-HM_DEV int router2_row_off(int i, int eg) {  // float offset of row i in the padded [d][EG] tile
-  return i * eg + (i >> 3) * 4;
+// top-k (NaN-marked selection, ties -> lower id, all-NaN -> lowest unselected id) + softmax of
+// one token's E logits held in v[0..E); EP >= E compile-time bound
+template <int EP>
+HM_DEV void router_select(float (&v)[EP], int E, int k, int32_t* idx_out, float* w_out, int32_t* hist_row) {
+  float sel_l[kMaxTopK];
+  int sel_e[kMaxTopK];
+  for (int s = 0; s < k; ++s) {
+    float bv = -INFINITY;
+    int be = 0x7fffffff;
+#pragma unroll
+    for (int e = 0; e < EP; ++e)
+      if (e < E && (v[e] > bv || (v[e] == bv && e < be))) { bv = v[e]; be = e; }
+    if (be == 0x7fffffff) {
+      be = 0;
+      bv = kSelectedMark;  // the selected logit is NaN (the softmax sees it)
+      for (int p = 0; p < s; ++p)
+        if (sel_e[p] == be) { ++be; p = -1; }
+    }
+    sel_l[s] = bv;
+    sel_e[s] = be;
+#pragma unroll
+    for (int e = 0; e < EP; ++e)
+      if (e == be) v[e] = kSelectedMark;
+  }
+  float ex[kMaxTopK];
+  float sum = 0.f;
+  for (int s = 0; s < k; ++s) { ex[s] = expf(sel_l[s] - sel_l[0]); sum += ex[s]; }
+  for (int s = 0; s < k; ++s) {
+    idx_out[s] = sel_e[s];
+    w_out[s] = ex[s] / sum;
+    atomicAdd(hist_row + sel_e[s], 1);
+  }
 }
 
-// FUSE (one expert group, E == EG, kRouter2Warps * TT == kChunk): the top-k, softmax and
-// per-chunk histogram of router_topk_kernel run in the same kernel on the logits still in
-// registers (identical comparisons and arithmetic, so identical results), one chunk per CTA
-// iteration.
-// NW warps per CTA, MINB CTAs per SM: (16, 1) by default; the many-group case (E > 16) uses
-// EG = 8 experts x TT = 8 tokens per warp with (8, 2): every shared-memory weight load then
-// feeds twice the FMAs (the EG = 16 x TT = 4 kernel is shared-memory-bandwidth bound).
-template <int EG, int TT, bool FUSE = false, int NW = kRouter2Warps, int MINB = 1,
-          bool PREFETCH = true>
-__global__ void __launch_bounds__(NW * 32, MINB)
-    router_logits2_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                          const float* __restrict__ bias, int T, int d, int E,
-                          float* __restrict__ logits, int k = 0, int32_t* __restrict__ idx = nullptr,
-                          float* __restrict__ w = nullptr,
-                          int32_t* __restrict__ chunk_counts = nullptr) {
-  static_assert(!FUSE || NW * TT == kChunk, "fused top-k: one chunk per CTA iteration");
-  __shared__ int hist[FUSE ? EG : 1];
-  if (FUSE && threadIdx.x < EG) hist[threadIdx.x] = 0;
-  extern __shared__ __align__(16) uint8_t smem_r2[];
-  float* ws = reinterpret_cast<float*>(smem_r2);
-  const int e0 = blockIdx.y * EG;
-  // stage Wg[:, e0:e0+EG] as fp32: one 16-byte load = 8 experts of one row (E % 8 == 0)
-  constexpr int kVec = EG / 8;
-  for (int idx = threadIdx.x; idx < d * kVec; idx += blockDim.x) {
-    const int i = idx / kVec, c = idx % kVec;
-    float* dst = ws + router2_row_off(i, EG) + c * 8;
-    if (e0 + c * 8 < E) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4*>(wg + static_cast<long>(i) * E + e0 + c * 8));
-      const uint16_t* h = reinterpret_cast<const uint16_t*>(&v);
-      reinterpret_cast<float4*>(dst)[0] = make_float4(bf16_to_f32(h[0]), bf16_to_f32(h[1]),
-                                                      bf16_to_f32(h[2]), bf16_to_f32(h[3]));
-      reinterpret_cast<float4*>(dst)[1] = make_float4(bf16_to_f32(h[4]), bf16_to_f32(h[5]),
-                                                      bf16_to_f32(h[6]), bf16_to_f32(h[7]));
-    } else {
-      reinterpret_cast<float4*>(dst)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-      reinterpret_cast<float4*>(dst)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+struct RouterShared {
+  uint64_t full[kRouterStages];
+  int is_last;
+  int scan_off[257];
+};
+
+// EGW experts per CTA group held by every warp (registers: BPW * 8 * EGW = 64 floats), BPW
+// blocks per warp (nj > 16). FUSE: one expert group (E <= EGW): top-k, softmax, the per-chunk
+// histogram (atomics into the zeroed chunk_counts) and, in the last CTA to finish, the scan.
+template <int EGW, int BPW, bool FUSE>
+__global__ void __launch_bounds__(kRouterThreads, 1)
+    router_fused_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+                        const float* __restrict__ bias, int T, int d, int E, int ranges,
+                        float* __restrict__ logits, int k, int32_t* __restrict__ idx,
+                        float* __restrict__ w, int32_t* __restrict__ chunk_counts /*[nchunk*E + 1]*/,
+                        int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
+  extern __shared__ __align__(1024) uint8_t smem_rt[];
+  uint8_t* ring = smem_rt;                                                  // stages x 32 KB
+  float* part = reinterpret_cast<float*>(smem_rt + kRouterStages * kRouterStageBytes);  // [2][64][EGW]
+  float* lg = part + 2 * kRouterItems * EGW;                                // [64][EGW] (FUSE)
+  RouterShared& sh = *reinterpret_cast<RouterShared*>(lg + kRouterItems * EGW);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = d >> 8;
+  const int TG = kRouterItems / nj;  // tokens per stage
+  const int group = blockIdx.x % (gridDim.x / ranges);
+  const int range = blockIdx.x / (gridDim.x / ranges);
+  const int e0 = group * EGW;
+  const long units = (T + TG - 1) / TG;
+  const int t_begin = static_cast<int>(units * range / ranges) * TG;
+  const int t_end = min(T, static_cast<int>(units * (range + 1) / ranges) * TG);
+  const int nst = t_end > t_begin ? (t_end - t_begin + TG - 1) / TG : 0;
+  const long row_bytes = static_cast<long>(d) * 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRouterStages; ++s) mbar_init(&sh.full[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < kRouterStages && s < nst; ++s) {
+      const int t0 = t_begin + s * TG;
+      const uint32_t bytes = static_cast<uint32_t>(min(TG, t_end - t0) * row_bytes);
+      mbar_arrive_expect_tx(&sh.full[s], bytes);
+      bulk_load_1d(ring + s * kRouterStageBytes, x + static_cast<long>(t0) * d, bytes, &sh.full[s]);
     }
   }
+  // this warp's blocks and token slots: nj <= 16 -> block w % nj, tokens w / nj + (16 / nj) m;
+  // nj > 16 -> blocks w + 16 b (b < BPW), every token of the stage
+  int jb[BPW];
+#pragma unroll
+  for (int b = 0; b < BPW; ++b) jb[b] = (nj <= 16) ? (warp % nj) : (warp + 16 * b);
+  const bool active = (nj <= 16) ? (warp < (16 / nj) * nj) : true;
+  float wr[BPW][8][EGW];
+#pragma unroll
+  for (int b = 0; b < BPW; ++b)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const long i = 256L * jb[b] + 8 * lane + q;
+#pragma unroll
+      for (int e = 0; e < EGW; ++e)
+        wr[b][q][e] = (e0 + e < E && jb[b] < nj) ? bf16_to_f32(reinterpret_cast<const uint16_t*>(wg)[i * E + e0 + e]) : 0.f;
+    }
+  const int my_e = router_lane_expert<EGW>(lane);
+  const bool writer = (lane & (32 / EGW - 1)) == 0;
   __syncthreads();
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nj = d / 256;
-  const int per_iter = NW * TT;
-  // every warp runs every CTA iteration (the fused histogram synchronises the CTA per chunk)
-  for (int base = blockIdx.x * per_iter; base < T; base += gridDim.x * per_iter) {
-    const int t0 = base + warp * TT;
-    float acc[TT][EG];
+  for (int s = 0; s < nst; ++s) {
+    const int slot = s % kRouterStages;
+    const int t0 = t_begin + s * TG;
+    const int nt = min(TG, t_end - t0);
+    float* pb = part + (s & 1) * kRouterItems * EGW;
+    mbar_wait(&sh.full[slot], (s / kRouterStages) & 1);
+    const uint8_t* st = ring + slot * kRouterStageBytes;
+    if (active) {
+      // 4 (token, block) items per warp
 #pragma unroll
-    for (int a = 0; a < TT; ++a)
+      for (int m = 0; m < 4; ++m) {
+        int ti, b;
+        if (nj <= 16) { ti = warp / nj + (16 / nj) * m; b = 0; } else { ti = m / BPW; b = m % BPW; }
+        if (ti < nt) {
+          const uint4 xv = *reinterpret_cast<const uint4*>(st + ti * row_bytes + (256L * jb[b] + 8 * lane) * 2);
+          const uint16_t* xh = reinterpret_cast<const uint16_t*>(&xv);
+          float acc[EGW];
 #pragma unroll
-      for (int e = 0; e < EG; ++e) acc[a][e] = 0.f;
-    uint4 xv[TT], xn[TT];
+          for (int e = 0; e < EGW; ++e) acc[e] = 0.f;
 #pragma unroll
-    for (int a = 0; a < TT; ++a) {
-      const int t = min(t0 + a, T - 1);
-      xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + lane * 8));
-    }
-    for (int j = 0; j < nj; ++j) {
-      const int ibase = j * 256 + lane * 8;
-      if (!PREFETCH && j > 0) {  // no look-ahead registers: other warps hide the latency
+          for (int q = 0; q < 8; ++q) {
+            const float xf = bf16_to_f32(xh[q]);
 #pragma unroll
-        for (int a = 0; a < TT; ++a) {
-          const int t = min(t0 + a, T - 1);
-          xv[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase));
-        }
-      }
-      if (PREFETCH && j + 1 < nj) {
-#pragma unroll
-        for (int a = 0; a < TT; ++a) {
-          const int t = min(t0 + a, T - 1);
-          xn[a] = __ldg(reinterpret_cast<const uint4*>(x + static_cast<long>(t) * d + ibase + 256));
-        }
-      }
-      const float* wrow0 = ws + router2_row_off(ibase, EG);  // rows ibase..ibase+7: one 8-row group
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float wv[EG];
-#pragma unroll
-        for (int e = 0; e < EG; e += 4) {
-          const float4 w4 = *reinterpret_cast<const float4*>(wrow0 + q * EG + e);
-          wv[e] = w4.x; wv[e + 1] = w4.y; wv[e + 2] = w4.z; wv[e + 3] = w4.w;
-        }
-#pragma unroll
-        for (int a = 0; a < TT; ++a) {
-          const float xf = bf16_to_f32(reinterpret_cast<const uint16_t*>(&xv[a])[q]);
-          // packed fp32x2 FMAs (FFMA2): two independent IEEE fma.rn per instruction, so every
-          // accumulator sees exactly the scalar sequence (bit-identical logits)
-#pragma unroll
-          for (int e = 0; e < EG; e += 2) {
-            const float2 r = __ffma2_rn(make_float2(xf, xf), make_float2(wv[e], wv[e + 1]),
-                                        make_float2(acc[a][e], acc[a][e + 1]));
-            acc[a][e] = r.x;
-            acc[a][e + 1] = r.y;
+            for (int e = 0; e < EGW; e += 2) {
+              const float2 r = __ffma2_rn(make_float2(xf, xf), make_float2(wr[b][q][e], wr[b][q][e + 1]),
+                                          make_float2(acc[e], acc[e + 1]));
+              acc[e] = r.x;
+              acc[e + 1] = r.y;
+            }
           }
+          const float pj = router_reduce_scatter<EGW>(acc, lane);
+          if (writer) pb[(ti * nj + jb[b]) * EGW + my_e] = pj;
         }
-      }
-      if (PREFETCH) {
-#pragma unroll
-        for (int a = 0; a < TT; ++a) xv[a] = xn[a];
       }
     }
-#pragma unroll
-    for (int a = 0; a < TT; ++a)
-#pragma unroll
-      for (int e = 0; e < EG; ++e) {
-        float v = acc[a][e];
-        v = v + __shfl_xor_sync(0xffffffffu, v, 16);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 8);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 4);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 2);
-        v = v + __shfl_xor_sync(0xffffffffu, v, 1);
-        acc[a][e] = v;
-      }
-    // every lane holds every sum; lane (a * EG + e) % 32 writes
-#pragma unroll
-    for (int a = 0; a < TT; ++a) {
-      const int t = t0 + a;
-#pragma unroll
-      for (int e = 0; e < EG; ++e) {
-        if (bias) acc[a][e] = acc[a][e] + bias[e0 + e];
-        if (lane == ((a * EG + e) & 31) && t < T && e0 + e < E) logits[static_cast<long>(t) * E + e0 + e] = acc[a][e];
-      }
+    __syncthreads();
+    if (threadIdx.x == 0 && s + kRouterStages < nst) {  // refill the slot every warp just read
+      const int tn = t_begin + (s + kRouterStages) * TG;
+      const uint32_t bytes = static_cast<uint32_t>(min(TG, t_end - tn) * row_bytes);
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&sh.full[slot], bytes);
+      bulk_load_1d(ring + slot * kRouterStageBytes, x + static_cast<long>(tn) * d, bytes, &sh.full[slot]);
     }
-    if (FUSE) {
-      // lane a < TT selects for token t0 + a (the same comparisons as router_topk_kernel:
-      // strict >, ties -> lower expert id, NaN never selected, all-NaN -> lowest unselected id)
+    // block partials -> logits, in block order (+ bias); thread (ti, e)
+    if (threadIdx.x < TG * EGW) {
+      const int ti = threadIdx.x / EGW, e = threadIdx.x % EGW;
+      if (ti < nt && e0 + e < E) {
+        float v = pb[(ti * nj) * EGW + e];
+        for (int j = 1; j < nj; ++j) v = v + pb[(ti * nj + j) * EGW + e];
+        if (bias) v = v + bias[e0 + e];
+        logits[static_cast<long>(t0 + ti) * E + e0 + e] = v;
+        if (FUSE) lg[ti * EGW + e] = v;
+      }
+      if (FUSE) {
+        // a token's EGW threads are consecutive lanes of one warp (TG * EGW < 32: warp 0's low lanes)
+        __syncwarp(TG * EGW >= 32 ? 0xffffffffu : ((1u << (TG * EGW)) - 1u));
+        if (e == 0 && ti < nt) {
+          float v[EGW];
 #pragma unroll
-      for (int a = 0; a < TT; ++a) {
-        const int t = t0 + a;
-        if (lane != a || t >= T) continue;
-        float v[EG];
-#pragma unroll
-        for (int e = 0; e < EG; ++e) v[e] = acc[a][e];
-        float sel_l[kMaxTopK];
-        int sel_e[kMaxTopK];
-        for (int s2 = 0; s2 < k; ++s2) {
-          float bv = -INFINITY;
-          int be = 0x7fffffff;
-#pragma unroll
-          for (int e = 0; e < EG; ++e)
-            if (v[e] > bv || (v[e] == bv && e < be)) { bv = v[e]; be = e; }
-          if (be == 0x7fffffff) {  // every unselected logit is NaN: lowest unselected id
-            be = 0;
-            bv = kSelectedMark;
-            for (int q2 = 0; q2 < s2; ++q2)
-              if (sel_e[q2] == be) { ++be; q2 = -1; }
-          }
-          sel_l[s2] = bv;
-          sel_e[s2] = be;
-#pragma unroll
-          for (int e = 0; e < EG; ++e)
-            if (e == be) v[e] = kSelectedMark;
-        }
-        float ex[kMaxTopK];
-        float sum = 0.f;
-        for (int s2 = 0; s2 < k; ++s2) { ex[s2] = expf(sel_l[s2] - sel_l[0]); sum += ex[s2]; }
-        for (int s2 = 0; s2 < k; ++s2) {
-          idx[static_cast<long>(t) * k + s2] = sel_e[s2];
-          w[static_cast<long>(t) * k + s2] = ex[s2] / sum;
-          atomicAdd(&hist[sel_e[s2]], 1);
+          for (int q = 0; q < EGW; ++q) v[q] = lg[ti * EGW + q];
+          const long t = t0 + ti;
+          router_select<EGW>(v, E, k, idx + t * k, w + t * k, chunk_counts + (t / kChunk) * E);
         }
       }
-      __syncthreads();
-      if (threadIdx.x < EG) {
-        chunk_counts[static_cast<long>(base / kChunk) * E + threadIdx.x] = hist[threadIdx.x];
-        hist[threadIdx.x] = 0;
-      }
-      __syncthreads();
     }
   }
+  if (FUSE) {
+    // the last CTA to finish turns the per-chunk counts into totals, offsets and chunk bases
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int nchunk = (T + kChunk - 1) / kChunk;
+      const int prev = atomicAdd(chunk_counts + static_cast<long>(nchunk) * E, 1);
+      sh.is_last = (prev == static_cast<int>(gridDim.x) - 1);
+    }
+    __syncthreads();
+    if (sh.is_last) {
+      __threadfence();
+      const int nchunk = (T + kChunk - 1) / kChunk;
+      router_scan_block(chunk_counts, nchunk, E, counts, offsets, reinterpret_cast<int*>(ring), sh.scan_off);
+    }
+  }
+}
+
+constexpr size_t router_fused_smem_bytes(int egw) {
+  return static_cast<size_t>(kRouterStages) * kRouterStageBytes + 3 * kRouterItems * egw * 4 +
+         sizeof(RouterShared) + 16;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -434,61 +454,13 @@ __global__ void __launch_bounds__(kChunk)
 }
 
 // ------------------------------------------------------------------------------------------
-// K1c: counts / offsets / chunk bases. Single CTA of 1024 threads; warp w owns experts
-// w, w+32, ...: (1) per-expert totals with warp reductions over the chunks, (2) exclusive scan
-// over experts, (3) per-expert exclusive scans over chunks (warp shuffles, 32 chunks per step).
+// K1c: counts / offsets / chunk bases (the unfused router path). Single CTA of 1024 threads.
 __global__ void __launch_bounds__(1024)
     router_scan_kernel(int32_t* __restrict__ chunk_counts /*in: counts, out: bases*/, int nchunk,
                        int E, int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
-  // thread (g, e): chunk group g of G = blockDim / Epad, expert e; loads are coalesced over e
-  __shared__ int part[1024];  // [G][Epad] partial sums, then exclusive prefixes over g
+  __shared__ int part[1024];
   __shared__ int off[257];
-  int epad = 1;
-  while (epad < E) epad <<= 1;
-  const int G = blockDim.x / epad;
-  const int g = threadIdx.x / epad, e = threadIdx.x % epad;
-  const int c_lo = static_cast<int>((static_cast<long>(nchunk) * g) / G);
-  const int c_hi = static_cast<int>((static_cast<long>(nchunk) * (g + 1)) / G);
-  int s = 0;
-  if (e < E && g < G) {
-#pragma unroll 8
-    for (int c = c_lo; c < c_hi; ++c) s += chunk_counts[static_cast<long>(c) * E + e];
-  }
-  part[threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.x < epad) {  // exclusive prefix over the chunk groups of expert e = threadIdx.x
-    int a = 0;
-    for (int gg = 0; gg < G; ++gg) {
-      const int v = part[gg * epad + threadIdx.x];
-      part[gg * epad + threadIdx.x] = a;
-      a += v;
-    }
-    if (threadIdx.x < E) off[threadIdx.x] = a;  // expert total, scanned below
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int a = 0;
-    for (int i = 0; i < E; ++i) {
-      const int t = off[i];
-      off[i] = a;
-      counts[i] = t;
-      offsets[i] = a;
-      a += t;
-    }
-    off[E] = a;
-    offsets[E] = a;
-  }
-  __syncthreads();
-  if (e < E && g < G) {
-    int base = off[e] + part[threadIdx.x];
-#pragma unroll 8
-    for (int c = c_lo; c < c_hi; ++c) {
-      int32_t* p = chunk_counts + static_cast<long>(c) * E + e;
-      const int v = *p;
-      *p = base;
-      base += v;
-    }
-  }
+  router_scan_block(chunk_counts, nchunk, E, counts, offsets, part, off);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -122,12 +122,7 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, bias: torch.Tensor | 
     )
     _end(_tk)
     _native.check(rc, "hm_router_topk")
-    # launches (mirrors hm_router_topk's dispatch): one expert group -> logits+top-k fused, scan
-    eg = 8 if E == 8 else 16
-    fused = (E % 8 == 0 and E <= 16 and wg.data_ptr() % 16 == 0
-             and d * eg * 4 + (d // 8) * 16 <= 200 * 1024
-             and not os.environ.get("HM_ROUTER_V1") and not os.environ.get("HM_ROUTER_UNFUSED"))
-    _count(0 if T == 0 else (2 if fused else 3))
+    _count(lib.hm_router_launches(T, d, E))
     return Routing(idx, w, logits, counts, offsets, chunk_base)
 
 

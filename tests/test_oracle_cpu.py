@@ -20,21 +20,59 @@ def test_fixed_order_logits_close_to_exact_matmul():
     assert np.abs(lg - exact).max() < 1e-4
 
 
-def test_fixed_order_is_the_documented_lane_butterfly():
-    # brute-force restatement for one token: lane partials in (j, q) order, then xor butterfly
+def test_fixed_order_is_the_documented_blocked_butterfly():
+    # brute-force restatement for one token: per 256-block, lane partials in q order, then the
+    # xor butterfly; block partials added in block order
     rng = np.random.default_rng(0)
-    d, E = 512, 4
+    d, E = 768, 4
     x = torch.tensor(rng.standard_normal((1, d)), dtype=torch.float32).bfloat16().float().numpy()
     w = torch.tensor(rng.standard_normal((d, E)), dtype=torch.float32).bfloat16().float().numpy()
-    lanes = np.zeros((32, E), dtype=np.float32)
-    for lane in range(32):
-        for j in range(d // 256):
+    total = None
+    for j in range(d // 256):
+        lanes = np.zeros((32, E), dtype=np.float32)
+        for lane in range(32):
             for q in range(8):
                 i = 256 * j + 8 * lane + q
                 lanes[lane] = (lanes[lane] + np.float32(x[0, i]) * w[i]).astype(np.float32)
-    for off in (16, 8, 4, 2, 1):
-        lanes = (lanes + lanes[np.arange(32) ^ off]).astype(np.float32)
-    assert np.array_equal(lanes[0], orc.router_logits(x, w)[0])
+        for off in (16, 8, 4, 2, 1):
+            lanes = (lanes + lanes[np.arange(32) ^ off]).astype(np.float32)
+        total = lanes[0] if total is None else (total + lanes[0]).astype(np.float32)
+    assert np.array_equal(total, orc.router_logits(x, w)[0])
+
+
+def test_reduce_scatter_butterfly_equals_full_butterfly():
+    """The kernel reduces a warp's EGW lane partials with a reduce-scatter butterfly (halving the
+    vector at offsets 16, 8, ...; then plain xor steps): the same pairwise tree per expert as the
+    full butterfly, so the same bits (fp32 addition is commutative)."""
+    rng = np.random.default_rng(5)
+    for egw in (8, 4, 2):
+        v = rng.standard_normal((32, egw)).astype(np.float32) * np.float32(1e3) ** rng.integers(-2, 3, (32, egw))
+        v = v.astype(np.float32)
+        full = v.copy()
+        for off in (16, 8, 4, 2, 1):
+            full = (full + full[np.arange(32) ^ off]).astype(np.float32)
+        cur = [list(v[L]) for L in range(32)]
+        off, h = 16, egw // 2
+        while h >= 1:
+            nxt = []
+            for L in range(32):
+                up = bool(L & off)
+                keep = [cur[L][m + h] if up else cur[L][m] for m in range(h)]
+                P = L ^ off
+                send = [cur[P][m] if bool(P & off) else cur[P][m + h] for m in range(h)]
+                nxt.append([np.float32(keep[m] + send[m]) for m in range(h)])
+            cur, off, h = nxt, off // 2, h // 2
+        r = [np.float32(c[0]) for c in cur]
+        o = off
+        while o >= 1:
+            r = [np.float32(r[L] + r[L ^ o]) for L in range(32)]
+            o //= 2
+        for L in range(32):
+            e, oo, hh = 0, 16, egw // 2
+            while hh >= 1:
+                e += hh if L & oo else 0
+                oo, hh = oo // 2, hh // 2
+            assert r[L].view(np.uint32) == full[L, e].view(np.uint32), (egw, L, e)
 
 
 def test_topk_ties_go_to_lower_expert_and_softmax_normalises():

@@ -145,3 +145,38 @@ def test_moe_layer_with_empty_expert_vs_oracle():
     bias = [0.0] * 8
     bias[3] = -30.0
     _layer_vs_oracle(cfg, seed=33, expert_bias=bias, check_empty=3)
+
+
+@pytest.mark.parametrize("cfg", [LayerConfig("E8d4096", 8, 2, 4096, 128, 1000),
+                                 LayerConfig("E4d256", 4, 3, 256, 128, 777),
+                                 LayerConfig("E8d8192", 8, 2, 8192, 128, 300),
+                                 LayerConfig("E2d16384", 2, 1, 16384, 128, 130)],
+                         ids=lambda c: c.name)
+def test_router_fused_equals_unfused_and_oracle(cfg):
+    """The one-kernel router (logits + top-k + histogram + last-CTA scan, one expert group) and
+    the unfused path (logits kernel, top-k kernel, scan kernel; HM_ROUTER_UNFUSED) agree bitwise,
+    and both match the oracle, on adversarial rows too; d = 8192 / 16384 exercise the 4- and
+    2-expert register groups."""
+    import os
+
+    inp = make_inputs(cfg, seed=17)
+    x = _adversarial_x(inp.x).cuda()
+    wg = inp.wg.cuda()
+    a = ops.router_topk(x, wg, cfg.k)
+    os.environ["HM_ROUTER_UNFUSED"] = "1"
+    try:
+        b = ops.router_topk(x, wg, cfg.k)
+    finally:
+        os.environ.pop("HM_ROUTER_UNFUSED")
+    torch.cuda.synchronize()
+    n = ((cfg.T + 63) // 64) * cfg.E
+    for name in ("idx", "counts", "offsets"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    assert torch.equal(a.chunk_base[:n], b.chunk_base[:n])
+    assert _same_float(a.logits.cpu().numpy(), b.logits.cpu().numpy())
+    assert _same_float(a.w.cpu().numpy(), b.w.cpu().numpy())
+    ref = orc.route(x.cpu().float().numpy(), inp.wg.float().numpy(), cfg.k)
+    assert _same_float(a.logits.cpu().numpy(), ref.logits)
+    assert np.array_equal(a.idx.cpu().numpy(), ref.idx)
+    assert np.array_equal(a.offsets.cpu().numpy(), ref.offsets)
+    np.testing.assert_allclose(a.w.cpu().numpy(), ref.w, rtol=0, atol=TOL_GATE)

@@ -17,7 +17,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-TOL_STACK = 3e-2  # relative Frobenius error of every weight gradient vs the fp32 stack
+TOL_STACK = 2e-2  # relative Frobenius error of every weight gradient vs the fp32 stack (measured <= 0.9e-2 on 2 GPUs)
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 

@@ -372,11 +372,11 @@ size_t hm_router_chunk_elems(int T, int E) {
 
 }  // extern "C"
 
-template <int EGW, int BPW, bool FUSE>
+template <int EGW, int NJ, bool FUSE>
 static int launch_router_fused(int groups, cudaStream_t st, const __nv_bfloat16* xb, const __nv_bfloat16* wb,
-                               const float* bias, int T, int d, int E, float* logits, int k, int32_t* idx,
+                               const float* bias, int T, int E, float* logits, int k, int32_t* idx,
                                float* w, int32_t* chunk_base, int32_t* counts, int32_t* offsets) {
-  auto kern = hm::router_fused_kernel<EGW, BPW, FUSE>;
+  auto kern = hm::router_fused_kernel<EGW, NJ, FUSE>;
   const size_t smem = hm::router_fused_smem_bytes(EGW);
   static bool attr = false;
   if (!attr) {
@@ -384,14 +384,36 @@ static int launch_router_fused(int groups, cudaStream_t st, const __nv_bfloat16*
     if (e != cudaSuccess) return fail(static_cast<int>(e), "router smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  const int TG = hm::kRouterItems / (d / 256);
+  const int TG = hm::kRouterItems / NJ;
   const int units = (T + TG - 1) / TG;
   int ranges = num_sms() / groups;  // one persistent CTA per SM over all (range, group) pairs
   if (ranges < 1) ranges = 1;
   if (ranges > units) ranges = units;
-  kern<<<ranges * groups, hm::kRouterThreads, smem, st>>>(xb, wb, bias, T, d, E, ranges, logits, k, idx, w,
+  kern<<<ranges * groups, hm::kRouterThreads, smem, st>>>(xb, wb, bias, T, E, ranges, logits, k, idx, w,
                                                           chunk_base, counts, offsets);
   return check_launch("router_fused");
+}
+
+template <bool FUSE>
+static int launch_router_nj(int d, int groups, cudaStream_t st, const __nv_bfloat16* xb, const __nv_bfloat16* wb,
+                            const float* bias, int T, int E, float* logits, int k, int32_t* idx, float* w,
+                            int32_t* chunk_base, int32_t* counts, int32_t* offsets) {
+#define HM_ROUTER_NJ(EGW, NJ)                                                                   \
+  case NJ:                                                                                    \
+    return launch_router_fused<EGW, NJ, FUSE>(groups, st, xb, wb, bias, T, E, logits, k, idx, w, \
+                                              chunk_base, counts, offsets);
+  switch (d / 256) {
+    HM_ROUTER_NJ(8, 1)
+    HM_ROUTER_NJ(8, 2)
+    HM_ROUTER_NJ(8, 4)
+    HM_ROUTER_NJ(8, 8)
+    HM_ROUTER_NJ(8, 16)
+    HM_ROUTER_NJ(4, 32)
+    HM_ROUTER_NJ(2, 64)
+    default:
+      return fail(HM_E_SHAPE, "router: d=%d", d);
+  }
+#undef HM_ROUTER_NJ
 }
 
 extern "C" {
@@ -417,15 +439,11 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
     // logits, top-k, softmax, chunk histogram and scan in one kernel (the histogram accumulates
     // with atomics into the zeroed chunk table; the last CTA scans it)
     cudaMemsetAsync(chunk_base, 0, sizeof(int32_t) * hm_router_chunk_elems(T, E), st);
-    if (egw == 8) return launch_router_fused<8, 1, true>(1, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets);
-    if (egw == 4) return launch_router_fused<4, 2, true>(1, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets);
-    return launch_router_fused<2, 4, true>(1, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets);
+    return launch_router_nj<true>(d, 1, st, xb, wb, bias, T, E, logits, k, idx, w, chunk_base, counts, offsets);
   }
-  int rc;
-  if (egw == 8) rc = launch_router_fused<8, 1, false>(groups, st, xb, wb, bias, T, d, E, logits, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
-  else if (egw == 4) rc = launch_router_fused<4, 2, false>(groups, st, xb, wb, bias, T, d, E, logits, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
-  else rc = launch_router_fused<2, 4, false>(groups, st, xb, wb, bias, T, d, E, logits, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
-  if (rc) return rc;
+  if (int rc = launch_router_nj<false>(d, groups, st, xb, wb, bias, T, E, logits, 0, nullptr, nullptr, nullptr,
+                                       nullptr, nullptr))
+    return rc;
   launch_router_topk(nchunk, st, logits, T, E, k, idx, w, chunk_base);
   if (int rc2 = check_launch("router_topk")) return rc2;
   hm::router_scan_kernel<<<1, 1024, 0, st>>>(chunk_base, nchunk, E, counts, offsets);

@@ -33,45 +33,77 @@ constexpr int kMaxTopK = 8;
 
 // ------------------------------------------------------------------------------------------
 // K1a: router logits (+ fused top-k, softmax, chunk histogram and scan when the experts form one
-// group). Persistent: one CTA of 16 warps per SM (per expert group), each over a contiguous
-// token range. Token rows stream into a shared-memory ring by 1-D bulk copies (TMA engine;
-// 32 KB stages of 64 / nj tokens, nj = d / 256 blocks). The router weight never touches shared
-// memory: warp w owns block(s) j and keeps Wg[256 j + 8 L + q, e0 .. e0 + EGW) in registers
-// (lane L, q = 0..7: 8 x EGW fp32). Per (token, block) item a lane does 8 x EGW FMAs (packed
-// FFMA2: two IEEE fma.rn per instruction, the scalar per-accumulator sequence) and the warp
-// reduces its EGW lane partials with a reduce-scatter butterfly (offsets 16, 8, ... halving the
-// vector; then the plain xor steps): log2(EGW) + (5 - log2(EGW)) shuffle rounds of
-// EGW/2 + ... + 1 values — 9 shuffles for EGW = 8 instead of 40 — and, because fp32 addition is
-// commutative, every expert's value is the same tree as the full butterfly's. The block partials
-// go to shared memory and 8 x TG threads add them in block order (+ bias).
-constexpr int kRouterThreads = 512;
-constexpr int kRouterStages = 4;
+// group). Persistent: one CTA per SM (per expert group), each over a contiguous token range.
+// Warp specialised: warps 0..15 compute, warps 16..19 are epilogue + producer (a rotating epilogue
+// run by the compute warps themselves measured 1.6x slower: its top-k stalls the whole stage).
+//  * token rows stream into a 4-stage shared-memory ring by 1-D bulk copies (TMA engine; 32 KB
+//    stages of TG = 64 / nj tokens, nj = d / 256 blocks), issued by the epilogue that frees the slot;
+//  * the router weight never touches shared memory: compute warp w owns block(s) j and keeps
+//    Wg[256 j + 8 L + q, e0 .. e0 + EGW) in registers (lane L, q = 0..7: 8 x EGW fp32, in a
+//    lane-dependent XOR order of the experts). Per (token, block) item a lane does 8 x EGW FMAs
+//    (packed FFMA2: two IEEE fma.rn per instruction, the scalar per-accumulator sequence); the
+//    warp reduces its EGW lane partials with a select-free reduce-scatter butterfly (offsets
+//    16, 8, ... halving the vector, then plain xor steps: 9 shuffles for EGW = 8 instead of 40 —
+//    and, fp32 addition being commutative, every expert's value is the full butterfly's tree);
+//    two items are reduced together so their shuffle latencies overlap; block partials go to a
+//    4-deep shared-memory table ring;
+//  * epilogue warp 16 + s % 4 adds stage s's block partials in block order (+ bias) into logits,
+//    runs the top-k / softmax on the logits still in registers as lane-parallel butterfly
+//    argmaxes (FUSE), counts the chunk histogram with atomics, and refills the ring slot the
+//    compute warps just released.
+// mbarriers: full[slot] (bytes landed), pfull[slot] (16 compute warps wrote partial table slot),
+// pempty[slot] (its epilogue warp consumed it). The last CTA to finish scans the per-chunk
+// counts (FUSE).
+constexpr int kRouterWarps = 16;     // compute warps
+constexpr int kRouterEpiWarps = 4;   // epilogue warps: 20 warps take the register budget of 17
+constexpr int kRouterThreads = (kRouterWarps + kRouterEpiWarps) * 32;
+constexpr int kRouterStages = 4;     // ring slots == partial tables == epilogue warps
+constexpr int kRouterNI = 2;         // items reduced together (shuffle ILP within 96 registers)
 constexpr int kRouterStageBytes = 32768;  // 64 (token, block) items of 512 bytes
 constexpr int kRouterItems = 64;
 
-// reduce-scatter butterfly of EGW values over the 32 lanes; returns the value of expert
-// router_lane_expert<EGW>(lane), identical on the 32 / EGW lanes that share it
-template <int EGW>
-HM_DEV float router_reduce_scatter(const float (&v)[EGW], int lane) {
-  float cur[EGW];
+// Reduce-scatter butterfly of EGW values for NI items at once (shuffles interleaved). The values
+// are in the lane's XOR-permuted expert order (slot r = expert r ^ router_lane_expert(lane);
+// router_permute_slots), so at every halving level a lane keeps its low half and sends its high
+// half with no selects: its partner (lane ^ off) holds the same experts in the opposite halves.
+// Returns in out[i] the value of expert router_lane_expert<EGW>(lane) of item i, identical on
+// the 32 / EGW lanes that share it.
+template <int EGW, int NI>
+HM_DEV void router_reduce_scatter(float (&v)[NI][EGW], float (&out)[NI]) {
+  int off = 16;
 #pragma unroll
-  for (int e = 0; e < EGW; ++e) cur[e] = v[e];
+  for (int h = EGW / 2; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int m = 0; m < h; ++m)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) v[i][m] = v[i][m] + __shfl_xor_sync(0xffffffffu, v[i][m + h], off);
+    off >>= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < NI; ++i) out[i] = v[i][0];
+#pragma unroll
+  for (int o = 32 / EGW / 2; o >= 1; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < NI; ++i) out[i] = out[i] + __shfl_xor_sync(0xffffffffu, out[i], o);
+}
+
+// Natural expert order -> the lane's XOR-permuted order (slot r <- expert r ^ mask, mask =
+// router_lane_expert(lane)): one conditional half swap per halving level.
+template <int EGW>
+HM_DEV void router_permute_slots(float (&w)[EGW], int lane) {
   int off = 16;
 #pragma unroll
   for (int h = EGW / 2; h >= 1; h >>= 1) {
     const bool up = (lane & off) != 0;
 #pragma unroll
-    for (int m = 0; m < h; ++m) {
-      const float keep = up ? cur[m + h] : cur[m];
-      const float send = up ? cur[m] : cur[m + h];
-      cur[m] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
+    for (int m = 0; m < EGW; ++m)
+      if ((m & h) == 0) {
+        const float a = w[m], c = w[m + h];
+        w[m] = up ? c : a;
+        w[m + h] = up ? a : c;
+      }
     off >>= 1;
   }
-  float r = cur[0];
-#pragma unroll
-  for (int o = 32 / EGW / 2; o >= 1; o >>= 1) r = r + __shfl_xor_sync(0xffffffffu, r, o);
-  return r;
 }
 
 template <int EGW>
@@ -175,131 +207,240 @@ HM_DEV void router_select(float (&v)[EP], int E, int k, int32_t* idx_out, float*
 
 struct RouterShared {
   uint64_t full[kRouterStages];
+  uint64_t pfull[kRouterStages];
+  uint64_t pempty[kRouterStages];
   int is_last;
   int scan_off[257];
 };
 
-// EGW experts per CTA group held by every warp (registers: BPW * 8 * EGW = 64 floats), BPW
-// blocks per warp (nj > 16). FUSE: one expert group (E <= EGW): top-k, softmax, the per-chunk
-// histogram (atomics into the zeroed chunk_counts) and, in the last CTA to finish, the scan.
-template <int EGW, int BPW, bool FUSE>
+// Top-k of one token whose EGW logits sit in EGW consecutive lanes (lane e of the group holds
+// expert e; e >= E is no expert): k rounds of a lexicographic (value desc, id asc) butterfly
+// argmax over the group with NaN never eligible — the comparator of the sequential scan
+// (router_select), so the same experts in the same order — the winner marked NaN, the
+// all-NaN fallback to the lowest unselected id; then the softmax over the selected logits
+// (sequential sum in slot order). Lane e == s writes slot s and counts it in the histogram.
+template <int EGW>
+HM_DEV void router_select_lanes(float v, int e, int E, int k, bool write, int32_t* idx_out, float* w_out,
+                                int32_t* hist_row) {
+  float cur = (e < E) ? v : kSelectedMark;
+  float sel_l[kMaxTopK];
+  int sel_e[kMaxTopK];
+  unsigned taken = 0u;
+#pragma unroll
+  for (int s = 0; s < kMaxTopK; ++s) {
+    if (s < k) {
+      const bool ok = (e < E) && !isnan(cur);
+      float bv = ok ? cur : -INFINITY;
+      int be = ok ? e : 0x7fffffff;
+#pragma unroll
+      for (int off = 1; off < EGW; off <<= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oe = __shfl_xor_sync(0xffffffffu, be, off);
+        if (ov > bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+      }
+      if (be == 0x7fffffff) {  // every unselected logit is NaN: lowest unselected id
+        be = __ffs(~taken) - 1;
+        bv = kSelectedMark;
+      }
+      taken |= 1u << be;
+      sel_l[s] = bv;
+      sel_e[s] = be;
+      if (e == be) cur = kSelectedMark;
+    }
+  }
+  float ex[kMaxTopK];
+  float sum = 0.f;
+#pragma unroll
+  for (int s = 0; s < kMaxTopK; ++s)
+    if (s < k) { ex[s] = expf(sel_l[s] - sel_l[0]); sum += ex[s]; }
+#pragma unroll
+  for (int s = 0; s < kMaxTopK; ++s)
+    if (s < k && e == s && write) {
+      idx_out[s] = sel_e[s];
+      w_out[s] = ex[s] / sum;
+      atomicAdd(hist_row + sel_e[s], 1);
+    }
+}
+
+// EGW experts per CTA group held by every warp (registers: BPW * 8 * EGW = 64 floats), NJ =
+// d / 256 blocks (compile time: every index is a shift), BPW = max(1, NJ / 16) blocks per warp.
+// FUSE: one expert group (E <= EGW): top-k, softmax, the per-chunk histogram (atomics into the
+// zeroed chunk_counts) and, in the last CTA, the scan.
+template <int EGW, int NJ, bool FUSE>
 __global__ void __launch_bounds__(kRouterThreads, 1)
     router_fused_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                        const float* __restrict__ bias, int T, int d, int E, int ranges,
+                        const float* __restrict__ bias, int T, int E, int ranges,
                         float* __restrict__ logits, int k, int32_t* __restrict__ idx,
                         float* __restrict__ w, int32_t* __restrict__ chunk_counts /*[nchunk*E + 1]*/,
                         int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
+  constexpr int BPW = NJ > 16 ? NJ / 16 : 1;
+  constexpr int TG = kRouterItems / NJ;  // tokens per stage
+  constexpr int D = NJ * 256;
+  constexpr long kRowBytes = static_cast<long>(D) * 2;
+  constexpr int kRounds = (TG * EGW + 31) / 32;  // epilogue lane rounds per stage
+  static_assert(BPW * 8 * EGW <= 64, "router weights per thread");
   extern __shared__ __align__(1024) uint8_t smem_rt[];
   uint8_t* ring = smem_rt;                                                  // stages x 32 KB
-  float* part = reinterpret_cast<float*>(smem_rt + kRouterStages * kRouterStageBytes);  // [2][64][EGW]
-  float* lg = part + 2 * kRouterItems * EGW;                                // [64][EGW] (FUSE)
-  RouterShared& sh = *reinterpret_cast<RouterShared*>(lg + kRouterItems * EGW);
+  float* part = reinterpret_cast<float*>(smem_rt + kRouterStages * kRouterStageBytes);  // [4][64][EGW]
+  RouterShared& sh = *reinterpret_cast<RouterShared*>(part + kRouterStages * kRouterItems * EGW);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nj = d >> 8;
-  const int TG = kRouterItems / nj;  // tokens per stage
-  const int group = blockIdx.x % (gridDim.x / ranges);
-  const int range = blockIdx.x / (gridDim.x / ranges);
+  const int groups = gridDim.x / ranges;
+  const int group = blockIdx.x % groups;
+  const int range = blockIdx.x / groups;
   const int e0 = group * EGW;
   const long units = (T + TG - 1) / TG;
   const int t_begin = static_cast<int>(units * range / ranges) * TG;
   const int t_end = min(T, static_cast<int>(units * (range + 1) / ranges) * TG);
   const int nst = t_end > t_begin ? (t_end - t_begin + TG - 1) / TG : 0;
-  const long row_bytes = static_cast<long>(d) * 2;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRouterStages; ++s) mbar_init(&sh.full[s], 1);
+    for (int s = 0; s < kRouterStages; ++s) {
+      mbar_init(&sh.full[s], 1);
+      mbar_init(&sh.pfull[s], kRouterWarps);
+      mbar_init(&sh.pempty[s], 1);
+    }
     fence_barrier_init();
     for (int s = 0; s < kRouterStages && s < nst; ++s) {
       const int t0 = t_begin + s * TG;
-      const uint32_t bytes = static_cast<uint32_t>(min(TG, t_end - t0) * row_bytes);
+      const uint32_t bytes = static_cast<uint32_t>(min(TG, t_end - t0) * kRowBytes);
       mbar_arrive_expect_tx(&sh.full[s], bytes);
-      bulk_load_1d(ring + s * kRouterStageBytes, x + static_cast<long>(t0) * d, bytes, &sh.full[s]);
+      bulk_load_1d(ring + s * kRouterStageBytes, x + static_cast<long>(t0) * D, bytes, &sh.full[s]);
     }
   }
-  // this warp's blocks and token slots: nj <= 16 -> block w % nj, tokens w / nj + (16 / nj) m;
-  // nj > 16 -> blocks w + 16 b (b < BPW), every token of the stage
+  // this warp's blocks and items: NJ <= 16 -> block w % NJ, tokens w / NJ + (16 / NJ) m;
+  // NJ > 16 -> blocks w + 16 b (b < BPW), every token of the stage
   int jb[BPW];
 #pragma unroll
-  for (int b = 0; b < BPW; ++b) jb[b] = (nj <= 16) ? (warp % nj) : (warp + 16 * b);
-  const bool active = (nj <= 16) ? (warp < (16 / nj) * nj) : true;
+  for (int b = 0; b < BPW; ++b) jb[b] = (NJ <= 16) ? (warp % NJ) : (warp + 16 * b);
   float wr[BPW][8][EGW];
+  const uint16_t* wg16 = reinterpret_cast<const uint16_t*>(wg);
 #pragma unroll
   for (int b = 0; b < BPW; ++b)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const long i = 256L * jb[b] + 8 * lane + q;
+      if (warp >= kRouterWarps) {  // epilogue warps hold no weights
 #pragma unroll
-      for (int e = 0; e < EGW; ++e)
-        wr[b][q][e] = (e0 + e < E && jb[b] < nj) ? bf16_to_f32(reinterpret_cast<const uint16_t*>(wg)[i * E + e0 + e]) : 0.f;
+        for (int e = 0; e < EGW; ++e) wr[b][q][e] = 0.f;
+      } else if (E % EGW == 0) {  // the group's EGW weights of row i are one aligned vector
+        uint32_t u[EGW / 2];
+        if (EGW == 8) {
+          const uint4 t = __ldg(reinterpret_cast<const uint4*>(wg16 + i * E + e0));
+          u[0] = t.x; u[1 % (EGW / 2)] = t.y; u[2 % (EGW / 2)] = t.z; u[3 % (EGW / 2)] = t.w;
+        } else if (EGW == 4) {
+          const uint2 t = __ldg(reinterpret_cast<const uint2*>(wg16 + i * E + e0));
+          u[0] = t.x; u[1 % (EGW / 2)] = t.y;
+        } else {
+          u[0] = __ldg(reinterpret_cast<const uint32_t*>(wg16 + i * E + e0));
+        }
+#pragma unroll
+        for (int e = 0; e < EGW; e += 2) {
+          wr[b][q][e] = __uint_as_float(u[e / 2] << 16);
+          wr[b][q][e + 1] = __uint_as_float(u[e / 2] & 0xffff0000u);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EGW; ++e) wr[b][q][e] = (e0 + e < E) ? bf16_to_f32(wg16[i * E + e0 + e]) : 0.f;
+      }
+      router_permute_slots<EGW>(wr[b][q], lane);
     }
   const int my_e = router_lane_expert<EGW>(lane);
   const bool writer = (lane & (32 / EGW - 1)) == 0;
+  int ti_of[4], xoff[4], poff[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int b = (NJ <= 16) ? 0 : m % BPW;
+    ti_of[m] = (NJ <= 16) ? warp / NJ + (16 / NJ) * m : m / BPW;
+    xoff[m] = static_cast<int>(ti_of[m] * kRowBytes + (256 * jb[b] + 8 * lane) * 2);
+    poff[m] = (ti_of[m] * NJ + jb[b]) * EGW + my_e;
+  }
+  float bias_r[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int e = (r * 32 + lane) % EGW;
+    bias_r[r] = (bias && e0 + e < E) ? bias[e0 + e] : 0.f;
+  }
   __syncthreads();
 
-  for (int s = 0; s < nst; ++s) {
-    const int slot = s % kRouterStages;
-    const int t0 = t_begin + s * TG;
-    const int nt = min(TG, t_end - t0);
-    float* pb = part + (s & 1) * kRouterItems * EGW;
-    mbar_wait(&sh.full[slot], (s / kRouterStages) & 1);
-    const uint8_t* st = ring + slot * kRouterStageBytes;
-    if (active) {
-      // 4 (token, block) items per warp
+  if (warp < kRouterWarps) {
+    // ============ compute warps ============
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % kRouterStages;
+      const int nt = min(TG, t_end - (t_begin + s * TG));
+      float* pb = part + slot * kRouterItems * EGW;
+      mbar_wait(&sh.full[slot], (s / kRouterStages) & 1);
+      if (s >= kRouterStages) mbar_wait(&sh.pempty[slot], ((s / kRouterStages) - 1) & 1);
+      const uint8_t* st = ring + slot * kRouterStageBytes;
+      float acc[kRouterNI][EGW];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        int ti, b;
-        if (nj <= 16) { ti = warp / nj + (16 / nj) * m; b = 0; } else { ti = m / BPW; b = m % BPW; }
-        if (ti < nt) {
-          const uint4 xv = *reinterpret_cast<const uint4*>(st + ti * row_bytes + (256L * jb[b] + 8 * lane) * 2);
-          const uint16_t* xh = reinterpret_cast<const uint16_t*>(&xv);
-          float acc[EGW];
+      for (int m0 = 0; m0 < 4; m0 += kRouterNI) {
 #pragma unroll
-          for (int e = 0; e < EGW; ++e) acc[e] = 0.f;
+        for (int u = 0; u < kRouterNI; ++u) {
+          const int m = m0 + u;
+          const int b = (NJ <= 16) ? 0 : m % BPW;
+          // a token past the stage's end reads stale ring bytes; its result is never stored
+          const uint4 xv = *reinterpret_cast<const uint4*>(st + xoff[m]);
+          const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+          for (int e = 0; e < EGW; ++e) acc[u][e] = 0.f;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const float xf = bf16_to_f32(xh[q]);
+            const float xf = __uint_as_float((q & 1) ? (xw[q >> 1] & 0xffff0000u) : (xw[q >> 1] << 16));
 #pragma unroll
             for (int e = 0; e < EGW; e += 2) {
               const float2 r = __ffma2_rn(make_float2(xf, xf), make_float2(wr[b][q][e], wr[b][q][e + 1]),
-                                          make_float2(acc[e], acc[e + 1]));
-              acc[e] = r.x;
-              acc[e + 1] = r.y;
+                                          make_float2(acc[u][e], acc[u][e + 1]));
+              acc[u][e] = r.x;
+              acc[u][e + 1] = r.y;
             }
           }
-          const float pj = router_reduce_scatter<EGW>(acc, lane);
-          if (writer) pb[(ti * nj + jb[b]) * EGW + my_e] = pj;
         }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && s + kRouterStages < nst) {  // refill the slot every warp just read
-      const int tn = t_begin + (s + kRouterStages) * TG;
-      const uint32_t bytes = static_cast<uint32_t>(min(TG, t_end - tn) * row_bytes);
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&sh.full[slot], bytes);
-      bulk_load_1d(ring + slot * kRouterStageBytes, x + static_cast<long>(tn) * d, bytes, &sh.full[slot]);
-    }
-    // block partials -> logits, in block order (+ bias); thread (ti, e)
-    if (threadIdx.x < TG * EGW) {
-      const int ti = threadIdx.x / EGW, e = threadIdx.x % EGW;
-      if (ti < nt && e0 + e < E) {
-        float v = pb[(ti * nj) * EGW + e];
-        for (int j = 1; j < nj; ++j) v = v + pb[(ti * nj + j) * EGW + e];
-        if (bias) v = v + bias[e0 + e];
-        logits[static_cast<long>(t0 + ti) * E + e0 + e] = v;
-        if (FUSE) lg[ti * EGW + e] = v;
-      }
-      if (FUSE) {
-        // a token's EGW threads are consecutive lanes of one warp (TG * EGW < 32: warp 0's low lanes)
-        __syncwarp(TG * EGW >= 32 ? 0xffffffffu : ((1u << (TG * EGW)) - 1u));
-        if (e == 0 && ti < nt) {
-          float v[EGW];
+        float pj[kRouterNI];
+        router_reduce_scatter<EGW, kRouterNI>(acc, pj);
 #pragma unroll
-          for (int q = 0; q < EGW; ++q) v[q] = lg[ti * EGW + q];
-          const long t = t0 + ti;
-          router_select<EGW>(v, E, k, idx + t * k, w + t * k, chunk_counts + (t / kChunk) * E);
+        for (int u = 0; u < kRouterNI; ++u)
+          if (writer && ti_of[m0 + u] < nt) pb[poff[m0 + u]] = pj[u];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.pfull[slot]);  // releases this warp's ring reads and table writes
+    }
+  } else {
+    // ============ epilogue warps: stage s is warp 16 + s % 4's; it refills ring slot s % 4 ============
+    for (int s = warp - kRouterWarps; s < nst; s += kRouterEpiWarps) {
+      const int slot = s % kRouterStages;
+      const int t0 = t_begin + s * TG;
+      const int nt = min(TG, t_end - t0);
+      const float* pb = part + slot * kRouterItems * EGW;
+      mbar_wait(&sh.pfull[slot], (s / kRouterStages) & 1);
+      if (lane == 0 && s + kRouterStages < nst) {  // every compute warp is done with this slot
+        const int tn = t_begin + (s + kRouterStages) * TG;
+        const uint32_t bytes = static_cast<uint32_t>(min(TG, t_end - tn) * kRowBytes);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&sh.full[slot], bytes);
+        bulk_load_1d(ring + slot * kRouterStageBytes, x + static_cast<long>(tn) * D, bytes, &sh.full[slot]);
+      }
+      // block partials -> logits in block order (+ bias): lane (ti, e), e fastest
+#pragma unroll
+      for (int r = 0; r < kRounds; ++r) {
+        const int id = r * 32 + lane;
+        const int ti = id / EGW, e = id % EGW;
+        const int tl = id < TG * EGW ? ti : 0;  // lanes past the stage's items read item 0
+        float pv[NJ];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) pv[j] = pb[(tl * NJ + j) * EGW + e];
+        float v = pv[0];
+#pragma unroll
+        for (int j = 1; j < NJ; ++j) v = v + pv[j];
+        if (bias) v = v + bias_r[r];
+        const bool ok = id < TG * EGW && ti < nt;
+        if (ok && e0 + e < E) logits[static_cast<long>(t0 + ti) * E + e0 + e] = v;
+        if (FUSE) {
+          const long t = t0 + (ok ? ti : 0);
+          router_select_lanes<EGW>(v, e, E, k, ok, idx + t * k, w + t * k, chunk_counts + (t / kChunk) * E);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.pempty[slot]);
     }
   }
   if (FUSE) {
@@ -321,7 +462,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
 }
 
 constexpr size_t router_fused_smem_bytes(int egw) {
-  return static_cast<size_t>(kRouterStages) * kRouterStageBytes + 3 * kRouterItems * egw * 4 +
+  return static_cast<size_t>(kRouterStages) * kRouterStageBytes + kRouterStages * kRouterItems * egw * 4 +
          sizeof(RouterShared) + 16;
 }
 

@@ -387,8 +387,10 @@ def test_topk_thread_per_token_matches_warp_kernel(cfg):
         b = _with_env("HM_TOPK_WARP", lambda: ops.router_topk(x, wg, cfg.k))
     finally:
         os.environ.pop("HM_ROUTER_UNFUSED", None)
-    for name in ("idx", "w", "counts", "offsets", "chunk_base"):
+    for name in ("idx", "w", "counts", "offsets"):
         assert torch.equal(_bits(getattr(a, name)), _bits(getattr(b, name))), name
+    n = ((cfg.T + 63) // 64) * cfg.E  # the table's last element is the fused kernel's counter
+    assert torch.equal(a.chunk_base[:n], b.chunk_base[:n])
 
 
 @pytest.mark.parametrize("cfg", [with_tokens(C3, 777), with_tokens(C1, 500)], ids=lambda c: c.name)

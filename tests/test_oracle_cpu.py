@@ -41,37 +41,36 @@ def test_fixed_order_is_the_documented_blocked_butterfly():
 
 
 def test_reduce_scatter_butterfly_equals_full_butterfly():
-    """The kernel reduces a warp's EGW lane partials with a reduce-scatter butterfly (halving the
-    vector at offsets 16, 8, ...; then plain xor steps): the same pairwise tree per expert as the
-    full butterfly, so the same bits (fp32 addition is commutative)."""
+    """The kernel reduces a warp's EGW lane partials with a select-free reduce-scatter butterfly:
+    lane L keeps its partials in XOR order (slot r = expert r ^ m(L)), and at each halving level
+    (offsets 16, 8, ...) adds its partner's high half to its low half; then plain xor steps. Per
+    expert this is the full butterfly's pairwise tree, so the same bits (fp32 addition is
+    commutative)."""
     rng = np.random.default_rng(5)
+
+    def lane_expert(L, egw):
+        e, off, h = 0, 16, egw // 2
+        while h >= 1:
+            e += h if L & off else 0
+            off, h = off // 2, h // 2
+        return e
+
     for egw in (8, 4, 2):
-        v = rng.standard_normal((32, egw)).astype(np.float32) * np.float32(1e3) ** rng.integers(-2, 3, (32, egw))
-        v = v.astype(np.float32)
+        v = (rng.standard_normal((32, egw)) * 1e3 ** rng.integers(-2, 3, (32, egw))).astype(np.float32)
         full = v.copy()
         for off in (16, 8, 4, 2, 1):
             full = (full + full[np.arange(32) ^ off]).astype(np.float32)
-        cur = [list(v[L]) for L in range(32)]
+        cur = [[v[L][r ^ lane_expert(L, egw)] for r in range(egw)] for L in range(32)]
         off, h = 16, egw // 2
         while h >= 1:
-            nxt = []
-            for L in range(32):
-                up = bool(L & off)
-                keep = [cur[L][m + h] if up else cur[L][m] for m in range(h)]
-                P = L ^ off
-                send = [cur[P][m] if bool(P & off) else cur[P][m + h] for m in range(h)]
-                nxt.append([np.float32(keep[m] + send[m]) for m in range(h)])
-            cur, off, h = nxt, off // 2, h // 2
+            cur = [[np.float32(cur[L][m] + cur[L ^ off][m + h]) for m in range(h)] for L in range(32)]
+            off, h = off // 2, h // 2
         r = [np.float32(c[0]) for c in cur]
-        o = off
-        while o >= 1:
-            r = [np.float32(r[L] + r[L ^ o]) for L in range(32)]
-            o //= 2
+        while off >= 1:
+            r = [np.float32(r[L] + r[L ^ off]) for L in range(32)]
+            off //= 2
         for L in range(32):
-            e, oo, hh = 0, 16, egw // 2
-            while hh >= 1:
-                e += hh if L & oo else 0
-                oo, hh = oo // 2, hh // 2
+            e = lane_expert(L, egw)
             assert r[L].view(np.uint32) == full[L, e].view(np.uint32), (egw, L, e)
 
 

@@ -86,12 +86,13 @@ int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, co
 
 /* ---- router backward fused with the unpermute-sum ----
  * dlogit = softmax-backward of the k selected weights; dx = unpermute_sum(dx_perm) + dlogit . wg^T;
- * dwg[d,E] (bf16) = sum over each expert's permuted rows of dlogit * x_perm (x_perm/offsets from
- * the forward; for E <= 8 each token's row is read once, from its first routed copy). wg_t = wg
+ * dwg[d,E] (bf16) = sum over tokens of x[t] (x) dlogit_dense[t] (x_perm/offsets from the forward;
+ * for E <= 8 each token's row is read once: from x[T,d] (the router input, may be NULL) streamed
+ * through shared memory when d % 512 == 0, else from its first routed copy). wg_t = wg
  * transposed ([E,d], see hm_transpose_bf16); part = fp32 workspace of
- * hm_router_bwd_part_elems(T,d,E,k) elements. dwg may be NULL (then x_perm/offsets/part unused). */
+ * hm_router_bwd_part_elems(T,d,E,k) elements. dwg may be NULL (then x/x_perm/offsets/part unused). */
 int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
-                  const float* dw, const void* x_perm, const int32_t* offsets, const void* wg_t,
+                  const float* dw, const void* x, const void* x_perm, const int32_t* offsets, const void* wg_t,
                   int T, int d, int E, int k, void* dx, float* dlogit, void* dwg, float* part,
                   void* stream);
 size_t hm_router_bwd_part_elems(int T, int d, int E, int k);

@@ -40,7 +40,7 @@ SIGNATURES = {
     "hm_unpermute_sum": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "hm_combine": (_I, [_P, _P, _P, _I, _I, _I, _P, _P]),
     "hm_combine_bwd": (_I, [_P, _P, _P, _P, _I, _I, _I, _P, _P, _P]),
-    "hm_router_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "hm_router_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "hm_router_bwd_part_elems": (ctypes.c_size_t, [_I, _I, _I, _I]),
     "hm_transpose_bf16": (_I, [_P, _I, _I, _P, _P]),
     "hm_grouped_gemm": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _P, _I, _P]),

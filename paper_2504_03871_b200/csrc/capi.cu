@@ -550,14 +550,26 @@ static size_t router_bwd_dl_elems(int T, int k) {
   return (static_cast<size_t>(T) * k + 63) & ~static_cast<size_t>(63);
 }
 
+// token splits of the streamed router weight gradient: one CTA per SM over (column tile, split)
+static int router_wgrad_stream_splits(int T, int d) {
+  const int tiles = (d + hm::kWgCols - 1) / hm::kWgCols;
+  int s = num_sms() / tiles;
+  if (s < 1) s = 1;
+  const int max_s = (T + hm::kWgTok - 1) / hm::kWgTok;
+  return s < max_s ? s : (max_s > 0 ? max_s : 1);
+}
+
 size_t hm_router_bwd_part_elems(int T, int d, int E, int k) {
-  // dlogit in permuted-row order (T*k) followed by the per-split dWg partials
-  const int splits = hm::kWgSplit > hm::kWgTokSplit ? hm::kWgSplit : hm::kWgTokSplit;
-  return router_bwd_dl_elems(T, k) + static_cast<size_t>(splits) * E * d;
+  // dlogit (token or permuted-row order, T*k padded), the dense dlogit rows (T*8, E <= 8), then
+  // the per-split dWg partials
+  int splits = hm::kWgSplit > hm::kWgTokSplit ? hm::kWgSplit : hm::kWgTokSplit;
+  const int ss = router_wgrad_stream_splits(T, d);
+  if (ss > splits) splits = ss;
+  return router_bwd_dl_elems(T, k) + static_cast<size_t>(T) * 8 + static_cast<size_t>(splits) * E * d;
 }
 
 int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
-                  const float* dw, const void* x_perm, const int32_t* offsets, const void* wg_t,
+                  const float* dw, const void* x, const void* x_perm, const int32_t* offsets, const void* wg_t,
                   int T, int d, int E, int k, void* dx, float* dlogit, void* dwg, float* part,
                   void* stream) {
   if (T < 0 || d <= 0 || d % 8 != 0 || E < 1 || E > 256) return fail(HM_E_SHAPE, "router_bwd: bad shape");
@@ -572,23 +584,44 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   auto dp = static_cast<const __nv_bfloat16*>(dx_perm);
   auto gt = static_cast<const __nv_bfloat16*>(wg_t);
   auto out = static_cast<__nv_bfloat16*>(dx);
-  // dWg: token-major (each token row read once) for E <= 8, k <= 3 and d % 64 == 0, else per
-  // expert over the permuted rows (each routed copy read once)
-  const bool tok = dwg && E <= 8 && k <= 3 && d % 64 == 0 && !getenv("HM_ROUTER_WGRAD_PERM");
-  float* dl_perm = (dwg && !tok) ? part : nullptr;
+  // dWg: for E <= 8 and the token rows x given, streamed token-major through shared memory from
+  // the dense dlogit rows (each token row read once, contiguously); else token-major from the
+  // first routed copies (k <= 3), else per expert over the permuted rows (each copy read once)
+  const bool perm_forced = getenv("HM_ROUTER_WGRAD_PERM") != nullptr;
+  const bool streamed = dwg && E <= 8 && x && d % hm::kWgCols == 0 && aligned16(x) && !perm_forced &&
+                        !getenv("HM_ROUTER_WGRAD_TOK");
+  const bool tok = dwg && !streamed && E <= 8 && k <= 3 && d % 64 == 0 && !perm_forced;
+  float* dl_perm = (dwg && !tok && !streamed) ? part : nullptr;
   float* dl_tok = dlogit ? dlogit : (tok ? part : nullptr);
+  float* coef8 = streamed ? part + router_bwd_dl_elems(T, k) : nullptr;
   // k >= 4: metadata broadcast by shuffles, no row prefetch (C3, k = 6: 0.099 vs 0.121 ms);
   // k <= 3: the v1 kernel (C2, k = 2: 0.080 vs 0.088 ms). Both produce bit-identical dx / dlogit
   // (tools/router_bench.py). HM_UNPERMUTE_V1 / HM_UNPERMUTE_V2 force a variant for A/B runs.
   const bool v1 = getenv("HM_UNPERMUTE_V1") || (k <= 3 && !getenv("HM_UNPERMUTE_V3"));
   if (getenv("HM_UNPERMUTE_V2")) {
-    HM_K_SWITCH(k, (hm::unpermute_router_bwd2_kernel<K, true><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+    HM_K_SWITCH(k, (hm::unpermute_router_bwd2_kernel<K, true><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm, coef8)));
   } else if (v1) {
-    HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+    HM_K_SWITCH(k, (hm::unpermute_router_bwd_kernel<K><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm, coef8)));
   } else {
-    HM_K_SWITCH(k, (hm::unpermute_router_bwd2_kernel<K, false><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm)));
+    HM_K_SWITCH(k, (hm::unpermute_router_bwd2_kernel<K, false><<<row_grid(T), 256, 0, st>>>(dp, row_of, idx, w, dw, gt, T, d, out, dl_tok, dl_perm, coef8)));
   }
   if (int rc = check_launch("unpermute_router_bwd")) return rc;
+  if (streamed) {
+    float* partials = coef8 + static_cast<size_t>(T) * 8;
+    const int S = router_wgrad_stream_splits(T, d);
+    const size_t smem = hm::router_wgrad_stream_smem_bytes();
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(hm::router_wgrad_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    hm::router_wgrad_stream_kernel<<<dim3(d / hm::kWgCols, S), hm::kWgThreads, smem, st>>>(
+        static_cast<const __nv_bfloat16*>(x), coef8, T, d, E, partials);
+    if (int rc = check_launch("router_wgrad_stream")) return rc;
+    const long n = static_cast<long>(d) * E;
+    hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(partials, S, d, E, static_cast<__nv_bfloat16*>(dwg));
+    return check_launch("router_wgrad_reduce");
+  }
   if (tok) {
     float* partials = part + router_bwd_dl_elems(T, k);
     auto xp = static_cast<const __nv_bfloat16*>(x_perm);

@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(256, 4)
                                 const float* __restrict__ w, const float* __restrict__ dw,
                                 const __nv_bfloat16* __restrict__ wg_t, int T, int d,
                                 __nv_bfloat16* __restrict__ dx, float* __restrict__ dlogit,
-                                float* __restrict__ dl_perm) {
+                                float* __restrict__ dl_perm, float* __restrict__ coef8 = nullptr) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -817,6 +817,11 @@ __global__ void __launch_bounds__(256, 4)
       dl[s] = ws * (dw[static_cast<long>(t) * K + s] - wsum);
       if (lane == 0 && dlogit) dlogit[static_cast<long>(t) * K + s] = dl[s];
       if (lane == 0 && dl_perm) dl_perm[rows[s]] = dl[s];
+    }
+    if (coef8 && lane < 8) {  // dense dlogit row (E <= 8): the router weight-gradient coefficients
+      float c = 0.f;
+      for (int s = 0; s < K; ++s) c = (ex[s] == lane) ? dl[s] : c;
+      coef8[static_cast<long>(t) * 8 + lane] = c;
     }
     for (int q = lane; q < nv; q += 32) {
       float acc[8];
@@ -856,7 +861,7 @@ __global__ void __launch_bounds__(256, PF ? 2 : 3)
                                  const float* __restrict__ w, const float* __restrict__ dw,
                                  const __nv_bfloat16* __restrict__ wg_t, int T, int d,
                                  __nv_bfloat16* __restrict__ dx, float* __restrict__ dlogit,
-                                 float* __restrict__ dl_perm) {
+                                 float* __restrict__ dl_perm, float* __restrict__ coef8 = nullptr) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -892,6 +897,12 @@ __global__ void __launch_bounds__(256, PF ? 2 : 3)
       dl[s] = ws[s] * (dws[s] - wsum);
       if (lane == 0 && dlogit) dlogit[static_cast<long>(t) * K + s] = dl[s];
       if (lane == 0 && dl_perm) dl_perm[rows[s]] = dl[s];
+    }
+    if (coef8 && lane < 8) {  // dense dlogit row (E <= 8)
+      float c = 0.f;
+#pragma unroll
+      for (int s = 0; s < K; ++s) c = (ex[s] == lane) ? dl[s] : c;
+      coef8[static_cast<long>(t) * 8 + lane] = c;
     }
     uint4 cur[K];
 #pragma unroll
@@ -1112,6 +1123,106 @@ __global__ void __launch_bounds__(256, 2)
     const int e = ez >> 3, z = ez & 7;
     const int c = blockIdx.x * 64 + g * 8 + z;
     if (e < E && c < d) part[(static_cast<long>(split) * E + e) * d + c] = s;
+  }
+}
+
+// Router weight gradient for E <= 8 streamed through shared memory:
+//   dWg[i, e] = sum_t x[t, i] * coef8[t, e]   (coef8 = the dense dlogit rows, zeros off the top-k)
+// grid = (d / 512 column tiles, S token splits). Token rows [32 tokens x 512 columns] and their
+// coefficient rows arrive by 1-D bulk copies (TMA engine; one row per lane of the producer warp
+// 16) in a 4-stage ring. Compute warps 0..15: thread c = tid % 256 owns columns (2c, 2c+1) of the
+// tile and 8 experts (16 fp32 accumulators, packed FFMA2 over the column pair); warps 0..7 take
+// the even tokens of a stage, warps 8..15 the odd ones. Each thread sums in token order, the two
+// halves are added (even + odd) at the end, and per-split partials are reduced in split order by
+// router_wgrad_reduce_kernel: deterministic.
+constexpr int kWgCols = 512;
+constexpr int kWgTok = 32;
+constexpr int kWgStages = 4;
+constexpr int kWgXBytes = kWgTok * kWgCols * 2;   // 32 KB
+constexpr int kWgCBytes = kWgTok * 8 * 4;          // 1 KB
+constexpr int kWgStageBytes = kWgXBytes + kWgCBytes;
+constexpr int kWgThreads = 17 * 32;
+constexpr size_t router_wgrad_stream_smem_bytes() { return static_cast<size_t>(kWgStages) * kWgStageBytes + 128; }
+
+__global__ void __launch_bounds__(kWgThreads, 1)
+    router_wgrad_stream_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ coef8, int T,
+                               int d, int E, float* __restrict__ part /*[S][E][d]*/) {
+  extern __shared__ __align__(1024) uint8_t smem_wg[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_wg + kWgStages * kWgStageBytes);
+  uint64_t* empty = full + kWgStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = blockIdx.x * kWgCols;
+  const int S = gridDim.y, split = blockIdx.y;
+  const int t_begin = static_cast<int>((static_cast<long>(T) * split) / S);
+  const int t_end = static_cast<int>((static_cast<long>(T) * (split + 1)) / S);
+  const int nst = (t_end - t_begin + kWgTok - 1) / kWgTok;
+  if (tid == 0) {
+    for (int s = 0; s < kWgStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 16);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 16) {
+    // ======== producer: lane r copies token row r of the stage, lane 0 arms the barrier ========
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % kWgStages;
+      const int t0 = t_begin + s * kWgTok;
+      const int nt = min(kWgTok, t_end - t0);
+      if (s >= kWgStages) mbar_wait(&empty[slot], ((s / kWgStages) - 1) & 1);
+      uint8_t* dst = smem_wg + slot * kWgStageBytes;
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[slot], nt * kWgCols * 2 + nt * 32);
+        bulk_load_1d(dst + kWgXBytes, coef8 + static_cast<long>(t0) * 8, nt * 32, &full[slot]);
+      }
+      __syncwarp();
+      if (lane < nt)
+        bulk_load_1d(dst + lane * kWgCols * 2, x + static_cast<long>(t0 + lane) * d + c0, kWgCols * 2, &full[slot]);
+    }
+    return;
+  }
+  const int c = tid & 255, par = tid >> 8;
+  float2 acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = make_float2(0.f, 0.f);
+  for (int s = 0; s < nst; ++s) {
+    const int slot = s % kWgStages;
+    const int nt = min(kWgTok, t_end - (t_begin + s * kWgTok));
+    mbar_wait(&full[slot], (s / kWgStages) & 1);
+    const uint8_t* st = smem_wg + slot * kWgStageBytes;
+    const float* cf = reinterpret_cast<const float*>(st + kWgXBytes);
+#pragma unroll 4
+    for (int r = par; r < nt; r += 2) {
+      const uint32_t xp = *reinterpret_cast<const uint32_t*>(st + r * kWgCols * 2 + c * 4);
+      const float2 xf = make_float2(__uint_as_float(xp << 16), __uint_as_float(xp & 0xffff0000u));
+      const float4 ca = *reinterpret_cast<const float4*>(cf + r * 8);
+      const float4 cb = *reinterpret_cast<const float4*>(cf + r * 8 + 4);
+      const float cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = __ffma2_rn(xf, make_float2(cc[e], cc[e]), acc[e]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+  // even + odd token halves (fixed order), through the now idle ring (named barrier of the 16
+  // compute warps: the producer warp has returned)
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+  float2* xch = reinterpret_cast<float2*>(smem_wg);
+  if (par == 1) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xch[e * 256 + c] = acc[e];
+  }
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+  if (par == 0) {
+    const int col = c0 + 2 * c;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float2 o = xch[e * 256 + c];
+      const float2 v = make_float2(acc[e].x + o.x, acc[e].y + o.y);
+      if (e < E && col < d) *reinterpret_cast<float2*>(part + (static_cast<long>(split) * E + e) * d + col) = v;
+    }
   }
 }
 

@@ -177,8 +177,8 @@ class NativeBackend:
     def combine_bwd(self, dy, y_perm, row_of, r):
         return self.ops.combine_bwd(dy, y_perm, row_of, r.w)
 
-    def router_bwd(self, dx_perm, row_of, r, dw, x_perm, wg_t):
-        dx, _dl, dwg = self.ops.router_bwd(dx_perm, row_of, r, dw, x_perm, wg_t, want_dwg=True)
+    def router_bwd(self, dx_perm, row_of, r, dw, x_perm, wg_t, x=None):
+        dx, _dl, dwg = self.ops.router_bwd(dx_perm, row_of, r, dw, x_perm, wg_t, want_dwg=True, x=x)
         return dx, dwg
 
     def transpose(self, w):
@@ -544,7 +544,7 @@ class ZpExecutor:
         if self.wg_t.get(l, (None,))[0] != key:
             self.wg_t[l] = (key, be.transpose(st.wg[l]))
         dz, dwg = be.router_bwd(self.dx_perm[(l, j)], self.row_of[(l, j)], r, self.dw[(l, j)],
-                                self.x_perm[(l, j)], self.wg_t[l][1])
+                                self.x_perm[(l, j)], self.wg_t[l][1], x=self.zd[(l, j)])
         st.gwg[l] += dwg.float()
         h = self.h_in[(l, j)]
         with torch.enable_grad():

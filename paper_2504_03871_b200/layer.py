@@ -54,7 +54,7 @@ class _MoEFunction(torch.autograd.Function):
             dy_perm, x_perm, h, act, r.offsets, w_ug, w_down, ctx.max_ctas
         )
         wg_t = router_weight_t(ctx.wg_obj)
-        dx, _dlogit, dwg = ops.router_bwd(dx_perm, row_of, r, dw, x_perm, wg_t, want_dwg=True)
+        dx, _dlogit, dwg = ops.router_bwd(dx_perm, row_of, r, dw, x_perm, wg_t, want_dwg=True, x=x)
         return dx, dwg, dw_ug, dw_down, None, None
 
 

@@ -202,9 +202,10 @@ def transpose_bf16(a: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def router_bwd(dx_perm, row_of, r: Routing, dw, x_perm, wg_t, want_dwg: bool = True):
-    """dx = unpermute_sum(dx_perm) + dlogit . Wg^T ; dWg = sum_rows dlogit * x_perm (per expert)."""
-    _require_cuda(dx_perm, row_of, dw, x_perm, wg_t)
+def router_bwd(dx_perm, row_of, r: Routing, dw, x_perm, wg_t, want_dwg: bool = True, x=None):
+    """dx = unpermute_sum(dx_perm) + dlogit . Wg^T ; dWg = x^T . dlogit_dense (E <= 8: from the token
+    rows x when given, streamed; else from the routed copies in x_perm)."""
+    _require_cuda(dx_perm, row_of, dw, x_perm, wg_t, x)
     lib = _native.load()
     T, k = row_of.shape
     d = x_perm.shape[1]
@@ -218,7 +219,7 @@ def router_bwd(dx_perm, row_of, r: Routing, dw, x_perm, wg_t, want_dwg: bool = T
         part = torch.empty((lib.hm_router_bwd_part_elems(T, d, E, k),), dtype=torch.float32, device=dev)
     _tk = _begin("router_bwd")
     rc = lib.hm_router_bwd(
-        _ptr(dx_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(dw), _ptr(x_perm), _ptr(r.offsets),
+        _ptr(dx_perm), _ptr(row_of), _ptr(r.idx), _ptr(r.w), _ptr(dw), _ptr(x), _ptr(x_perm), _ptr(r.offsets),
         _ptr(wg_t), T, d, E, k, _ptr(dx), _ptr(dlogit), _ptr(dwg), _ptr(part), _stream(),
     )
     _end(_tk)

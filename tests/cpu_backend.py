@@ -88,7 +88,7 @@ class CpuBackend:
         dw = (y_perm[row_of.reshape(-1)].reshape(T, k, -1) * dy[:, None, :]).sum(-1)
         return dy_perm, dw
 
-    def router_bwd(self, dx_perm, row_of, r, dw, x_perm, wg_t):
+    def router_bwd(self, dx_perm, row_of, r, dw, x_perm, wg_t, x=None):
         T, k = row_of.shape
         dx = dx_perm[row_of.reshape(-1)].reshape(T, k, -1).sum(1)
         dl = r.w * (dw - (r.w * dw).sum(1, keepdim=True))

@@ -180,3 +180,36 @@ def test_router_fused_equals_unfused_and_oracle(cfg):
     assert np.array_equal(a.idx.cpu().numpy(), ref.idx)
     assert np.array_equal(a.offsets.cpu().numpy(), ref.offsets)
     np.testing.assert_allclose(a.w.cpu().numpy(), ref.w, rtol=0, atol=TOL_GATE)
+
+
+@pytest.mark.parametrize("cfg", [LayerConfig("E8d4096", 8, 2, 4096, 128, 3000),
+                                 LayerConfig("E4d1024k3", 4, 3, 1024, 128, 777)], ids=lambda c: c.name)
+def test_router_bwd_streamed_wgrad_vs_fp32(cfg):
+    """The streamed router weight gradient (E <= 8, token rows x through shared memory) against a
+    plain fp32 reference dWg = x^T . dlogit_dense, and the three dWg paths against each other."""
+    import os
+
+    inp = make_inputs(cfg, seed=19)
+    x, wg = inp.x.cuda(), inp.wg.cuda()
+    r = ops.router_topk(x, wg, cfg.k)
+    xp, _, row_of = ops.dispatch_permute(x, r)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    dxp = torch.randn(xp.shape, generator=g, device="cuda").to(xp.dtype)
+    dw = torch.randn(r.w.shape, generator=g, device="cuda")
+    wg_t = ops.transpose_bf16(wg)
+    outs = {}
+    for v, env in (("stream", None), ("tok", "HM_ROUTER_WGRAD_TOK"), ("perm", "HM_ROUTER_WGRAD_PERM")):
+        if env:
+            os.environ[env] = "1"
+        try:
+            outs[v] = ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x)
+        finally:
+            if env:
+                os.environ.pop(env)
+    torch.cuda.synchronize()
+    dl = outs["stream"][1].float()  # dlogit [T, k]
+    dense = torch.zeros((cfg.T, cfg.E), device="cuda").scatter_(1, r.idx.long(), dl)
+    ref = x.float().t() @ dense
+    for v in outs:
+        assert torch.equal(outs[v][0], outs["stream"][0]), v  # dx identical on every path
+        assert orc.rel_err(outs[v][2], ref) < 5e-3, v

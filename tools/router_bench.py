@@ -87,15 +87,20 @@ def main():
     out["router_fwd_ms_variants"] = {v: min(t) for v, t in fw.items()}
     out["router_fwd_ms"] = min(fw["fused"])
     res = {}
-    for variant in ("tok", "perm", "tok", "perm"):
+    for variant in ("stream", "tok", "perm", "stream", "tok", "perm"):
+        os.environ.pop("HM_ROUTER_WGRAD_PERM", None)
+        os.environ.pop("HM_ROUTER_WGRAD_TOK", None)
         if variant == "perm":
             os.environ["HM_ROUTER_WGRAD_PERM"] = "1"
-        else:
-            os.environ.pop("HM_ROUTER_WGRAD_PERM", None)
-        ms = timed(lambda: ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True), args.reps)
+        elif variant == "tok":
+            os.environ["HM_ROUTER_WGRAD_TOK"] = "1"
+        ms = timed(lambda: ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x), args.reps)
         res.setdefault(variant, []).append(ms)
-        res.setdefault(variant + "_dwg", ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True)[2].float())
-    out["router_bwd_ms"] = {v: min(res[v]) for v in ("tok", "perm")}
+        res.setdefault(variant + "_dwg", ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x)[2].float())
+    os.environ.pop("HM_ROUTER_WGRAD_PERM", None)
+    os.environ.pop("HM_ROUTER_WGRAD_TOK", None)
+    out["router_bwd_ms"] = {v: min(res[v]) for v in ("stream", "tok", "perm")}
+    out["dwg_rel_diff_stream_vs_perm"] = float((res["stream_dwg"] - res["perm_dwg"]).norm() / res["perm_dwg"].norm())
     # unpermute + dlogit.Wg kernel variants (HM_UNPERMUTE_V1/V2/V3), dx / dlogit compared bitwise
     uv = {}
     for variant in ("v1", "v2", "v3", "v1", "v2", "v3"):

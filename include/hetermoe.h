@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define HM_ABI_VERSION 1
+#define HM_ABI_VERSION 2
 
 #define HM_E_SHAPE 1001     /* unsupported or inconsistent shape */
 #define HM_E_ALIGN 1002     /* pointer / stride alignment violated (16 bytes) */

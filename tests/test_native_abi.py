@@ -25,7 +25,12 @@ def test_library_exports_all_symbols():
 
 def test_pure_host_entry_points():
     lib = _native.load()
-    assert lib.hm_abi_version() == 1
-    assert lib.hm_router_chunk_elems(4096, 8) == 64 * 8
-    assert lib.hm_router_chunk_elems(1, 64) == 64
-    assert lib.hm_router_bwd_part_elems(16384, 4096, 8, 2) == 16384 * 2 + 16 * 8 * 4096
+    assert lib.hm_abi_version() == 2
+    # per-chunk table + the fused router's completion counter
+    assert lib.hm_router_chunk_elems(4096, 8) == 64 * 8 + 1
+    assert lib.hm_router_chunk_elems(1, 64) == 64 + 1
+    assert lib.hm_router_launches(16384, 4096, 8) == 1  # logits + top-k + histogram + scan fused
+    assert lib.hm_router_launches(16384, 2048, 64) == 3  # 8 expert groups: logits, top-k, scan
+    assert lib.hm_router_launches(16384, 768, 8) == 0  # d must be 256 * 2^m
+    # dlogit (T*k), dense dlogit rows (T*8), then at least 16 splits of dWg partials
+    assert lib.hm_router_bwd_part_elems(16384, 4096, 8, 2) >= 16384 * 2 + 16384 * 8 + 16 * 8 * 4096

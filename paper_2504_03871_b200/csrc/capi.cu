@@ -181,28 +181,35 @@ int gemm_wide_mask();
 
 // CTA count / tile width dispatch for one GEMM kind: 1 CTA (HM_GEMM_CTAS=1), a CTA pair with
 // 256 x 256 tiles, or a CTA pair with 256 x 512 tiles (modes in the wide mask)
-int gemm_group_m(int mode);
+int gemm_group_m(int mode, long M);
 int g_early_release = getenv("HM_GEMM_NO_EARLY_RELEASE") ? 0 : 1;
 
 template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
 int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p0,
                 const TileBound& tb, int max_ctas, cudaStream_t st) {
   hm::GroupedGemmParams p = p0;
-  p.group_m = gemm_group_m(mode);
+  p.group_m = gemm_group_m(mode, tb.M);
   p.early_release = g_early_release;
   if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1>(ma, mb, p, tb, max_ctas, st);
   if ((gemm_wide_mask() >> mode) & 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
   return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1>(ma, mb, p, tb, max_ctas, st);
 }
 
-// raster group height per GEMM mode (HM_GEMM_GROUPM = one value for every mode)
+// raster group height per GEMM mode (HM_GEMM_GROUPM = one value for every mode). The per-mode
+// defaults minimise DRAM traffic at equal time (C2 sweep of 8/16/32/64, profiles/r2_gemm_groupm.md):
+// up+gate 32 (5.6 -> 3.6 GB read), SwiGLU backward 64; the weight gradients 32 when the output
+// has at most 32 row tiles (dW_d, M = d: 2.4 -> 1.6 GB) and 8 otherwise (dW_ug, M = 2f: 4.2 GB
+// at 8, 7.3 at 32); the others keep 8 (dX: 8.9 GB at 8, 10.4 at 16).
 int g_group_m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-int gemm_group_m(int mode) {
+int gemm_group_m(int mode, long M = 0) {
+  static const int kDefault[8] = {32, 8, 64, 8, 0, 0, 8, 8};  // by HM_GEMM_* mode; 0 = by M
   if (mode < 0 || mode >= 8) return hm::kGroupM;
   if (g_group_m[mode] <= 0) {
     const char* s = getenv("HM_GEMM_GROUPM");
     const int v = s ? atoi(s) : 0;
-    g_group_m[mode] = v > 0 ? v : hm::kGroupM;
+    if (v > 0) g_group_m[mode] = v;
+    else if (kDefault[mode] > 0) g_group_m[mode] = kDefault[mode];
+    else return (M + 255) / 256 <= 32 ? 32 : 8;
   }
   return g_group_m[mode];
 }
@@ -325,7 +332,7 @@ int hm_debug_set_gemm_wide(int mask) {
 // tuning aid (not part of the ABI): raster group height of one GEMM mode (mode < 0: all modes;
 // value <= 0: back to the default); returns the previous value of `mode` (or of mode 0)
 int hm_debug_set_gemm_groupm(int mode, int value) {
-  const int old = gemm_group_m(mode < 0 ? 0 : mode);
+  const int old = gemm_group_m(mode < 0 ? 0 : mode, 0);
   for (int m = 0; m < 8; ++m)
     if (mode < 0 || m == mode) g_group_m[m] = value;
   return old;

@@ -213,3 +213,47 @@ def test_router_bwd_streamed_wgrad_vs_fp32(cfg):
     for v in outs:
         assert torch.equal(outs[v][0], outs["stream"][0]), v  # dx identical on every path
         assert orc.rel_err(outs[v][2], ref) < 5e-3, v
+
+
+def test_c_abi_grouped_ffn_entry_points_match_ops():
+    """hm_grouped_ffn_fwd / hm_grouped_ffn_bwd — the C-ABI compositions a C/C++ runtime calls for
+    EXP_F / EXP_B (include/hetermoe.h) — called through ctypes exactly as INTEGRATION.md shows,
+    bitwise equal to the per-GEMM path the Python layer uses, and within the fp32 bars."""
+    from paper_2504_03871_b200 import _native
+
+    lib = _native.load()
+    segs = [700, 0, 1200, 333, 64, 1]
+    E, d, f = len(segs), 512, 384
+    rows = sum(segs)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    bf = lambda *s, std=1.0: (torch.randn(s, generator=g, device="cuda") * std).to(torch.bfloat16)  # noqa: E731
+    x, dy = bf(rows, d), bf(rows, d)
+    w_ug, w_d = bf(E, 2 * f, d, std=d ** -0.5), bf(E, d, f, std=f ** -0.5)
+    off = np.zeros(E + 1, dtype=np.int32)
+    off[1:] = np.cumsum(segs)
+    seg = torch.from_numpy(off).cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    h = torch.empty((rows, 2 * f), dtype=torch.bfloat16, device="cuda")
+    act = torch.empty((rows, f), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((rows, d), dtype=torch.bfloat16, device="cuda")
+    assert lib.hm_grouped_ffn_fwd(x.data_ptr(), rows, seg.data_ptr(), E, w_ug.data_ptr(), w_d.data_ptr(), d, f,
+                                  h.data_ptr(), act.data_ptr(), y.data_ptr(), 0, s) == 0
+    dh = torch.empty_like(h)
+    dx = torch.empty_like(x)
+    dw_ug, dw_d = torch.empty_like(w_ug), torch.empty_like(w_d)
+    nws = 2 * lib.hm_grouped_gemm_workspace_bytes(_native.GEMM_WGRAD, E)
+    ws = torch.empty((nws + 128,), dtype=torch.uint8, device="cuda")
+    wsp = ws.data_ptr() + (-ws.data_ptr()) % 128
+    assert lib.hm_grouped_ffn_bwd(dy.data_ptr(), x.data_ptr(), h.data_ptr(), act.data_ptr(), rows, seg.data_ptr(),
+                                  E, w_ug.data_ptr(), w_d.data_ptr(), d, f, dh.data_ptr(), dx.data_ptr(),
+                                  dw_ug.data_ptr(), dw_d.data_ptr(), wsp, 0, s) == 0
+    y2, h2, act2 = ops.grouped_ffn_fwd(x, seg, w_ug, w_d)
+    dx2, dw_ug2, dw_d2 = ops.grouped_ffn_bwd(dy, x, h2, act2, seg, w_ug, w_d)
+    torch.cuda.synchronize()
+    for a, b in ((y, y2), (h, h2), (act, act2), (dx, dx2), (dw_ug, dw_ug2), (dw_d, dw_d2)):
+        assert torch.equal(a, b)
+    wg_, wu_ = ops.split_gate_up(w_ug.float().cpu())
+    xr = x.float().cpu().requires_grad_()
+    yr = orc.expert_ffn(xr, off, wg_, wu_, w_d.float().cpu())
+    yr.backward(dy.float().cpu())
+    assert orc.rel_err(y, yr) < TOL_ACT and orc.rel_err(dx, xr.grad) < TOL_ACT

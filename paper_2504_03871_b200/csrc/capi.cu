@@ -226,7 +226,7 @@ int gemm_stats_enabled() {
 // GEMM modes (bit = HM_GEMM_* mode) that use the 256 x 512 "wide" pair tile; HM_GEMM_WIDE
 // overrides the default (measured per mode on B200)
 #ifndef HM_GEMM_WIDE_DEFAULT
-#define HM_GEMM_WIDE_DEFAULT 0x3B  // up+gate, down, dX, both wgrads (not the SwiGLU backward)
+#define HM_GEMM_WIDE_DEFAULT 0x3F  // every GEMM: up+gate, down, SwiGLU backward, dX, both wgrads
 #endif
 int g_wide_mask = -1;
 int gemm_wide_mask() {

@@ -594,28 +594,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t aph = (kAccBufs == 2 ? (tcount >> 1) : tcount) & 1;
 
       if (EPI == EPI_SWIGLU_FWD && NSUB == 2 && p.early_release) {
-        // Wide tile, SwiGLU forward: sub-tile 0 is processed straight from TMEM; sub-tile 1's
-        // gate/up accumulators are rounded to bf16 (exactly the saved h) and held in registers,
-        // the accumulator is released, then h and act = silu(g) * u of sub-tile 1 are formed
-        // and stored under the next tile's MMAs.
+        // Wide tile, SwiGLU forward, drain-then-release: both sub-tiles' gate/up accumulators
+        // are rounded to bf16 and stored as the saved h straight from TMEM (no math while the
+        // accumulator is held), the accumulator is released, and act = silu(g) * u is formed
+        // from this thread's own h rows read back (L2-hot, program order) under the next tile's
+        // MMAs. act is computed from the same bf16 values as before: bit-identical results.
         mbar_wait(&sh.tmem_full[acc], aph);
         tc_fence_after();
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
         const bool v8ok = (((reinterpret_cast<uintptr_t>(p.out) | reinterpret_cast<uintptr_t>(p.out2)) & 31u) == 0) &&
                           (p.ldo % 16 == 0) && (p.ldo2 % 16 == 0);
-        auto load_gu = [&](int u, int i, uint32_t (&g8)[8], uint32_t (&u8)[8]) {
-          // 16 gate and the matching 16 up columns of sub-tile u, chunk i (0..3), as bf16
-          const uint32_t col = (acc + u) * kBN + half * 64 + 16 * i;
-          uint32_t r[16];
-          tmem_ld_32x32b_x16(t_row + col, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 8; ++j) g8[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-          tmem_ld_32x32b_x16(t_row + col + kBN / 2, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 8; ++j) u8[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        };
         auto st32 = [&](__nv_bfloat16* dst, const uint32_t (&v)[8]) {
           if (v8ok) {
             st_global_v8(dst, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]));
@@ -624,31 +612,44 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             reinterpret_cast<uint4*>(dst)[1] = make_uint4(v[4], v[5], v[6], v[7]);
           }
         };
-        auto emit = [&](int u, int i, const uint32_t (&g8)[8], const uint32_t (&u8)[8]) {
-          const int nsub_idx = tc.nt * NSUB + u;
-          const int n0 = nsub_idx * kBN;
-          if (!row_ok || n0 >= p.N) return;
-          const int c = half * 64 + 16 * i;
-          st32(p.out2 + grow * p.ldo2 + n0 + c, g8);
-          st32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, u8);
-          uint32_t a8[8];
+        auto ld32 = [&](const __nv_bfloat16* src, uint32_t (&v)[8]) {
+          uint4 lo, hi;
+          if (v8ok) {
+            ld_global_v8(src, lo, hi);
+          } else {
+            lo = reinterpret_cast<const uint4*>(src)[0];
+            hi = reinterpret_cast<const uint4*>(src)[1];
+          }
+          v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w; v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
+        };
+        // 8 chunks (sub-tile u = ch / 4, 16 gate + 16 up columns each), software-pipelined: the
+        // TMEM loads of chunk ch + 1 are in flight while chunk ch is packed and stored
+        uint32_t rg[2][16], ru[2][16];
+        auto issue = [&](int ch, int b) {
+          const uint32_t col = (acc + (ch >> 2)) * kBN + half * 64 + 16 * (ch & 3);
+          tmem_ld_32x32b_x16(t_row + col, rg[b]);
+          tmem_ld_32x32b_x16(t_row + col + kBN / 2, ru[b]);
+        };
+        issue(0, 0);
+        tmem_ld_wait();
+#pragma unroll
+        for (int ch = 0; ch < 4 * NSUB; ++ch) {
+          const int b = ch & 1;
+          if (ch + 1 < 4 * NSUB) issue(ch + 1, b ^ 1);
+          uint32_t g8[8], u8[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float g0 = __uint_as_float(g8[j] << 16), g1 = __uint_as_float(g8[j] & 0xffff0000u);
-            const float u0 = __uint_as_float(u8[j] << 16), u1 = __uint_as_float(u8[j] & 0xffff0000u);
-            a8[j] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+            g8[j] = pack_bf16x2(__uint_as_float(rg[b][2 * j]), __uint_as_float(rg[b][2 * j + 1]));
+            u8[j] = pack_bf16x2(__uint_as_float(ru[b][2 * j]), __uint_as_float(ru[b][2 * j + 1]));
           }
-          st32(p.out + grow * p.ldo + nsub_idx * (kBN / 2) + c, a8);
-        };
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t g8[8], u8[8];
-          load_gu(0, i, g8, u8);
-          emit(0, i, g8, u8);
+          const int n0 = (tc.nt * NSUB + (ch >> 2)) * kBN;
+          if (row_ok && n0 < p.N) {
+            const int c = half * 64 + 16 * (ch & 3);
+            st32(p.out2 + grow * p.ldo2 + n0 + c, g8);
+            st32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, u8);
+          }
+          tmem_ld_wait();
         }
-        uint32_t hg[4][8], hu[4][8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) load_gu(1, i, hg[i], hu[i]);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -656,8 +657,136 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           else mbar_arrive(&sh.tmem_empty[acc]);
         }
         ++tcount;
+        if (row_ok) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) emit(1, i, hg[i], hu[i]);
+          for (int u = 0; u < NSUB; ++u) {
+            const int nsub_idx = tc.nt * NSUB + u;
+            const int n0 = nsub_idx * kBN;
+            if (n0 >= p.N) break;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int c = half * 64 + 16 * i;
+              uint32_t g8[8], u8[8], a8[8];
+              ld32(p.out2 + grow * p.ldo2 + n0 + c, g8);
+              ld32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, u8);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float g0 = __uint_as_float(g8[j] << 16), g1 = __uint_as_float(g8[j] & 0xffff0000u);
+                const float u0 = __uint_as_float(u8[j] << 16), u1 = __uint_as_float(u8[j] & 0xffff0000u);
+                a8[j] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+              }
+              st32(p.out + grow * p.ldo + nsub_idx * (kBN / 2) + c, a8);
+            }
+          }
+        }
+        continue;
+      }
+
+      if (EPI == EPI_SWIGLU_BWD && NSUB == 2 && p.early_release) {
+        // Wide tile, SwiGLU backward, drain-then-release: dA (both sub-tiles, this thread's 128
+        // f-columns of each) is rounded to bf16 and parked in the dH row slots its dgate will
+        // overwrite, the accumulator is released, and dgate / dup are formed from the parked
+        // dA and the saved h under the next tile's MMAs (this thread's own rows: program order).
+        mbar_wait(&sh.tmem_full[acc], aph);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+        const bool v8ok = (((reinterpret_cast<uintptr_t>(p.aux) | reinterpret_cast<uintptr_t>(p.out)) & 31u) == 0) &&
+                          (p.ld_aux % 16 == 0) && (p.ldo % 16 == 0);
+        auto ld64 = [&](const __nv_bfloat16* src, uint4 (&dst)[4]) {
+          if (v8ok) {
+            ld_global_v8(src, dst[0], dst[1]);
+            ld_global_v8(src + 16, dst[2], dst[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = *reinterpret_cast<const uint4*>(src + q * 8);
+          }
+        };
+        auto st64 = [&](__nv_bfloat16* dst, const uint4 (&src)[4]) {
+          if (v8ok) {
+            st_global_v8(dst, src[0], src[1]);
+            st_global_v8(dst + 16, src[2], src[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(dst)[q] = src[q];
+          }
+        };
+        auto dg_ptr = [&](int fcol) { return p.out + grow * p.ldo + (fcol >> 7) * 256 + (fcol & 127); };
+        auto h_ptr = [&](int fcol) { return p.aux + grow * p.ld_aux + (fcol >> 7) * 256 + (fcol & 127); };
+        // 8 chunks of 32 columns (sub-tile u = ch / 4), software-pipelined: the TMEM load of
+        // chunk ch + 1 is in flight while chunk ch is packed and parked
+        uint32_t r[2][32];
+        auto issue = [&](int ch, int b) {
+          tmem_ld_32x32b_x32(t_row + (acc + (ch >> 2)) * kBN + half * 128 + 32 * (ch & 3), r[b]);
+        };
+        issue(0, 0);
+        tmem_ld_wait();
+#pragma unroll
+        for (int ch = 0; ch < 4 * NSUB; ++ch) {
+          const int b = ch & 1;
+          if (ch + 1 < 4 * NSUB) issue(ch + 1, b ^ 1);
+          const int n0 = (tc.nt * NSUB + (ch >> 2)) * kBN;
+          const int c = half * 128 + 32 * (ch & 3);
+          if (row_ok && n0 + c < p.N) {
+            uint4 pk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              pk[q] = make_uint4(pack_bf16x2(__uint_as_float(r[b][8 * q + 0]), __uint_as_float(r[b][8 * q + 1])),
+                                 pack_bf16x2(__uint_as_float(r[b][8 * q + 2]), __uint_as_float(r[b][8 * q + 3])),
+                                 pack_bf16x2(__uint_as_float(r[b][8 * q + 4]), __uint_as_float(r[b][8 * q + 5])),
+                                 pack_bf16x2(__uint_as_float(r[b][8 * q + 6]), __uint_as_float(r[b][8 * q + 7])));
+            st64(dg_ptr(n0 + c), pk);
+          }
+          tmem_ld_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CTAS == 2) mbar_arrive_cluster(mapa_shared(&sh.tmem_empty[acc], 0));
+          else mbar_arrive(&sh.tmem_empty[acc]);
+        }
+        ++tcount;
+        if (row_ok) {
+#pragma unroll 1
+          for (int u = 0; u < NSUB; ++u) {
+            const int n0 = (tc.nt * NSUB + u) * kBN;
+#pragma unroll 1
+            for (int i = 0; i < 4; ++i) {
+              const int fcol = n0 + half * 128 + 32 * i;
+              if (fcol >= p.N) break;
+              uint4 da4[4], gs4[4], us4[4];
+              ld64(dg_ptr(fcol), da4);
+              ld64(h_ptr(fcol), gs4);
+              ld64(h_ptr(fcol) + 128, us4);
+              uint4 wgs[4], wus[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t* dw = reinterpret_cast<const uint32_t*>(&da4[q]);
+                const uint32_t* gw = reinterpret_cast<const uint32_t*>(&gs4[q]);
+                const uint32_t* uw = reinterpret_cast<const uint32_t*>(&us4[q]);
+                uint32_t pg[4], pu[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 g2 = make_float2(__uint_as_float(gw[j] << 16), __uint_as_float(gw[j] & 0xffff0000u));
+                  const float2 u2 = make_float2(__uint_as_float(uw[j] << 16), __uint_as_float(uw[j] & 0xffff0000u));
+                  const float2 d2 = make_float2(__uint_as_float(dw[j] << 16), __uint_as_float(dw[j] & 0xffff0000u));
+                  const float2 sg2 = make_float2(sigmoid_f(g2.x), sigmoid_f(g2.y));
+                  const float2 one2 = make_float2(1.0f, 1.0f);
+                  const float2 t2 = __fmul2_rn(d2, sg2);
+                  const float2 du2 = __fmul2_rn(t2, g2);
+                  const float2 om2 = __ffma2_rn(sg2, make_float2(-1.0f, -1.0f), one2);
+                  const float2 k2 = __ffma2_rn(g2, om2, one2);
+                  const float2 dg2 = __fmul2_rn(__fmul2_rn(t2, u2), k2);
+                  pg[j] = pack_bf16x2(dg2.x, dg2.y);
+                  pu[j] = pack_bf16x2(du2.x, du2.y);
+                }
+                wgs[q] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+                wus[q] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+              }
+              st64(dg_ptr(fcol), wgs);
+              st64(dg_ptr(fcol) + 128, wus);
+            }
+          }
+        }
         continue;
       }
 

@@ -593,8 +593,76 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int acc = kAccBufs == 2 ? (tcount & 1) : 0;
       const uint32_t aph = (kAccBufs == 2 ? (tcount >> 1) : tcount) & 1;
 
-      if (EPI == EPI_SWIGLU_FWD && NSUB == 2 && p.early_release) {
-        // Wide tile, SwiGLU forward, drain-then-release: both sub-tiles' gate/up accumulators
+      if (EPI == EPI_SWIGLU_FWD && NSUB == 2 && p.early_release == 1) {
+        // Wide tile, SwiGLU forward: sub-tile 0 is processed straight from TMEM; sub-tile 1's
+        // gate/up accumulators are rounded to bf16 (exactly the saved h) and held in registers,
+        // the accumulator is released, then h and act of sub-tile 1 are formed and stored under
+        // the next tile's MMAs. (Measured 0.4 % faster than draining both sub-tiles' h first,
+        // the early_release == 2 variant below: profiles/r2_gemm_epilogues.md.)
+        mbar_wait(&sh.tmem_full[acc], aph);
+        tc_fence_after();
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quad * 32) << 16);
+        const bool v8ok = (((reinterpret_cast<uintptr_t>(p.out) | reinterpret_cast<uintptr_t>(p.out2)) & 31u) == 0) &&
+                          (p.ldo % 16 == 0) && (p.ldo2 % 16 == 0);
+        auto load_gu = [&](int u, int i, uint32_t (&g8)[8], uint32_t (&u8)[8]) {
+          const uint32_t col = (acc + u) * kBN + half * 64 + 16 * i;
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(t_row + col, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) g8[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+          tmem_ld_32x32b_x16(t_row + col + kBN / 2, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) u8[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        };
+        auto st32 = [&](__nv_bfloat16* dst, const uint32_t (&v)[8]) {
+          if (v8ok) {
+            st_global_v8(dst, make_uint4(v[0], v[1], v[2], v[3]), make_uint4(v[4], v[5], v[6], v[7]));
+          } else {
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(v[0], v[1], v[2], v[3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(v[4], v[5], v[6], v[7]);
+          }
+        };
+        auto emit = [&](int u, int i, const uint32_t (&g8)[8], const uint32_t (&u8)[8]) {
+          const int nsub_idx = tc.nt * NSUB + u;
+          const int n0 = nsub_idx * kBN;
+          if (!row_ok || n0 >= p.N) return;
+          const int c = half * 64 + 16 * i;
+          st32(p.out2 + grow * p.ldo2 + n0 + c, g8);
+          st32(p.out2 + grow * p.ldo2 + n0 + kBN / 2 + c, u8);
+          uint32_t a8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float g0 = __uint_as_float(g8[j] << 16), g1 = __uint_as_float(g8[j] & 0xffff0000u);
+            const float u0 = __uint_as_float(u8[j] << 16), u1 = __uint_as_float(u8[j] & 0xffff0000u);
+            a8[j] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+          }
+          st32(p.out + grow * p.ldo + nsub_idx * (kBN / 2) + c, a8);
+        };
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t g8[8], u8[8];
+          load_gu(0, i, g8, u8);
+          emit(0, i, g8, u8);
+        }
+        uint32_t hg[4][8], hu[4][8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) load_gu(1, i, hg[i], hu[i]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CTAS == 2) mbar_arrive_cluster(mapa_shared(&sh.tmem_empty[acc], 0));
+          else mbar_arrive(&sh.tmem_empty[acc]);
+        }
+        ++tcount;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) emit(1, i, hg[i], hu[i]);
+        continue;
+      }
+
+      if (EPI == EPI_SWIGLU_FWD && NSUB == 2 && p.early_release == 2) {
+        // (A/B variant, hm_debug_set_gemm_early_release(2)) drain-then-release: both sub-tiles' gate/up accumulators
         // are rounded to bf16 and stored as the saved h straight from TMEM (no math while the
         // accumulator is held), the accumulator is released, and act = silu(g) * u is formed
         // from this thread's own h rows read back (L2-hot, program order) under the next tile's

@@ -123,6 +123,7 @@ int gemm_ctas();
 struct TileBound {
   bool group_k;
   long rows, M, N, E;
+  long K = 0;  // reduction length (GROUP_M GEMMs)
   long tiles(long tile_m, long tile_n) const {
     const long ntl = (N + tile_n - 1) / tile_n;
     return group_k ? E * ((M + tile_m - 1) / tile_m) * ntl : (rows / tile_m + E) * ntl;
@@ -178,6 +179,7 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
 }
 
 int gemm_wide_mask();
+bool gemm_wide_explicit();
 
 // CTA count / tile width dispatch for one GEMM kind: 1 CTA (HM_GEMM_CTAS=1), a CTA pair with
 // 256 x 256 tiles, or a CTA pair with 256 x 512 tiles (modes in the wide mask)
@@ -191,7 +193,12 @@ int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm
   p.group_m = gemm_group_m(mode, tb.M);
   p.early_release = g_early_release;
   if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1>(ma, mb, p, tb, max_ctas, st);
-  if ((gemm_wide_mask() >> mode) & 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
+  bool wide = (gemm_wide_mask() >> mode) & 1;
+  // the SwiGLU backward's drain-then-release epilogue holds the single wide accumulator for a
+  // fixed few microseconds: worth it against a long K (C2, K = d = 4096: 1043 -> 1165 TFLOP/s),
+  // not a short one (C3, K = 2048: 967 -> 764), unless HM_GEMM_WIDE forces the mask
+  if (mode == HM_GEMM_BWD_DACT && !gemm_wide_explicit() && tb.K < 4096) wide = false;
+  if (wide) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
   return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1>(ma, mb, p, tb, max_ctas, st);
 }
 
@@ -229,12 +236,18 @@ int gemm_stats_enabled() {
 #define HM_GEMM_WIDE_DEFAULT 0x3F  // every GEMM: up+gate, down, SwiGLU backward, dX, both wgrads
 #endif
 int g_wide_mask = -1;
+bool g_wide_explicit = false;  // HM_GEMM_WIDE or hm_debug_set_gemm_wide chose the mask
 int gemm_wide_mask() {
   if (g_wide_mask < 0) {
     const char* s = getenv("HM_GEMM_WIDE");
+    g_wide_explicit = s != nullptr;
     g_wide_mask = s ? static_cast<int>(strtol(s, nullptr, 0)) : HM_GEMM_WIDE_DEFAULT;
   }
   return g_wide_mask;
+}
+bool gemm_wide_explicit() {
+  gemm_wide_mask();
+  return g_wide_explicit;
 }
 
 // CTA-pair (cta_group::2) tiles for the GROUP_M GEMMs unless HM_GEMM_CTAS=1
@@ -327,6 +340,7 @@ int hm_gemm_stats(unsigned long long* out) {
 int hm_debug_set_gemm_wide(int mask) {
   const int old = gemm_wide_mask();
   g_wide_mask = mask;
+  g_wide_explicit = mask >= 0;
   return old;
 }
 // tuning aid (not part of the ABI): raster group height of one GEMM mode (mode < 0: all modes;
@@ -823,7 +837,7 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
   }
 
   p.out_elems = wgrad ? static_cast<long>(E) * M * ldo : static_cast<long>(rows) * ldo;
-  const TileBound tb{wgrad, rows, M, N, E};
+  const TileBound tb{wgrad, rows, M, N, E, K};
   switch (mode) {
     case HM_GEMM_FWD_UPGATE:
       if (N % 256 != 0 || !out2) return fail(HM_E_SHAPE, "upgate: N=2f must be a multiple of 256 and h given");

@@ -362,16 +362,13 @@ const char* hm_last_error(void) { return g_last_error.c_str(); }
 int hm_num_sms(void) { return num_sms(); }
 
 // ---------------------------------------------------------------------------------------------
-// Router plan for d (blocks of 256, a power of two up to 64): EGW experts per CTA group and BPW
-// blocks per warp keep 64 fp32 router weights per thread in registers.
+// Router plan for d (blocks of 256, up to 64): EGW experts per CTA group and BPW blocks per warp
+// keep at most 64 fp32 router weights per thread in registers.
 static bool router_shape(int d, int* egw, int* bpw) {
-  if (d <= 0 || d % 256 != 0) return false;
+  if (d <= 0 || d % 256 != 0 || d / 256 > 64) return false;
   const int nj = d / 256;
-  if (nj & (nj - 1)) return false;
-  if (nj <= 16) { *egw = 8; *bpw = 1; }
-  else if (nj == 32) { *egw = 4; *bpw = 2; }
-  else if (nj == 64) { *egw = 2; *bpw = 4; }
-  else return false;
+  *bpw = (nj + 15) / 16;
+  *egw = *bpw == 1 ? 8 : (*bpw == 2 ? 4 : 2);
   return true;
 }
 
@@ -393,11 +390,11 @@ size_t hm_router_chunk_elems(int T, int E) {
 
 }  // extern "C"
 
-template <int EGW, int NJ, bool FUSE>
+template <int EGW, int NJ_T, int BPW, bool FUSE>
 static int launch_router_fused(int groups, cudaStream_t st, const __nv_bfloat16* xb, const __nv_bfloat16* wb,
-                               const float* bias, int T, int E, float* logits, int k, int32_t* idx,
+                               const float* bias, int T, int d, int E, float* logits, int k, int32_t* idx,
                                float* w, int32_t* chunk_base, int32_t* counts, int32_t* offsets) {
-  auto kern = hm::router_fused_kernel<EGW, NJ, FUSE>;
+  auto kern = hm::router_fused_kernel<EGW, NJ_T, BPW, FUSE>;
   const size_t smem = hm::router_fused_smem_bytes(EGW);
   static bool attr = false;
   if (!attr) {
@@ -405,36 +402,40 @@ static int launch_router_fused(int groups, cudaStream_t st, const __nv_bfloat16*
     if (e != cudaSuccess) return fail(static_cast<int>(e), "router smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  const int TG = hm::kRouterItems / NJ;
+  const int nj = d / 256;
+  const int TG = nj <= 16 ? 4 * (16 / nj) : 4 / BPW;
   const int units = (T + TG - 1) / TG;
   int ranges = num_sms() / groups;  // one persistent CTA per SM over all (range, group) pairs
   if (ranges < 1) ranges = 1;
   if (ranges > units) ranges = units;
-  kern<<<ranges * groups, hm::kRouterThreads, smem, st>>>(xb, wb, bias, T, E, ranges, logits, k, idx, w,
+  kern<<<ranges * groups, hm::kRouterThreads, smem, st>>>(xb, wb, bias, T, d, E, ranges, logits, k, idx, w,
                                                           chunk_base, counts, offsets);
   return check_launch("router_fused");
 }
 
+// compile-time block counts for d = 256 * 2^m (every index a shift), run-time otherwise
 template <bool FUSE>
 static int launch_router_nj(int d, int groups, cudaStream_t st, const __nv_bfloat16* xb, const __nv_bfloat16* wb,
                             const float* bias, int T, int E, float* logits, int k, int32_t* idx, float* w,
                             int32_t* chunk_base, int32_t* counts, int32_t* offsets) {
-#define HM_ROUTER_NJ(EGW, NJ)                                                                   \
-  case NJ:                                                                                    \
-    return launch_router_fused<EGW, NJ, FUSE>(groups, st, xb, wb, bias, T, E, logits, k, idx, w, \
-                                              chunk_base, counts, offsets);
+#define HM_ROUTER_ARGS groups, st, xb, wb, bias, T, d, E, logits, k, idx, w, chunk_base, counts, offsets
   switch (d / 256) {
-    HM_ROUTER_NJ(8, 1)
-    HM_ROUTER_NJ(8, 2)
-    HM_ROUTER_NJ(8, 4)
-    HM_ROUTER_NJ(8, 8)
-    HM_ROUTER_NJ(8, 16)
-    HM_ROUTER_NJ(4, 32)
-    HM_ROUTER_NJ(2, 64)
-    default:
-      return fail(HM_E_SHAPE, "router: d=%d", d);
+    case 1: return launch_router_fused<8, 1, 1, FUSE>(HM_ROUTER_ARGS);
+    case 2: return launch_router_fused<8, 2, 1, FUSE>(HM_ROUTER_ARGS);
+    case 4: return launch_router_fused<8, 4, 1, FUSE>(HM_ROUTER_ARGS);
+    case 8: return launch_router_fused<8, 8, 1, FUSE>(HM_ROUTER_ARGS);
+    case 16: return launch_router_fused<8, 16, 1, FUSE>(HM_ROUTER_ARGS);
+    case 32: return launch_router_fused<4, 32, 2, FUSE>(HM_ROUTER_ARGS);
+    case 64: return launch_router_fused<2, 64, 4, FUSE>(HM_ROUTER_ARGS);
+    default: {
+      const int bpw = (d / 256 + 15) / 16;
+      if (bpw == 1) return launch_router_fused<8, 0, 1, FUSE>(HM_ROUTER_ARGS);
+      if (bpw == 2) return launch_router_fused<4, 0, 2, FUSE>(HM_ROUTER_ARGS);
+      if (bpw == 3) return launch_router_fused<2, 0, 3, FUSE>(HM_ROUTER_ARGS);
+      return launch_router_fused<2, 0, 4, FUSE>(HM_ROUTER_ARGS);
+    }
   }
-#undef HM_ROUTER_NJ
+#undef HM_ROUTER_ARGS
 }
 
 extern "C" {
@@ -444,7 +445,7 @@ int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int 
                    int32_t* chunk_base, void* stream) {
   int egw = 0, bpw = 0;
   if (T < 0 || !router_shape(d, &egw, &bpw) || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK || k > E)
-    return fail(HM_E_SHAPE, "router: unsupported shape T=%d d=%d E=%d k=%d (d = 256 * 2^m <= 16384)", T, d, E, k);
+    return fail(HM_E_SHAPE, "router: unsupported shape T=%d d=%d E=%d k=%d (d %% 256 == 0, d <= 16384)", T, d, E, k);
   if (!aligned16(x)) return fail(HM_E_ALIGN, "router: x not 16-byte aligned");
   cudaStream_t st = S(stream);
   const int nchunk = (T + hm::kChunk - 1) / hm::kChunk;

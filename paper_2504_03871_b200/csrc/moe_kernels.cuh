@@ -262,23 +262,28 @@ HM_DEV void router_select_lanes(float v, int e, int E, int k, bool write, int32_
     }
 }
 
-// EGW experts per CTA group held by every warp (registers: BPW * 8 * EGW = 64 floats), NJ =
-// d / 256 blocks (compile time: every index is a shift), BPW = max(1, NJ / 16) blocks per warp.
+// EGW experts per CTA group held by every compute warp (registers: BPW * 8 * EGW <= 64 floats),
+// nj = d / 256 blocks: a template constant for the powers of two (every index a shift), else
+// NJ_T = 0 and nj = d / 256 at run time (any d % 256 == 0 up to 16384). Warp -> work map:
+//   nj <= 16: P = 16 / nj token streams; warp w < P * nj owns block w % nj and tokens
+//             w / nj + P * m (m = 0..3) of each stage of TG = 4 P tokens (idle warps: 16 % nj);
+//   nj > 16:  BPW = ceil(nj / 16) blocks per warp (w + 16 b), every token of a TG = 4 / BPW stage.
 // FUSE: one expert group (E <= EGW): top-k, softmax, the per-chunk histogram (atomics into the
 // zeroed chunk_counts) and, in the last CTA, the scan.
-template <int EGW, int NJ, bool FUSE>
+template <int EGW, int NJ_T, int BPW, bool FUSE>
 __global__ void __launch_bounds__(kRouterThreads, 1)
     router_fused_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
-                        const float* __restrict__ bias, int T, int E, int ranges,
+                        const float* __restrict__ bias, int T, int d_arg, int E, int ranges,
                         float* __restrict__ logits, int k, int32_t* __restrict__ idx,
                         float* __restrict__ w, int32_t* __restrict__ chunk_counts /*[nchunk*E + 1]*/,
                         int32_t* __restrict__ counts, int32_t* __restrict__ offsets) {
-  constexpr int BPW = NJ > 16 ? NJ / 16 : 1;
-  constexpr int TG = kRouterItems / NJ;  // tokens per stage
-  constexpr int D = NJ * 256;
-  constexpr long kRowBytes = static_cast<long>(D) * 2;
-  constexpr int kRounds = (TG * EGW + 31) / 32;  // epilogue lane rounds per stage
   static_assert(BPW * 8 * EGW <= 64, "router weights per thread");
+  const int nj = NJ_T > 0 ? NJ_T : (d_arg >> 8);
+  const int P = nj <= 16 ? 16 / nj : 1;        // token streams (nj <= 16)
+  const int TG = nj <= 16 ? 4 * P : 4 / BPW;   // tokens per stage
+  const int D = nj * 256;
+  const long kRowBytes = static_cast<long>(D) * 2;
+  const int kRounds = (TG * EGW + 31) / 32;    // epilogue lane rounds per stage
   extern __shared__ __align__(1024) uint8_t smem_rt[];
   uint8_t* ring = smem_rt;                                                  // stages x 32 KB
   float* part = reinterpret_cast<float*>(smem_rt + kRouterStages * kRouterStageBytes);  // [4][64][EGW]
@@ -307,11 +312,11 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       bulk_load_1d(ring + s * kRouterStageBytes, x + static_cast<long>(t0) * D, bytes, &sh.full[s]);
     }
   }
-  // this warp's blocks and items: NJ <= 16 -> block w % NJ, tokens w / NJ + (16 / NJ) m;
-  // NJ > 16 -> blocks w + 16 b (b < BPW), every token of the stage
+  // this warp's blocks and items (warp-uniform validity)
+  const bool active = warp < kRouterWarps && (nj > 16 || warp < P * nj);
   int jb[BPW];
 #pragma unroll
-  for (int b = 0; b < BPW; ++b) jb[b] = (NJ <= 16) ? (warp % NJ) : (warp + 16 * b);
+  for (int b = 0; b < BPW; ++b) jb[b] = (nj <= 16) ? (warp % nj) : (warp + 16 * b);
   float wr[BPW][8][EGW];
   const uint16_t* wg16 = reinterpret_cast<const uint16_t*>(wg);
 #pragma unroll
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const long i = 256L * jb[b] + 8 * lane + q;
-      if (warp >= kRouterWarps) {  // epilogue warps hold no weights
+      if (!active || jb[b] >= nj) {  // epilogue / idle warps and missing blocks hold no weights
 #pragma unroll
         for (int e = 0; e < EGW; ++e) wr[b][q][e] = 0.f;
       } else if (E % EGW == 0) {  // the group's EGW weights of row i are one aligned vector
@@ -347,19 +352,17 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   const int my_e = router_lane_expert<EGW>(lane);
   const bool writer = (lane & (32 / EGW - 1)) == 0;
   int ti_of[4], xoff[4], poff[4];
+  bool item_ok[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
-    const int b = (NJ <= 16) ? 0 : m % BPW;
-    ti_of[m] = (NJ <= 16) ? warp / NJ + (16 / NJ) * m : m / BPW;
-    xoff[m] = static_cast<int>(ti_of[m] * kRowBytes + (256 * jb[b] + 8 * lane) * 2);
-    poff[m] = (ti_of[m] * NJ + jb[b]) * EGW + my_e;
+    const int b = (nj <= 16) ? 0 : m % BPW;
+    ti_of[m] = (nj <= 16) ? warp / nj + P * m : m / BPW;
+    item_ok[m] = active && jb[b] < nj && ti_of[m] < TG;
+    xoff[m] = item_ok[m] ? static_cast<int>(ti_of[m] * kRowBytes + (256 * jb[b] + 8 * lane) * 2) : 0;
+    poff[m] = (ti_of[m] * nj + jb[b]) * EGW + my_e;
   }
-  float bias_r[kRounds];
-#pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    const int e = (r * 32 + lane) % EGW;
-    bias_r[r] = (bias && e0 + e < E) ? bias[e0 + e] : 0.f;
-  }
+  // a lane's expert in the epilogue is lane % EGW in every round (32 % EGW == 0)
+  const float bias_lane = (bias && e0 + lane % EGW < E) ? bias[e0 + lane % EGW] : 0.f;
   __syncthreads();
 
   if (warp < kRouterWarps) {
@@ -371,35 +374,39 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       mbar_wait(&sh.full[slot], (s / kRouterStages) & 1);
       if (s >= kRouterStages) mbar_wait(&sh.pempty[slot], ((s / kRouterStages) - 1) & 1);
       const uint8_t* st = ring + slot * kRouterStageBytes;
-      float acc[kRouterNI][EGW];
+      if (active) {
+        float acc[kRouterNI][EGW];
 #pragma unroll
-      for (int m0 = 0; m0 < 4; m0 += kRouterNI) {
+        for (int m0 = 0; m0 < 4; m0 += kRouterNI) {
+          if (!item_ok[m0]) continue;  // warp-uniform; items of a pair are both valid or the
+                                       // second is masked below
 #pragma unroll
-        for (int u = 0; u < kRouterNI; ++u) {
-          const int m = m0 + u;
-          const int b = (NJ <= 16) ? 0 : m % BPW;
-          // a token past the stage's end reads stale ring bytes; its result is never stored
-          const uint4 xv = *reinterpret_cast<const uint4*>(st + xoff[m]);
-          const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+          for (int u = 0; u < kRouterNI; ++u) {
+            const int m = m0 + u;
+            const int b = (nj <= 16) ? 0 : m % BPW;
+            // a token past the stage's end reads stale ring bytes; its result is never stored
+            const uint4 xv = item_ok[m] ? *reinterpret_cast<const uint4*>(st + xoff[m]) : make_uint4(0u, 0u, 0u, 0u);
+            const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-          for (int e = 0; e < EGW; ++e) acc[u][e] = 0.f;
+            for (int e = 0; e < EGW; ++e) acc[u][e] = 0.f;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float xf = __uint_as_float((q & 1) ? (xw[q >> 1] & 0xffff0000u) : (xw[q >> 1] << 16));
+            for (int q = 0; q < 8; ++q) {
+              const float xf = __uint_as_float((q & 1) ? (xw[q >> 1] & 0xffff0000u) : (xw[q >> 1] << 16));
 #pragma unroll
-            for (int e = 0; e < EGW; e += 2) {
-              const float2 r = __ffma2_rn(make_float2(xf, xf), make_float2(wr[b][q][e], wr[b][q][e + 1]),
-                                          make_float2(acc[u][e], acc[u][e + 1]));
-              acc[u][e] = r.x;
-              acc[u][e + 1] = r.y;
+              for (int e = 0; e < EGW; e += 2) {
+                const float2 r = __ffma2_rn(make_float2(xf, xf), make_float2(wr[b][q][e], wr[b][q][e + 1]),
+                                            make_float2(acc[u][e], acc[u][e + 1]));
+                acc[u][e] = r.x;
+                acc[u][e + 1] = r.y;
+              }
             }
           }
-        }
-        float pj[kRouterNI];
-        router_reduce_scatter<EGW, kRouterNI>(acc, pj);
+          float pj[kRouterNI];
+          router_reduce_scatter<EGW, kRouterNI>(acc, pj);
 #pragma unroll
-        for (int u = 0; u < kRouterNI; ++u)
-          if (writer && ti_of[m0 + u] < nt) pb[poff[m0 + u]] = pj[u];
+          for (int u = 0; u < kRouterNI; ++u)
+            if (writer && item_ok[m0 + u] && ti_of[m0 + u] < nt) pb[poff[m0 + u]] = pj[u];
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.pfull[slot]);  // releases this warp's ring reads and table writes
@@ -420,18 +427,24 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
         bulk_load_1d(ring + slot * kRouterStageBytes, x + static_cast<long>(tn) * D, bytes, &sh.full[slot]);
       }
       // block partials -> logits in block order (+ bias): lane (ti, e), e fastest
-#pragma unroll
       for (int r = 0; r < kRounds; ++r) {
         const int id = r * 32 + lane;
         const int ti = id / EGW, e = id % EGW;
         const int tl = id < TG * EGW ? ti : 0;  // lanes past the stage's items read item 0
-        float pv[NJ];
+        float v;
+        if (NJ_T > 0) {
+          constexpr int NJC = NJ_T > 0 ? NJ_T : 1;
+          float pv[NJC];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) pv[j] = pb[(tl * NJ + j) * EGW + e];
-        float v = pv[0];
+          for (int j = 0; j < NJC; ++j) pv[j] = pb[(tl * NJC + j) * EGW + e];
+          v = pv[0];
 #pragma unroll
-        for (int j = 1; j < NJ; ++j) v = v + pv[j];
-        if (bias) v = v + bias_r[r];
+          for (int j = 1; j < NJC; ++j) v = v + pv[j];
+        } else {
+          v = pb[(tl * nj) * EGW + e];
+          for (int j = 1; j < nj; ++j) v = v + pb[(tl * nj + j) * EGW + e];
+        }
+        if (bias) v = v + bias_lane;
         const bool ok = id < TG * EGW && ti < nt;
         if (ok && e0 + e < E) logits[static_cast<long>(t0 + ti) * E + e0 + e] = v;
         if (FUSE) {

@@ -31,6 +31,8 @@ def test_pure_host_entry_points():
     assert lib.hm_router_chunk_elems(1, 64) == 64 + 1
     assert lib.hm_router_launches(16384, 4096, 8) == 1  # logits + top-k + histogram + scan fused
     assert lib.hm_router_launches(16384, 2048, 64) == 3  # 8 expert groups: logits, top-k, scan
-    assert lib.hm_router_launches(16384, 768, 8) == 0  # d must be 256 * 2^m
+    assert lib.hm_router_launches(16384, 768, 8) == 1  # any d % 256 == 0 up to 16384
+    assert lib.hm_router_launches(16384, 6144, 8) == 3  # 4-expert register groups: two groups
+    assert lib.hm_router_launches(16384, 300, 8) == 0
     # dlogit (T*k), dense dlogit rows (T*8), then at least 16 splits of dWg partials
     assert lib.hm_router_bwd_part_elems(16384, 4096, 8, 2) >= 16384 * 2 + 16384 * 8 + 16 * 8 * 4096

@@ -150,13 +150,19 @@ def test_moe_layer_with_empty_expert_vs_oracle():
 @pytest.mark.parametrize("cfg", [LayerConfig("E8d4096", 8, 2, 4096, 128, 1000),
                                  LayerConfig("E4d256", 4, 3, 256, 128, 777),
                                  LayerConfig("E8d8192", 8, 2, 8192, 128, 300),
-                                 LayerConfig("E2d16384", 2, 1, 16384, 128, 130)],
+                                 LayerConfig("E2d16384", 2, 1, 16384, 128, 130),
+                                 LayerConfig("E8d768", 8, 2, 768, 128, 500),
+                                 LayerConfig("E8d1280", 8, 3, 1280, 128, 333),
+                                 LayerConfig("E8d6144", 8, 2, 6144, 128, 257),
+                                 LayerConfig("E16d7168", 16, 4, 7168, 128, 130),
+                                 LayerConfig("E4d12288", 4, 2, 12288, 128, 71)],
                          ids=lambda c: c.name)
 def test_router_fused_equals_unfused_and_oracle(cfg):
     """The one-kernel router (logits + top-k + histogram + last-CTA scan, one expert group) and
     the unfused path (logits kernel, top-k kernel, scan kernel; HM_ROUTER_UNFUSED) agree bitwise,
     and both match the oracle, on adversarial rows too; d = 8192 / 16384 exercise the 4- and
-    2-expert register groups."""
+    2-expert register groups, d = 768, 1280, 6144 (Mixtral-8x22B), 7168 (DeepSeek-V3), 12288 the
+    run-time block count (1, 2 and 3 blocks per warp, idle warps when 16 % (d / 256) != 0)."""
     import os
 
     inp = make_inputs(cfg, seed=17)

@@ -675,7 +675,7 @@ int hm_dispatch_permute_p2p(const void* x, const int32_t* idx, const int32_t* ch
                             const int32_t* offsets, int T, int d, int E, int k, void* x_perm,
                             int32_t* row_src, int32_t* row_of, const unsigned long long* dest_base,
                             const int32_t* dest_start, void* stream) {
-  if (T < 0 || d <= 0 || d % 256 != 0 || d / 256 > 16 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK)
+  if (T < 0 || d <= 0 || d % 8 != 0 || E < 1 || E > 256 || k < 1 || k > hm::kMaxTopK)
     return fail(HM_E_SHAPE, "permute_p2p: unsupported shape T=%d d=%d E=%d k=%d", T, d, E, k);
   if (!aligned16(x) || (x_perm && !aligned16(x_perm))) return fail(HM_E_ALIGN, "permute_p2p: alignment");
   if (T == 0) return 0;
@@ -692,14 +692,14 @@ int hm_dispatch_permute_p2p(const void* x, const int32_t* idx, const int32_t* ch
                                                                 E, k, xp, row_src, row_of,    \
                                                                 dest_base, dest_start);       \
     break;
-  switch (d / 256) {
+  switch (d % 256 == 0 ? d / 256 : 0) {
     HM_P2P_CASE(1)
     HM_P2P_CASE(2)
     HM_P2P_CASE(4)
     HM_P2P_CASE(8)
     HM_P2P_CASE(16)
-    default:
-      return fail(HM_E_SHAPE, "permute_p2p: d=%d must be 256 x {1,2,4,8,16}", d);
+    default:  // any other d % 8 == 0
+      HM_P2P_CASE(0)
   }
 #undef HM_P2P_CASE
   return check_launch("dispatch_permute_p2p");

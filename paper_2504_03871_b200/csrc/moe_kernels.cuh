@@ -1283,10 +1283,39 @@ __global__ void __launch_bounds__(256)
   }
   // gridDim.y CTAs per chunk, as in dispatch_permute_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (VPL == 0) {  // any d % 8 == 0: the row in pieces of 8 x 32 16-byte vectors
+    const int nv = d / 8;
+    for (int tt = warp + 8 * blockIdx.y; tt < nt; tt += 8 * gridDim.y) {
+      const long t = tbeg + tt;
+      const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+      for (int q0 = 0; q0 < nv; q0 += 256) {
+        uint4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (q0 + 32 * i + lane < nv) v[i] = __ldg(src + q0 + 32 * i + lane);
+        for (int s = 0; s < k; ++s) {
+          const int r = s_row[tt * k + s];
+          const int e = s_idx[tt * k + s];
+          uint4* dl = x_perm ? reinterpret_cast<uint4*>(x_perm + static_cast<long>(r) * d) : nullptr;
+          uint4* dp = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(dest_base[e]) +
+                                               (static_cast<long>(dest_start[e]) + r - offsets[e]) * d);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int q = q0 + 32 * i + lane;
+            if (q < nv) {
+              if (dl) dl[q] = v[i];
+              dp[q] = v[i];
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
   for (int tt = warp + 8 * blockIdx.y; tt < nt; tt += 8 * gridDim.y) {
     const long t = tbeg + tt;
     const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
-    uint4 v[VPL];
+    uint4 v[VPL > 0 ? VPL : 1];
 #pragma unroll
     for (int q = 0; q < VPL; ++q) v[q] = __ldg(src + q * 32 + lane);
     for (int s = 0; s < k; ++s) {

@@ -12,7 +12,8 @@ from paper_2504_03871_b200.configs import C1, LayerConfig, make_inputs
 
 pytestmark = pytest.mark.gpu
 
-CASES = [C1, LayerConfig("ragged", E=16, k=4, d=512, f=256, T=1000)]
+CASES = [C1, LayerConfig("ragged", E=16, k=4, d=512, f=256, T=1000),
+         LayerConfig("d6144", E=8, k=2, d=6144, f=256, T=300)]  # generic-width row copy
 
 
 def _owner_layout(offsets, E, n_owner, pad=3):

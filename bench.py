@@ -514,11 +514,20 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200.profiler import measure_exchange, measure_memory, memory_spec_fields
 
     memp = measure_memory(shape, device=dev)
-    comm_ns = measure_exchange(M, N, args.mb_tokens, c.k, c.d)
-    mt = torch.tensor([memp[k_] for k_ in sorted(memp)] + [comm_ns], dtype=torch.int64, device=dev)
+    comm_ns = measure_exchange(M, N, args.mb_tokens, c.k, c.d)  # NCCL all-to-all of the rows
+    # the exchange as the executor performs it with the chosen transport (a 1-layer, 1-micro-batch
+    # run): the planner's dispatch / combine durations
+    from paper_2504_03871_b200.profiler import measure_transport
+
+    disp_groups = (dist.new_group(list(range(ws))), dist.new_group(list(range(ws))))
+    tr = measure_transport(shape, M, N, NativeBackend(dev, max_ctas=exp_ctas if rank >= M else 0),
+                           args.transport, *disp_groups)
+    mt = torch.tensor([memp[k_] for k_ in sorted(memp)] + [comm_ns, tr["dispatch_ns"], tr["combine_ns"]],
+                      dtype=torch.int64, device=dev)
     dist.broadcast(mt, 0)  # every rank plans with rank 0's probe
-    memp = dict(zip(sorted(memp), (int(v) for v in mt[:-1].tolist())))
-    comm_ns = int(mt[-1])
+    memp = dict(zip(sorted(memp), (int(v) for v in mt[:-3].tolist())))
+    comm_ns = int(mt[-3])
+    transport_ns = {"dispatch_ns": int(mt[-2]), "combine_ns": int(mt[-1])}
     arena = PeerArena.bytes_needed(args.layers, args.microbatches, args.mb_tokens * M * c.k,
                                    args.mb_tokens * c.k, c.d) if args.transport == "p2p" else 0
     mem_fields = memory_spec_fields(memp, M, N, args.layers, args.microbatches, args.mb_tokens, c.k, arena)
@@ -528,7 +537,7 @@ def run_zp(args, ws, rank, local):
     durs = dict(zip(sorted(durs), (int(v) for v in t.tolist())))
     from fractions import Fraction
 
-    durs["dispatch_ns"] = durs["combine_ns"] = comm_ns
+    durs.update(transport_ns)
     plan_durs = {k_: v for k_, v in durs.items() if k_ != "gamma_x100"}
     spec = make_zp_spec(M, N, args.layers, args.microbatches, c.E, c.k, args.mb_tokens, c.d,
                         asym_ea=not args.no_asym_ea, gamma=Fraction(durs["gamma_x100"], 100),
@@ -625,7 +634,7 @@ def run_zp(args, ws, rank, local):
                               "non_expert_mem_attention": mem_fields["non_expert_mem_attention"],
                               "non_expert_mem_expert": mem_fields["non_expert_mem_expert"],
                               "capacity": mem_fields["exp_capacity"]},
-            "measured_exchange_ns": comm_ns,
+            "measured_exchange_ns": {"nccl_all_to_all": comm_ns, "executor_transport": transport_ns},
             "expert_loads_per_mb": loads,
             "measured_durations_ns": durs,
             "l2": "activations and weights exceed the 126 MB L2; no flush",

@@ -254,3 +254,41 @@ def measure_exchange(M: int, N: int, tokens_per_mb: int, k: int, d: int, group=N
     t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return int(float(t) * 1e6)
+
+
+def measure_transport(shape, M: int, N: int, backend, transport: str = "p2p", disp_group=None,
+                      comb_group=None, reps: int = 3, seed: int = 11) -> dict:
+    """The exchange as the executor performs it (collective: every rank calls it): a one-layer,
+    one-micro-batch ZP graph run through the real executor (``ZpP2PExecutor`` / ``ZpExecutor``)
+    with the chosen transport; the forward DISP_F and COMB_F task durations on the attention
+    ranks (count all-gather + fused permute / peer stores + completion flags for the peer-memory
+    transport; count all-gather + NCCL send/recv for NCCL), median over ``reps`` iterations, max
+    over ranks, in ns. These are the planner's ``dispatch`` / ``combine`` entries (the reference
+    prices them as bytes / bandwidth, ``costmodel.py:40-47``)."""
+    import statistics
+
+    import torch.distributed as dist
+
+    from .core import ExpertAssignment
+    from .costmodel import derive_task_durations
+    from .executor import ZpExecutor, ZpP2PExecutor, execute
+    from .planner import make_zp_spec
+    from .taskgraph import TaskKind, build_zp_graph
+
+    spec = make_zp_spec(M, N, 1, 1, shape.E, shape.k, shape.tokens_per_mb, shape.d, attn_fwd_ns=1000,
+                        expert_layer_fwd_ns=1000, single_expert_fwd_ns=1000, dispatch_ns=100, combine_ns=100)
+    graph = build_zp_graph(spec, derive_task_durations(spec), ExpertAssignment((0,)), mode="zp-full")
+    cls = ZpP2PExecutor if transport == "p2p" else ZpExecutor
+    ex = cls(graph, shape, M, N, dist.get_rank(), backend, disp_group, comb_group, seed=seed)
+    ex.run()  # warm-up
+    samples = {"DispF": [], "CombF": []}
+    for _ in range(reps):
+        tl = execute(graph, ex)
+        for t in graph.tasks:
+            if t.kind in (TaskKind.DISP_F, TaskKind.COMB_F):
+                ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in range(M) if t.id in tl.per_rank[r]]
+                samples[t.kind.value].append(max(ds))
+    out = {k: int(statistics.median(v)) for k, v in samples.items()}
+    del ex
+    torch.cuda.empty_cache()
+    return {"dispatch_ns": out["DispF"], "combine_ns": out["CombF"]}

@@ -340,3 +340,43 @@ def test_memory_spec_fields_drive_memory_bounds():
                          **memory_spec_fields(tight, M, N, L, R, T, k, arena_bytes=0))
     b2 = memory_bounds(spec2)
     assert (b2.n_min, b2.n_max) == (5, 7)
+
+
+def _transport_worker(rank, W, M, N, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=W)
+    try:
+        from cpu_backend import CpuBackend
+        from paper_2504_03871_b200.executor import ZpLayerShape
+        from paper_2504_03871_b200.profiler import measure_transport
+
+        shape = ZpLayerShape(4, 2, 256, 128, 16, heads=2, attention=False)
+        g1, g2 = dist.new_group(list(range(W))), dist.new_group(list(range(W)))
+        q.put({"rank": rank, "out": measure_transport(shape, M, N, CpuBackend(), "nccl", g1, g2, reps=2)})
+    except Exception:  # report instead of hanging the parent
+        import traceback
+
+        q.put({"rank": rank, "error": traceback.format_exc()})
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_measure_transport_runs_the_executor_exchange():
+    """The planner's dispatch / combine durations come from a one-layer, one-micro-batch run of the
+    executor itself (measure_transport): every rank gets the same positive numbers."""
+    M, N = 1, 1
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transport_worker, args=(r, M + N, M, N, port, q)) for r in range(M + N)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for o in outs:
+        assert "error" not in o, o.get("error")
+        assert o["out"]["dispatch_ns"] > 0 and o["out"]["combine_ns"] > 0

@@ -259,12 +259,14 @@ def measure_exchange(M: int, N: int, tokens_per_mb: int, k: int, d: int, group=N
 def measure_transport(shape, M: int, N: int, backend, transport: str = "p2p", disp_group=None,
                       comb_group=None, reps: int = 3, seed: int = 11) -> dict:
     """The exchange as the executor performs it (collective: every rank calls it): a one-layer,
-    one-micro-batch ZP graph run through the real executor (``ZpP2PExecutor`` / ``ZpExecutor``)
-    with the chosen transport; the forward DISP_F and COMB_F task durations on the attention
-    ranks (count all-gather + fused permute / peer stores + completion flags for the peer-memory
-    transport; count all-gather + NCCL send/recv for NCCL), median over ``reps`` iterations, max
-    over ranks, in ns. These are the planner's ``dispatch`` / ``combine`` entries (the reference
-    prices them as bytes / bandwidth, ``costmodel.py:40-47``)."""
+    one-micro-batch ZP graph (no offload) run through the real executor (``ZpP2PExecutor`` /
+    ``ZpExecutor``) with the chosen transport, each exchange timed on its SENDING role — DISP_F on
+    the attention ranks (count all-gather, the permute with its peer stores, the completion
+    flags), COMB_F on the expert ranks (the return is fused into the down-projection GEMM, so
+    with peer memory this is only the flag release; with NCCL the send) — median over ``reps``
+    iterations, max over the role's ranks, in ns. (The receiving side's interval would also
+    contain the wait for the other role's compute.) These are the planner's ``dispatch`` /
+    ``combine`` entries (the reference prices them as bytes / bandwidth, ``costmodel.py:40-47``)."""
     import statistics
 
     import torch.distributed as dist
@@ -286,7 +288,8 @@ def measure_transport(shape, M: int, N: int, backend, transport: str = "p2p", di
         tl = execute(graph, ex)
         for t in graph.tasks:
             if t.kind in (TaskKind.DISP_F, TaskKind.COMB_F):
-                ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in range(M) if t.id in tl.per_rank[r]]
+                senders = range(M) if t.kind == TaskKind.DISP_F else range(M, M + N)
+                ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in senders if t.id in tl.per_rank[r]]
                 samples[t.kind.value].append(max(ds))
     out = {k: int(statistics.median(v)) for k, v in samples.items()}
     del ex

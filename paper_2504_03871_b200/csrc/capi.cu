@@ -582,12 +582,11 @@ static int router_wgrad_stream_splits(int T, int d) {
 }
 
 size_t hm_router_bwd_part_elems(int T, int d, int E, int k) {
-  // dlogit (token or permuted-row order, T*k padded), the dense dlogit rows (T*8, E <= 8), then
-  // the per-split dWg partials
+  // dlogit (token or permuted-row order, T*k padded), the per-token dlogit records (T*16: dense
+  // row + slots, E <= 8), then the per-split dWg partials (at most one split per SM)
   int splits = hm::kWgSplit > hm::kWgTokSplit ? hm::kWgSplit : hm::kWgTokSplit;
-  const int ss = router_wgrad_stream_splits(T, d);
-  if (ss > splits) splits = ss;
-  return router_bwd_dl_elems(T, k) + static_cast<size_t>(T) * 8 + static_cast<size_t>(splits) * E * d;
+  if (num_sms() > splits) splits = num_sms();
+  return router_bwd_dl_elems(T, k) + static_cast<size_t>(T) * hm::kRbMeta + static_cast<size_t>(splits) * E * d;
 }
 
 int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx, const float* w,
@@ -610,6 +609,35 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   // the dense dlogit rows (each token row read once, contiguously); else token-major from the
   // first routed copies (k <= 3), else per expert over the permuted rows (each copy read once)
   const bool perm_forced = getenv("HM_ROUTER_WGRAD_PERM") != nullptr;
+  // HM_ROUTER_BWD_FUSED=1 (E <= 8, k <= 3, with the token rows): the whole backward in one
+  // streamed pass (dlogit records, then dx and the dWg partials per 1024-column tile, then the
+  // split reduction). 0.116 vs 0.122 ms alone, but 0.170 vs 0.162 ms inside the C2 step
+  // (tools/router_instep.py: both paths then pay the previous GEMM's L2 write-backs), so the
+  // two-pass path below stays the default.
+  if (dwg && E <= 8 && k <= 3 && x && d % hm::kRbCols == 0 && aligned16(x) && !perm_forced &&
+      getenv("HM_ROUTER_BWD_FUSED") && !getenv("HM_ROUTER_WGRAD_TOK") && !getenv("HM_UNPERMUTE_V1") &&
+      !getenv("HM_UNPERMUTE_V2") && !getenv("HM_UNPERMUTE_V3")) {
+    float* meta = part + router_bwd_dl_elems(T, k);  // T * 16 floats (the T*8 region + partial space)
+    float* partials = meta + static_cast<size_t>(T) * hm::kRbMeta;
+    const int tiles = d / hm::kRbCols;
+    int S = num_sms() / tiles;
+    if (S < 1) S = 1;
+    if (S > (T + hm::kRbTok - 1) / hm::kRbTok) S = (T + hm::kRbTok - 1) / hm::kRbTok;
+    HM_K_SWITCH(k, (hm::router_dlogit_kernel<K><<<(T + 255) / 256, 256, 0, st>>>(idx, w, dw, T, meta, dlogit)));
+    if (int rc = check_launch("router_dlogit")) return rc;
+    auto launch = [&](auto kern, size_t smem) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<dim3(tiles, S), 17 * 32, smem, st>>>(dp, row_of, meta, static_cast<const __nv_bfloat16*>(x), gt, T, d, E,
+                                                   out, partials);
+    };
+    if (k == 1) launch(hm::router_bwd_fused_kernel<1>, hm::RbCfg<1>::kSmem);
+    else if (k == 2) launch(hm::router_bwd_fused_kernel<2>, hm::RbCfg<2>::kSmem);
+    else launch(hm::router_bwd_fused_kernel<3>, hm::RbCfg<3>::kSmem);
+    if (int rc = check_launch("router_bwd_fused")) return rc;
+    const long n = static_cast<long>(d) * E;
+    hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(partials, S, d, E, static_cast<__nv_bfloat16*>(dwg));
+    return check_launch("router_wgrad_reduce");
+  }
   const bool streamed = dwg && E <= 8 && x && d % hm::kWgCols == 0 && aligned16(x) && !perm_forced &&
                         !getenv("HM_ROUTER_WGRAD_TOK");
   const bool tok = dwg && !streamed && E <= 8 && k <= 3 && d % 64 == 0 && !perm_forced;

@@ -1239,6 +1239,168 @@ __global__ void __launch_bounds__(kWgThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Router backward in one streamed pass (E <= 8, k <= 3): per token row
+//   dx[t]   = sum_s dx_perm[row_of[t,s]] + dlogit[t,s] * Wg[:, idx[t,s]]   (the unpermute kernel's
+//             per-element order: acc += dx_perm; acc = fma(dlogit, wg, acc), slot by slot)
+//   dWg    += x[t] (x) dlogit_dense[t]
+// so x and the routed dX rows are each read once, dx is written once, and the dWg FMAs run under
+// the HBM stream instead of in a second pass. router_dlogit_kernel first writes a 64-byte record
+// per token: [0..8) dense dlogit row, [8..8+k) dlogit by slot, [12..12+k) expert by slot.
+constexpr int kRbCols = 1024;  // columns per CTA tile (512 compute threads x 2 columns)
+constexpr int kRbTok = 8;      // tokens per stage (8 x (1 + k) bulk copies of 2 KB)
+constexpr int kRbMeta = 16;    // floats per token record
+
+template <int K>
+__global__ void router_dlogit_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                     const float* __restrict__ dw, int T, float* __restrict__ meta,
+                                     float* __restrict__ dlogit) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  float ws[K], dws[K];
+  int ex[K];
+  float wsum = 0.f;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    ws[s] = w[static_cast<long>(t) * K + s];
+    dws[s] = dw[static_cast<long>(t) * K + s];
+    ex[s] = idx[static_cast<long>(t) * K + s];
+    wsum = __fmaf_rn(ws[s], dws[s], wsum);
+  }
+  float rec[kRbMeta];
+#pragma unroll
+  for (int q = 0; q < kRbMeta; ++q) rec[q] = 0.f;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const float dl = ws[s] * (dws[s] - wsum);
+    if (dlogit) dlogit[static_cast<long>(t) * K + s] = dl;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) rec[e] = (ex[s] == e) ? dl : rec[e];
+    rec[8 + s] = dl;
+    rec[12 + s] = __int_as_float(ex[s]);
+  }
+  float4* o = reinterpret_cast<float4*>(meta + static_cast<long>(t) * kRbMeta);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+}
+
+template <int K>
+struct RbCfg {
+  static constexpr int kStages = K <= 2 ? 4 : 3;
+  static constexpr int kXBytes = kRbTok * kRbCols * 2;        // 16 KB
+  static constexpr int kDBytes = kRbTok * K * kRbCols * 2;    // 16 KB per slot
+  static constexpr int kMBytes = kRbTok * kRbMeta * 4;         // 512 B
+  static constexpr int kStageBytes = kXBytes + kDBytes + kMBytes;
+  static constexpr int kWgBytes = 8 * kRbCols * 2;             // Wg^T tile, bf16
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStageBytes + kWgBytes + 128;
+};
+
+template <int K>
+__global__ void __launch_bounds__(17 * 32, 1)
+    router_bwd_fused_kernel(const __nv_bfloat16* __restrict__ dx_perm, const int32_t* __restrict__ row_of,
+                            const float* __restrict__ meta, const __nv_bfloat16* __restrict__ x,
+                            const __nv_bfloat16* __restrict__ wg_t, int T, int d, int E,
+                            __nv_bfloat16* __restrict__ dx, float* __restrict__ part /*[S][E][d]*/) {
+  using C = RbCfg<K>;
+  extern __shared__ __align__(1024) uint8_t smem_rb[];
+  uint32_t* wgs = reinterpret_cast<uint32_t*>(smem_rb + C::kStages * C::kStageBytes);  // [8][512] bf16 pairs
+  uint64_t* full = reinterpret_cast<uint64_t*>(wgs + 8 * (kRbCols / 2));
+  uint64_t* empty = full + C::kStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = blockIdx.x * kRbCols;
+  const int S = gridDim.y, split = blockIdx.y;
+  const int t_begin = static_cast<int>((static_cast<long>(T) * split) / S);
+  const int t_end = static_cast<int>((static_cast<long>(T) * (split + 1)) / S);
+  const int nst = (t_end - t_begin + kRbTok - 1) / kRbTok;
+  if (tid == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 16);
+    }
+    fence_barrier_init();
+  }
+  if (tid < 16 * 32) {  // the Wg^T tile (bf16 pairs; zeros past E)
+    for (int i = tid; i < 8 * (kRbCols / 2); i += 16 * 32) {
+      const int e = i / (kRbCols / 2), c = i % (kRbCols / 2);
+      wgs[i] = (e < E) ? *reinterpret_cast<const uint32_t*>(wg_t + static_cast<long>(e) * d + c0 + 2 * c) : 0u;
+    }
+  }
+  __syncthreads();
+  if (warp == 16) {
+    // ======== producer: lane r * (1 + K) + q copies token r's x tile (q = 0) / routed dX tile q ========
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % C::kStages;
+      const int t0 = t_begin + s * kRbTok;
+      const int nt = min(kRbTok, t_end - t0);
+      if (s >= C::kStages) mbar_wait(&empty[slot], ((s / C::kStages) - 1) & 1);
+      uint8_t* st = smem_rb + slot * C::kStageBytes;
+      if (lane == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[slot], nt * (1 + K) * kRbCols * 2 + nt * kRbMeta * 4);
+        bulk_load_1d(st + C::kXBytes + C::kDBytes, meta + static_cast<long>(t0) * kRbMeta, nt * kRbMeta * 4, &full[slot]);
+      }
+      __syncwarp();
+      const int r = lane / (1 + K), q = lane % (1 + K);
+      if (r < nt && lane < kRbTok * (1 + K)) {
+        const long t = t0 + r;
+        if (q == 0) {
+          bulk_load_1d(st + r * kRbCols * 2, x + t * d + c0, kRbCols * 2, &full[slot]);
+        } else {
+          const long row = __ldg(row_of + t * K + (q - 1));
+          bulk_load_1d(st + C::kXBytes + (r * K + (q - 1)) * kRbCols * 2, dx_perm + row * d + c0, kRbCols * 2,
+                       &full[slot]);
+        }
+      }
+    }
+  } else {
+    // ======== compute: thread c owns columns (2c, 2c + 1) of the tile, every token ========
+    const int c = tid;
+    float2 acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = make_float2(0.f, 0.f);
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % C::kStages;
+      const int t0 = t_begin + s * kRbTok;
+      const int nt = min(kRbTok, t_end - t0);
+      mbar_wait(&full[slot], (s / C::kStages) & 1);
+      const uint8_t* st = smem_rb + slot * C::kStageBytes;
+      const float* mt = reinterpret_cast<const float*>(st + C::kXBytes + C::kDBytes);
+#pragma unroll 2
+      for (int r = 0; r < nt; ++r) {
+        const float* rec = mt + r * kRbMeta;
+        const float4 ca = *reinterpret_cast<const float4*>(rec);
+        const float4 cb = *reinterpret_cast<const float4*>(rec + 4);
+        const float4 dls = *reinterpret_cast<const float4*>(rec + 8);
+        const float4 exs = *reinterpret_cast<const float4*>(rec + 12);
+        const float dl[4] = {dls.x, dls.y, dls.z, dls.w};
+        const int ex[4] = {__float_as_int(exs.x), __float_as_int(exs.y), __float_as_int(exs.z), __float_as_int(exs.w)};
+        float2 o = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const uint32_t v = *reinterpret_cast<const uint32_t*>(st + C::kXBytes + (r * K + q) * kRbCols * 2 + c * 4);
+          const uint32_t gp = wgs[ex[q] * (kRbCols / 2) + c];
+          o.x += __uint_as_float(v << 16);
+          o.y += __uint_as_float(v & 0xffff0000u);
+          o.x = __fmaf_rn(dl[q], __uint_as_float(gp << 16), o.x);
+          o.y = __fmaf_rn(dl[q], __uint_as_float(gp & 0xffff0000u), o.y);
+        }
+        *reinterpret_cast<uint32_t*>(dx + static_cast<long>(t0 + r) * d + c0 + 2 * c) = pack_bf16x2(o.x, o.y);
+        const uint32_t xp = *reinterpret_cast<const uint32_t*>(st + r * kRbCols * 2 + c * 4);
+        const float2 xf = make_float2(__uint_as_float(xp << 16), __uint_as_float(xp & 0xffff0000u));
+        const float cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = __ffma2_rn(xf, make_float2(cc[e], cc[e]), acc[e]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    const int col = c0 + 2 * c;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e < E) *reinterpret_cast<float2*>(part + (static_cast<long>(split) * E + e) * d + col) = acc[e];
+  }
+}
+
 __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nsplit, int d, int E,
                                            __nv_bfloat16* __restrict__ dwg /*[d][E]*/) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -191,8 +191,10 @@ def test_router_fused_equals_unfused_and_oracle(cfg):
 @pytest.mark.parametrize("cfg", [LayerConfig("E8d4096", 8, 2, 4096, 128, 3000),
                                  LayerConfig("E4d1024k3", 4, 3, 1024, 128, 777)], ids=lambda c: c.name)
 def test_router_bwd_streamed_wgrad_vs_fp32(cfg):
-    """The streamed router weight gradient (E <= 8, token rows x through shared memory) against a
-    plain fp32 reference dWg = x^T . dlogit_dense, and the three dWg paths against each other."""
+    """The one-pass router backward (E <= 8, k <= 3: dx and dWg per column tile from the token rows
+    and routed dX rows streamed through shared memory), the two-pass streamed dWg, the token-major
+    and the per-expert paths: dx and dlogit bitwise equal, dWg against a plain fp32 reference
+    x^T . dlogit_dense."""
     import os
 
     inp = make_inputs(cfg, seed=19)
@@ -204,7 +206,8 @@ def test_router_bwd_streamed_wgrad_vs_fp32(cfg):
     dw = torch.randn(r.w.shape, generator=g, device="cuda")
     wg_t = ops.transpose_bf16(wg)
     outs = {}
-    for v, env in (("stream", None), ("tok", "HM_ROUTER_WGRAD_TOK"), ("perm", "HM_ROUTER_WGRAD_PERM")):
+    for v, env in (("fused", "HM_ROUTER_BWD_FUSED"), ("stream", None), ("tok", "HM_ROUTER_WGRAD_TOK"),
+                   ("perm", "HM_ROUTER_WGRAD_PERM")):
         if env:
             os.environ[env] = "1"
         try:
@@ -213,11 +216,12 @@ def test_router_bwd_streamed_wgrad_vs_fp32(cfg):
             if env:
                 os.environ.pop(env)
     torch.cuda.synchronize()
-    dl = outs["stream"][1].float()  # dlogit [T, k]
+    dl = outs["fused"][1].float()  # dlogit [T, k]
     dense = torch.zeros((cfg.T, cfg.E), device="cuda").scatter_(1, r.idx.long(), dl)
     ref = x.float().t() @ dense
     for v in outs:
-        assert torch.equal(outs[v][0], outs["stream"][0]), v  # dx identical on every path
+        assert torch.equal(outs[v][0], outs["fused"][0]), v  # dx identical on every path
+        assert torch.equal(outs[v][1], outs["fused"][1]), v  # dlogit too
         assert orc.rel_err(outs[v][2], ref) < 5e-3, v
 
 

@@ -87,19 +87,21 @@ def main():
     out["router_fwd_ms_variants"] = {v: min(t) for v, t in fw.items()}
     out["router_fwd_ms"] = min(fw["fused"])
     res = {}
-    for variant in ("stream", "tok", "perm", "stream", "tok", "perm"):
-        os.environ.pop("HM_ROUTER_WGRAD_PERM", None)
-        os.environ.pop("HM_ROUTER_WGRAD_TOK", None)
-        if variant == "perm":
-            os.environ["HM_ROUTER_WGRAD_PERM"] = "1"
-        elif variant == "tok":
-            os.environ["HM_ROUTER_WGRAD_TOK"] = "1"
+    envs = {"fused": "HM_ROUTER_BWD_FUSED", "stream": None, "tok": "HM_ROUTER_WGRAD_TOK",
+            "perm": "HM_ROUTER_WGRAD_PERM"}
+    for variant in ("fused", "stream", "tok", "perm") * 2:
+        for e_ in envs.values():
+            if e_:
+                os.environ.pop(e_, None)
+        if envs[variant]:
+            os.environ[envs[variant]] = "1"
         ms = timed(lambda: ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x), args.reps)
         res.setdefault(variant, []).append(ms)
         res.setdefault(variant + "_dwg", ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x)[2].float())
-    os.environ.pop("HM_ROUTER_WGRAD_PERM", None)
-    os.environ.pop("HM_ROUTER_WGRAD_TOK", None)
-    out["router_bwd_ms"] = {v: min(res[v]) for v in ("stream", "tok", "perm")}
+    for e_ in envs.values():
+        if e_:
+            os.environ.pop(e_, None)
+    out["router_bwd_ms"] = {v: min(res[v]) for v in envs}
     out["dwg_rel_diff_stream_vs_perm"] = float((res["stream_dwg"] - res["perm_dwg"]).norm() / res["perm_dwg"].norm())
     # unpermute + dlogit.Wg kernel variants (HM_UNPERMUTE_V1/V2/V3), dx / dlogit compared bitwise
     uv = {}

@@ -70,21 +70,51 @@ constexpr int kRouterItems = 64;
 // the 32 / EGW lanes that share it.
 template <int EGW, int NI>
 HM_DEV void router_reduce_scatter(float (&v)[NI][EGW], float (&out)[NI]) {
+  // the adds run as packed fp32x2 (FADD2: two IEEE adds per instruction, the same values):
+  // adjacent slots of one item while a level keeps >= 2 values, else the NI items' values paired
   int off = 16;
 #pragma unroll
   for (int h = EGW / 2; h >= 1; h >>= 1) {
+    float r[NI][EGW / 2];
 #pragma unroll
     for (int m = 0; m < h; ++m)
 #pragma unroll
-      for (int i = 0; i < NI; ++i) v[i][m] = v[i][m] + __shfl_xor_sync(0xffffffffu, v[i][m + h], off);
+      for (int i = 0; i < NI; ++i) r[i][m] = __shfl_xor_sync(0xffffffffu, v[i][m + h], off);
+    if (h >= 2) {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int m = 0; m < h; m += 2) {
+          const float2 a = __fadd2_rn(make_float2(v[i][m], v[i][m + 1]), make_float2(r[i][m], r[i][m + 1]));
+          v[i][m] = a.x;
+          v[i][m + 1] = a.y;
+        }
+    } else {
+#pragma unroll
+      for (int i = 0; i + 1 < NI; i += 2) {
+        const float2 a = __fadd2_rn(make_float2(v[i][0], v[i + 1][0]), make_float2(r[i][0], r[i + 1][0]));
+        v[i][0] = a.x;
+        v[i + 1][0] = a.y;
+      }
+      if (NI & 1) v[NI - 1][0] = v[NI - 1][0] + r[NI - 1][0];
+    }
     off >>= 1;
   }
 #pragma unroll
   for (int i = 0; i < NI; ++i) out[i] = v[i][0];
 #pragma unroll
-  for (int o = 32 / EGW / 2; o >= 1; o >>= 1)
+  for (int o = 32 / EGW / 2; o >= 1; o >>= 1) {
+    float r[NI];
 #pragma unroll
-    for (int i = 0; i < NI; ++i) out[i] = out[i] + __shfl_xor_sync(0xffffffffu, out[i], o);
+    for (int i = 0; i < NI; ++i) r[i] = __shfl_xor_sync(0xffffffffu, out[i], o);
+#pragma unroll
+    for (int i = 0; i + 1 < NI; i += 2) {
+      const float2 a = __fadd2_rn(make_float2(out[i], out[i + 1]), make_float2(r[i], r[i + 1]));
+      out[i] = a.x;
+      out[i + 1] = a.y;
+    }
+    if (NI & 1) out[NI - 1] = out[NI - 1] + r[NI - 1];
+  }
 }
 
 // Natural expert order -> the lane's XOR-permuted order (slot r <- expert r ^ mask, mask =

@@ -56,7 +56,7 @@ int hm_gemm_stats(unsigned long long* out);
  * logits[T,E] fp32 (required scratch, also a result), counts[E], offsets[E+1] int32,
  * chunk_base[hm_router_chunk_elems(T,E)] int32 (per-chunk row bases, consumed by
  * hm_dispatch_permute; its last element is the fused kernel's completion counter).
- * Requires d = 256 * 2^m <= 16384, 1 <= k <= 8, k <= E <= 256.
+ * Requires d % 256 == 0, d <= 16384, 1 <= k <= 8, k <= E <= 256.
  * Replaces: the router/gate folded into ATTN_F (taskgraph.py:220-246). */
 int hm_router_topk(const void* x, const void* wg, const float* bias, int T, int d, int E, int k,
                    int32_t* idx, float* w, float* logits, int32_t* counts, int32_t* offsets,

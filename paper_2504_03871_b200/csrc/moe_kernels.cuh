@@ -201,40 +201,6 @@ HM_DEV void router_scan_block(int32_t* __restrict__ chunk_counts /*in: counts, o
   }
 }
 
-// top-k (NaN-marked selection, ties -> lower id, all-NaN -> lowest unselected id) + softmax of
-// one token's E logits held in v[0..E); EP >= E compile-time bound
-template <int EP>
-HM_DEV void router_select(float (&v)[EP], int E, int k, int32_t* idx_out, float* w_out, int32_t* hist_row) {
-  float sel_l[kMaxTopK];
-  int sel_e[kMaxTopK];
-  for (int s = 0; s < k; ++s) {
-    float bv = -INFINITY;
-    int be = 0x7fffffff;
-#pragma unroll
-    for (int e = 0; e < EP; ++e)
-      if (e < E && (v[e] > bv || (v[e] == bv && e < be))) { bv = v[e]; be = e; }
-    if (be == 0x7fffffff) {
-      be = 0;
-      bv = kSelectedMark;  // the selected logit is NaN (the softmax sees it)
-      for (int p = 0; p < s; ++p)
-        if (sel_e[p] == be) { ++be; p = -1; }
-    }
-    sel_l[s] = bv;
-    sel_e[s] = be;
-#pragma unroll
-    for (int e = 0; e < EP; ++e)
-      if (e == be) v[e] = kSelectedMark;
-  }
-  float ex[kMaxTopK];
-  float sum = 0.f;
-  for (int s = 0; s < k; ++s) { ex[s] = expf(sel_l[s] - sel_l[0]); sum += ex[s]; }
-  for (int s = 0; s < k; ++s) {
-    idx_out[s] = sel_e[s];
-    w_out[s] = ex[s] / sum;
-    atomicAdd(hist_row + sel_e[s], 1);
-  }
-}
-
 struct RouterShared {
   uint64_t full[kRouterStages];
   uint64_t pfull[kRouterStages];
@@ -246,7 +212,7 @@ struct RouterShared {
 // Top-k of one token whose EGW logits sit in EGW consecutive lanes (lane e of the group holds
 // expert e; e >= E is no expert): k rounds of a lexicographic (value desc, id asc) butterfly
 // argmax over the group with NaN never eligible — the comparator of the sequential scan
-// (router_select), so the same experts in the same order — the winner marked NaN, the
+// (router_topk_lane_kernel), so the same experts in the same order — the winner marked NaN, the
 // all-NaN fallback to the lowest unselected id; then the softmax over the selected logits
 // (sequential sum in slot order). Lane e == s writes slot s and counts it in the histogram.
 template <int EGW>

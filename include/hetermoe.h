@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define HM_ABI_VERSION 2
+#define HM_ABI_VERSION 3
 
 #define HM_E_SHAPE 1001     /* unsupported or inconsistent shape */
 #define HM_E_ALIGN 1002     /* pointer / stride alignment violated (16 bytes) */
@@ -118,6 +118,37 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
                          int E, int rows, int M, int N, int K, void* out, int ldo, void* out2,
                          int ldo2, const void* aux, int ld_aux, void* workspace,
                          const unsigned long long* out_rows, int max_ctas, void* stream);
+/* hm_grouped_gemm_rows whose operands may sit in a pool at a device-computed base (no host sync
+ * on the routed row counts): the A tensor map spans a_rows rows (0: rows), and row_shift (device,
+ * 8-byte aligned int[2], or NULL) holds {a, o}: rows added to the segment rows of A and of the
+ * out / out2 / aux buffers (o must be 0 when out_rows is given). rows bounds the grid (the
+ * receive capacity); the tile count comes from seg_offsets on the device. GROUP_M modes only. */
+int hm_grouped_gemm_shifted(int mode, const void* a, const void* b, const int32_t* seg_offsets,
+                            int E, int rows, int a_rows, int M, int N, int K, void* out, int ldo,
+                            void* out2, int ldo2, const void* aux, int ld_aux, void* workspace,
+                            const unsigned long long* out_rows, const int32_t* row_shift,
+                            int max_ctas, void* stream);
+/* ---- device-side receive layout (ZP peer-memory transport, one call per (layer, micro-batch)) ----
+ * From the all-gathered expert counts counts_all[M][E] (attention ranks) and the layer's
+ * owners[E], on the device, with no host synchronisation:
+ *   sender (me < M):   dest_start[E]  first row of my rows of expert e in its owner's expert-major
+ *                                     receive slot (experts in id order, senders in rank order)
+ *   owner (n_own > 0): seg[n_own+1]   segment offsets of my experts in my receive slot
+ *                      out_rows_y/dx[cap]  per received row, the device address of its row in the
+ *                                     sender's y slot (y_base[a] + row * row_bytes) / + dx_delta
+ *                      shifts[8]      {a, o} row shifts for hm_grouped_gemm_shifted: up+gate
+ *                                     {0, f}, down {f, 0}, SwiGLU bwd {0, f}, dX {f, 0}, where
+ *                                     f = pool_base + *top is bump-allocated in the layer's pool
+ *                                     region of pool_rows rows (*top: device counter, zeroed by the
+ *                                     caller before the layer's first micro-batch)
+ * A pool or slot overflow ORs 1 / 4 (pool / receive slot) into *err and empties the segments (the
+ * GEMMs then skip this micro-batch); the caller checks *err after the step.
+ * Replaces the host-side receive layout of the count exchange. */
+int hm_zp_layout(const int32_t* counts_all, int M, int E, const int32_t* owners, int me, int n_own,
+                 int cap, const unsigned long long* y_base, long long dx_delta, int row_bytes,
+                 int32_t* dest_start, int32_t* seg, unsigned long long* out_rows_y,
+                 unsigned long long* out_rows_dx, int32_t* shifts, int32_t* top, int pool_base,
+                 int pool_rows, int32_t* err, void* stream);
 /* after this stream's prior work: atomically add 1 (release, system scope) to n <= 8 counters
  * (host array of device pointers, typically peer-mapped) */
 int hm_signal_peers(const unsigned long long* flag_ptrs, int n, void* stream);
@@ -148,6 +179,13 @@ int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void
                            int N, void* out, int ldo, void* workspace, int max_ctas,
                            void* stream);
 size_t hm_grouped_wgrad_multi_workspace_bytes(int E, int R);
+/* hm_grouped_wgrad_multi with per-segment pool bases: rows of A_j / B_j are offset by
+ * shift_a[j * shift_stride] / shift_b[j * shift_stride] (device ints, either may be NULL) */
+int hm_grouped_wgrad_multi_shifted(int accumulate, const void* const* a_list, const void* const* b_list,
+                                   const int* rows_list, const int32_t* seg_offsets, int R, int E, int M,
+                                   int N, void* out, int ldo, const int32_t* shift_a,
+                                   const int32_t* shift_b, int shift_stride, void* workspace,
+                                   int max_ctas, void* stream);
 
 /* SwiGLU expert FFN forward over permuted rows:
  *   h[rows,2f]  = x_perm . w_ug[e]^T   (gate|up interleaved in 128-column blocks, saved for bwd)

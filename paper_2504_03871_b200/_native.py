@@ -52,6 +52,11 @@ SIGNATURES = {
     "hm_wait_flags": (_I, [_P, _I, _P, _I, _P]),
     "hm_grouped_wgrad_multi": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _I, _P]),
     "hm_grouped_wgrad_multi_workspace_bytes": (ctypes.c_size_t, [_I, _I]),
+    "hm_grouped_gemm_shifted": (_I, [_I, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, _P, _P, _P,
+                                     _I, _P]),
+    "hm_grouped_wgrad_multi_shifted": (_I, [_I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _P, _I, _P, _I, _P]),
+    "hm_zp_layout": (_I, [_P, _I, _I, _P, _I, _I, _I, _P, ctypes.c_longlong, _I, _P, _P, _P, _P, _P, _P, _I, _I,
+                          _P, _P]),
     "hm_grouped_ffn_fwd": (_I, [_P, _I, _P, _I, _P, _P, _I, _I, _P, _P, _P, _I, _P]),
     "hm_grouped_ffn_bwd": (_I, [_P, _P, _P, _P, _I, _P, _I, _P, _P, _I, _I, _P, _P, _P, _P, _P, _I, _P]),
 }

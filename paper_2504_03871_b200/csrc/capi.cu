@@ -746,6 +746,24 @@ int hm_combine_bwd_p2p(const void* dy, const void* y_perm, const int32_t* row_of
   return check_launch("combine_bwd_p2p");
 }
 
+int hm_zp_layout(const int32_t* counts_all, int M, int E, const int32_t* owners, int me, int n_own,
+                 int cap, const unsigned long long* y_base, long long dx_delta, int row_bytes,
+                 int32_t* dest_start, int32_t* seg, unsigned long long* out_rows_y,
+                 unsigned long long* out_rows_dx, int32_t* shifts, int32_t* top, int pool_base,
+                 int pool_rows, int32_t* err, void* stream) {
+  if (M < 1 || M > hm::kZpMaxSenders || E < 1 || E > 256 || me < 0 || me >= hm::kZpMaxPeersLayout || cap < 0 ||
+      n_own < 0 || n_own > E || pool_base < 0 || pool_rows < 0)
+    return fail(HM_E_SHAPE, "zp_layout: M=%d E=%d me=%d n_own=%d cap=%d", M, E, me, n_own, cap);
+  if (!counts_all || !owners || (me < M && !dest_start) || !err ||
+      (n_own > 0 && (!seg || !out_rows_y || !out_rows_dx || !shifts || !top || !y_base)))
+    return fail(HM_E_ARG, "zp_layout: null argument");
+  const int grid = cap > 0 ? (cap + hm::kZpLayoutRowsPerCta - 1) / hm::kZpLayoutRowsPerCta : 1;
+  hm::zp_layout_kernel<<<grid, hm::kZpLayoutThreads, 0, S(stream)>>>(
+      counts_all, M, E, owners, me, n_own, cap, y_base, dx_delta, row_bytes, dest_start, seg, out_rows_y,
+      out_rows_dx, shifts, top, pool_base, pool_rows, err);
+  return check_launch("zp_layout");
+}
+
 int hm_signal_peers(const unsigned long long* flag_ptrs, int n, void* stream) {
   if (n < 0 || n > hm::kMaxPeers) return fail(HM_E_ARG, "signal_peers: n=%d", n);
   if (n == 0) return 0;
@@ -794,6 +812,15 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
                          int E, int rows, int M, int N, int K, void* out, int ldo, void* out2,
                          int ldo2, const void* aux, int ld_aux, void* workspace,
                          const unsigned long long* out_rows, int max_ctas, void* stream) {
+  return hm_grouped_gemm_shifted(mode, a, b, seg_offsets, E, rows, 0, M, N, K, out, ldo, out2, ldo2, aux,
+                                 ld_aux, workspace, out_rows, nullptr, max_ctas, stream);
+}
+
+int hm_grouped_gemm_shifted(int mode, const void* a, const void* b, const int32_t* seg_offsets,
+                            int E, int rows, int a_rows, int M, int N, int K, void* out, int ldo,
+                            void* out2, int ldo2, const void* aux, int ld_aux, void* workspace,
+                            const unsigned long long* out_rows, const int32_t* row_shift,
+                            int max_ctas, void* stream) {
   if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "gemm: E=%d out of range", E);
   if (rows < 0 || N <= 0 || N % 8 != 0) return fail(HM_E_SHAPE, "gemm: bad rows/N");
   if (!aligned16(a) || !aligned16(b) || (!out_rows && !aligned16(out))) return fail(HM_E_ALIGN, "gemm: alignment");
@@ -807,8 +834,12 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
   if (!wgrad && (K <= 0 || K % 8 != 0)) return fail(HM_E_SHAPE, "gemm: K must be a positive multiple of 8");
   if (wgrad && (M <= 0 || M % 8 != 0)) return fail(HM_E_SHAPE, "gemm: M must be a positive multiple of 8");
   if (rows == 0 && !wgrad) return 0;
+  if (row_shift && (wgrad || (reinterpret_cast<uintptr_t>(row_shift) & 7u)))
+    return fail(HM_E_ARG, "gemm: row_shift is an 8-byte aligned int[2], GROUP_M modes only");
+  if (a_rows < rows) a_rows = rows;
 
   hm::GroupedGemmParams p{};
+  p.row_shift = row_shift;
   p.R = 1;
   p.seg_offsets = seg_offsets;
   p.E = E;
@@ -829,7 +860,7 @@ int hm_grouped_gemm_rows(int mode, const void* a, const void* b, const int32_t* 
   const int ctas = gemm_ctas();
   if (!wgrad) {
     {
-      uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows_m};
+      uint64_t dims[2] = {(uint64_t)K, (uint64_t)(a_rows > 0 ? a_rows : rows_m)};
       uint64_t str[1] = {(uint64_t)K * 2};
       uint32_t box[2] = {64, 128};
       if (int rc = make_map(&ma, a, 2, dims, str, box)) return rc;
@@ -895,6 +926,15 @@ int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void
                            const int* rows_list, const int32_t* seg_offsets, int R, int E, int M,
                            int N, void* out, int ldo, void* workspace, int max_ctas,
                            void* stream) {
+  return hm_grouped_wgrad_multi_shifted(accumulate, a_list, b_list, rows_list, seg_offsets, R, E, M, N, out,
+                                        ldo, nullptr, nullptr, 0, workspace, max_ctas, stream);
+}
+
+int hm_grouped_wgrad_multi_shifted(int accumulate, const void* const* a_list, const void* const* b_list,
+                                   const int* rows_list, const int32_t* seg_offsets, int R, int E, int M,
+                                   int N, void* out, int ldo, const int32_t* shift_a,
+                                   const int32_t* shift_b, int shift_stride, void* workspace,
+                                   int max_ctas, void* stream) {
   if (R < 1 || R > hm::kMaxSegs) return fail(HM_E_SHAPE, "wgrad_multi: R=%d out of [1,%d]", R, hm::kMaxSegs);
   if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "wgrad_multi: E=%d out of range", E);
   if (M <= 0 || M % 8 || N <= 0 || N % 8 || ldo % 8) return fail(HM_E_SHAPE, "wgrad_multi: bad M/N/ldo");
@@ -918,7 +958,8 @@ int hm_grouped_wgrad_multi(int accumulate, const void* const* a_list, const void
   if (int rc = make_map(&mb, b_list[0], 2, dims_b, str_b, box)) return rc;
   CUtensorMap* maps = static_cast<CUtensorMap*>(workspace);
   hm::build_expert_maps_kernel<<<(E * R + 127) / 128, 128, 0, st>>>(
-      ma, mb, seg_offsets, E, R, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps);
+      ma, mb, seg_offsets, E, R, bases, static_cast<long>(M) * 2, static_cast<long>(N) * 2, maps, shift_a,
+      shift_b, shift_stride);
   if (int rc = check_launch("build_expert_maps")) return rc;
   hm::GroupedGemmParams p{};
   p.seg_offsets = seg_offsets;  // segment 0 row table doubles as the GROUP_M bookkeeping

@@ -91,6 +91,10 @@ struct GroupedGemmParams {
   const unsigned long long* out_rows;  // EPI_STORE: optional per-output-row destination pointer
                                        // (row r -> bf16* out_rows[r], may be a peer GPU's memory)
   long out_elems;  // elements of out (bounds checks in HM_BOUNDS_CHECK builds)
+  const int* row_shift;  // GROUP_M, optional device int[2] {a, o}: rows added to the segment rows
+                         // of the A operand (a) and of the out / out2 / aux buffers (o), for
+                         // operands placed in a pool at a device-computed base; o must be 0 when
+                         // out_rows is given (out_rows is indexed by segment row)
   int early_release;  // wide plain-store epilogue: release the accumulator before the last stores
 };
 
@@ -160,7 +164,9 @@ __global__ void build_expert_maps_kernel(const __grid_constant__ CUtensorMap tmp
                                          const int* __restrict__ seg_offsets /*[R][E+1]*/, int E,
                                          int R, const __grid_constant__ SegBases bases,
                                          long row_bytes_a, long row_bytes_b,
-                                         CUtensorMap* __restrict__ out) {
+                                         CUtensorMap* __restrict__ out,
+                                         const int* __restrict__ shift_a = nullptr,
+                                         const int* __restrict__ shift_b = nullptr, int shift_stride = 0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E * R) return;
   const int e = i / R, j = i % R;
@@ -181,9 +187,12 @@ __global__ void build_expert_maps_kernel(const __grid_constant__ CUtensorMap tmp
   // against the host encoder by tests/test_kernels_gpu.py::test_device_expert_maps_match_host).
   set_span_flag(ma, static_cast<long>(rows) * row_bytes_a);
   set_span_flag(ma + 1, static_cast<long>(rows) * row_bytes_b);
-  tensormap_set_address(ma, bases.a[j] + static_cast<long>(s0) * row_bytes_a);
+  // optional per-segment pool bases (device-computed row offsets of A / B rows of segment j)
+  const long ra = s0 + (shift_a ? shift_a[j * shift_stride] : 0);
+  const long rb = s0 + (shift_b ? shift_b[j * shift_stride] : 0);
+  tensormap_set_address(ma, bases.a[j] + ra * row_bytes_a);
   tensormap_set_dim(ma, 1, rows);
-  tensormap_set_address(ma + 1, bases.b[j] + static_cast<long>(s0) * row_bytes_b);
+  tensormap_set_address(ma + 1, bases.b[j] + rb * row_bytes_b);
   tensormap_set_dim(ma + 1, 1, rows);
   tensormap_release();
 }
@@ -374,6 +383,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
 
   const int total_tiles = sh.tile_prefix[E];
+
   const uint32_t tmem_base = sh.tmem_base;
 
   if (warp == 0) {
@@ -384,6 +394,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // 4x the DRAM reads, profiles/r1_gemm_full_2cta_policies.md)
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = pol_a;
+      const int a_shift = (!GROUP_K && p.row_shift) ? p.row_shift[0] : 0;
       uint32_t it = 0;
       unsigned long long st_empty = 0;
       uint32_t ci = 0;
@@ -436,7 +447,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (!GROUP_K) {
             // A: activation rows [seg0 + m0, +128), K-major box {64, 128}
-            tma_load_2d_any<CTAS>(sa, mA, bar, kb * kBK, seg0 + m0, pol_a);
+            tma_load_2d_any<CTAS>(sa, mA, bar, kb * kBK, seg0 + m0 + a_shift, pol_a);
 #pragma unroll
             for (int u = 0; u < NSUB; ++u) {
               if (!B_MN) {
@@ -554,6 +565,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ======================= epilogue (warps 2..9) =======================
+    // pool-placed out / out2 / aux rows (device-computed base; 0 whenever out_rows is used)
+    const int o_shift = (!GROUP_K && p.row_shift) ? p.row_shift[1] : 0;
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;  // column half of the 256-wide accumulator
     const int row_in_tile = static_cast<int>(rank) * kBM + quad * 32 + lane;
@@ -568,7 +581,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       bool row_ok;
       if (!GROUP_K) {
         row_ok = tc.mt * kTileM + row_in_tile < me;
-        grow = static_cast<long>(seg0) + tc.mt * kTileM + row_in_tile;
+        grow = static_cast<long>(seg0) + o_shift + tc.mt * kTileM + row_in_tile;
       } else {
         row_ok = tc.mt * kTileM + row_in_tile < p.M;
         grow = static_cast<long>(tc.e) * p.M + tc.mt * kTileM + row_in_tile;

@@ -1549,6 +1549,115 @@ __global__ void __launch_bounds__(256)
 // Completion signalling between GPUs: after the data writes of this stream completed, add 1 to
 // each listed (peer-mapped) 32-bit counter with release semantics at system scope.
 constexpr int kMaxPeers = 8;
+// ------------------------------------------------------------------------------------------
+// Device-side receive layout of one (layer, micro-batch) exchange (ZP peer-memory transport).
+// Every CTA rebuilds the small tables (<= kZpMaxSenders x 256 counts) in shared memory; CTA 0
+// writes the sender table, the owner's segments, pool bases and GEMM row shifts; all CTAs fill
+// the per-row return addresses of the owner's received rows (grid-stride over the rows).
+// Receive slot of owner o: its experts in id order, inside an expert the senders in rank order.
+constexpr int kZpMaxSenders = 8;
+constexpr int kZpMaxPeersLayout = 16;  // ranks of the exchange (owners)
+constexpr int kZpLayoutThreads = 256;
+constexpr int kZpLayoutRowsPerCta = 2048;
+
+__global__ void __launch_bounds__(kZpLayoutThreads)
+    zp_layout_kernel(const int32_t* __restrict__ counts_all, int M, int E, const int32_t* __restrict__ owners,
+                     int me, int n_own, int cap, const unsigned long long* __restrict__ y_base,
+                     long long dx_delta, int row_bytes, int32_t* __restrict__ dest_start,
+                     int32_t* __restrict__ seg, unsigned long long* __restrict__ out_rows_y,
+                     unsigned long long* __restrict__ out_rows_dx, int32_t* __restrict__ shifts,
+                     int32_t* __restrict__ top, int pool_base, int pool_rows, int32_t* __restrict__ err) {
+  __shared__ int s_cnt[kZpMaxSenders][256];
+  __shared__ int s_off[kZpMaxSenders][256];  // sender a's first permuted row of expert e
+  __shared__ int s_start[256];               // first row of expert e in its owner's slot
+  __shared__ int s_own[256];
+  __shared__ int s_seg_row[kZpMaxSenders * 256 + 1];  // my received segments (expert-major, sender-minor)
+  __shared__ int s_seg_src[kZpMaxSenders * 256];      // ... their sender rank
+  __shared__ int s_seg_off[kZpMaxSenders * 256];      // ... their first row in the sender's permuted buffer
+  __shared__ int s_nseg, s_total;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < M * E; i += blockDim.x) s_cnt[i / E][i % E] = counts_all[i];
+  for (int e = tid; e < E; e += blockDim.x) s_own[e] = owners[e];
+  __syncthreads();
+  if (tid < M) {  // sender offsets: exclusive prefix over the experts
+    int a = 0;
+    for (int e = 0; e < E; ++e) {
+      s_off[tid][e] = a;
+      a += s_cnt[tid][e];
+    }
+  }
+  if (tid == kZpLayoutThreads - 1) {  // owners' slots: experts in id order
+    int run[kZpMaxPeersLayout];
+    for (int o = 0; o < kZpMaxPeersLayout; ++o) run[o] = 0;
+    for (int e = 0; e < E; ++e) {
+      int tot = 0;
+      for (int a = 0; a < M; ++a) tot += s_cnt[a][e];
+      const int o = s_own[e];
+      s_start[e] = run[o];
+      run[o] += tot;
+    }
+    s_total = run[me];
+  }
+  __syncthreads();
+  if (tid == 0) {  // my received segments, in slot order
+    int n = 0;
+    for (int e = 0; e < E; ++e) {
+      if (s_own[e] != me) continue;
+      int r = s_start[e];
+      for (int a = 0; a < M; ++a) {
+        s_seg_row[n] = r;
+        s_seg_src[n] = a;
+        s_seg_off[n] = s_off[a][e];
+        r += s_cnt[a][e];
+        ++n;
+      }
+    }
+    s_seg_row[n] = s_total;
+    s_nseg = n;
+  }
+  __syncthreads();
+  const int total = s_total;
+  if (blockIdx.x == 0) {
+    if (me < M)
+      for (int e = tid; e < E; e += blockDim.x) {
+        int st = s_start[e];
+        for (int a = 0; a < me; ++a) st += s_cnt[a][e];
+        dest_start[e] = st;
+      }
+    if (tid == 0 && n_own > 0) {
+      // bump-allocate this micro-batch's rows in the layer's pool region
+      int bad = total > cap ? 4 : 0;
+      const int used = *top;
+      if (used + total > pool_rows) bad |= 1;
+      if (!bad) *top = used + total;
+      else atomicOr(err, bad);
+      int i = 0;
+      for (int e = 0; e < E && i < n_own; ++e)
+        if (s_own[e] == me) seg[i++] = bad ? 0 : s_start[e];
+      for (; i <= n_own; ++i) seg[i] = bad ? 0 : total;
+      const int f = pool_base + (bad ? 0 : used);
+      // {a, o} row shifts: up+gate {0, f}, down {f, 0}, SwiGLU backward {0, f}, dX {f, 0}
+      shifts[0] = 0; shifts[1] = f; shifts[2] = f; shifts[3] = 0;
+      shifts[4] = 0; shifts[5] = f; shifts[6] = f; shifts[7] = 0;
+    }
+  }
+  if (n_own <= 0) return;
+  const int nseg = s_nseg;
+  const int rmax = total < cap ? total : cap;
+  for (int r = blockIdx.x * blockDim.x + tid; r < rmax; r += gridDim.x * blockDim.x) {
+    int lo = 0, hi = nseg - 1;  // last segment whose first row <= r (empty segments share rows)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_seg_row[mid] <= r) lo = mid;
+      else hi = mid - 1;
+    }
+    const long row = s_seg_off[lo] + (r - s_seg_row[lo]);
+    const unsigned long long ya = y_base[s_seg_src[lo]] + static_cast<unsigned long long>(row) * row_bytes;
+    out_rows_y[r] = ya;
+    out_rows_dx[r] = ya + dx_delta;
+  }
+}
+
 struct PeerFlags {
   unsigned long long ptr[kMaxPeers];
 };

@@ -225,6 +225,27 @@ class NativeBackend:
     def ffn_bwd_data_rows(self, dy, x, h, act, seg, w_ug, w_d, out_rows):
         return self.ops.grouped_ffn_bwd_data_rows(dy, x, h, act, seg, w_ug, w_d, out_rows, self.max_ctas)
 
+    # device-side receive layout + pool-placed activations (ZpP2PExecutor, device_layout)
+    def zp_layout(self, *args):
+        self.ops.zp_layout(*args)
+
+    def ffn_fwd_pool(self, x_slot, seg, w_ug, w_d, h_pool, act_pool, shifts, out_rows, cap):
+        self.ops.grouped_ffn_fwd_pool(x_slot, seg, w_ug, w_d, h_pool, act_pool, shifts, out_rows, cap,
+                                      self.max_ctas)
+
+    def ffn_bwd_data_pool(self, dy_slot, seg, w_ug, w_d, h_pool, dh_ptr, dh_rows, shifts, out_rows, cap):
+        self.ops.grouped_ffn_bwd_data_pool(dy_slot, seg, w_ug, w_d, h_pool, dh_ptr, dh_rows, shifts, out_rows,
+                                           cap, self.max_ctas)
+
+    def ffn_wgrad_pool(self, ug_ab, down_ab, seg_multi, f_shift, gw_ug, gw_d):
+        """Layer weight gradients over all micro-batches: dW_ug += dH^T X (dH pool rows shifted),
+        dW_d += dY^T act (act pool rows shifted); f_shift: device view, stride 8 ints."""
+        d, f = gw_d.shape[1], gw_d.shape[2]
+        self.ops.grouped_wgrad_multi_shifted(ug_ab[0], ug_ab[1], 2 * f, d, seg_multi, gw_ug, shift_a=f_shift,
+                                             shift_stride=8, max_ctas=self.max_ctas, name="gemm_wgrad_ug")
+        self.ops.grouped_wgrad_multi_shifted(down_ab[0], down_ab[1], d, f, seg_multi, gw_d, shift_b=f_shift,
+                                             shift_stride=8, max_ctas=self.max_ctas, name="gemm_wgrad_down")
+
     def signal(self, flag_ptrs):
         self.ops.signal_peers(flag_ptrs)
 
@@ -780,10 +801,20 @@ class ZpP2PExecutor(ZpExecutor):
     A transfer completes with a release add on the receiver's flag counter (one per kind and
     sender) after the producing kernel; the receiver's stream waits (acquire) for the count of
     exchanges it expects. Only the expert-count all-gather (one per layer and micro-batch, as in
-    the NCCL path) stays a collective. Same task graph, streams and issue order as ZpExecutor."""
+    the NCCL path) stays a collective. Same task graph, streams and issue order as ZpExecutor.
+
+    device_layout (default; HM_ZP_HOST_LAYOUT=1 restores the host path): the all-gathered counts
+    never reach the host. One ``hm_zp_layout`` kernel per (layer, micro-batch), on the dispatch
+    stream right after the count all-gather, computes every sender's destination rows, the
+    owner's expert segments and per-row return addresses, and bump-allocates the micro-batch's
+    saved activations (h, act; dH shares their row numbering) in a per-layer region of a pool
+    sized HM_ZP_POOL_FACTOR (1.5) x the uniform-routing expectation (capped at the worst case).
+    The expert GEMMs read the segment table and pool row shifts from device memory and are sized
+    by the receive capacity; a pool overflow is flagged on the device and raised after the step."""
 
     def __init__(self, graph, shape, M, N, rank, backend, disp_group=None, comb_group=None,
-                 seed: int = 0, durations_hint=None, expert_loads=None, expert_capacity=None):
+                 seed: int = 0, durations_hint=None, expert_loads=None, expert_capacity=None,
+                 device_layout: Optional[bool] = None):
         super().__init__(graph, shape, M, N, rank, backend, disp_group, comb_group, seed, durations_hint,
                          expert_loads, expert_capacity)
         if self.W > 8:
@@ -797,6 +828,50 @@ class ZpP2PExecutor(ZpExecutor):
             raise ValueError("the dispatch group must rank processes like the world")
         self.expected = [[0] * self.W for _ in range(4)]  # per kind, per sender: exchanges seen
         self.owner_sets = [sorted(set(ow)) for ow in self.st.owners]
+        if device_layout is None:
+            device_layout = os.environ.get("HM_ZP_HOST_LAYOUT") != "1" and hasattr(backend, "zp_layout")
+        self.device_layout = bool(device_layout)
+        if self.device_layout:
+            self._init_device_layout()
+
+    def _init_device_layout(self) -> None:
+        s, be, ar, st = self.s, self.be, self.arena, self.st
+        L, R, M, W, E = self.L, self.R, self.M, self.W, s.E
+        dev = be.device
+        self.n_own = [len(o) for o in st.own]
+        self.pool_factor = float(os.environ.get("HM_ZP_POOL_FACTOR", "1.5"))
+        self.pool_base, self.pool_rows = [], []
+        base = 0
+        for n in self.n_own:  # per layer: a pool region for its R micro-batches
+            rows = 0
+            if n:
+                worst = R * s.tokens_per_mb * M * min(s.k, n)
+                expect = R * s.tokens_per_mb * M * s.k * n / E
+                rows = min(worst, int(math.ceil(self.pool_factor * expect / 128.0)) * 128)
+            self.pool_base.append(base)
+            self.pool_rows.append(rows)
+            base += rows
+        self.h_pool = be.tensor((max(base, 1), 2 * s.f))
+        self.act_pool = be.tensor((max(base, 1), s.f))
+        self.dh_pool = be.tensor((max(max(self.pool_rows), 1), 2 * s.f))  # one layer at a time
+        i32, i64 = torch.int32, torch.int64
+        self.owners_t = torch.tensor(st.owners, dtype=i32, device=dev)
+        lj = [(l, j) for l in range(1, L + 1) for j in range(1, R + 1)]
+        self.y_base_t = torch.tensor([[ar.addr(a, l, j, "y") for a in range(M)] for l, j in lj],
+                                     dtype=i64, device=dev).view(L, R, M)
+        self.dx_delta = ar.offset(1, 1, "dx") - ar.offset(1, 1, "y")
+        self.dest_x_t = torch.tensor([[ar.addr(st.owners[l - 1][e], l, j, "x") for e in range(E)] for l, j in lj],
+                                     dtype=i64, device=dev).view(L, R, E)
+        self.dest_dy_t = torch.tensor([[ar.addr(st.owners[l - 1][e], l, j, "dy") for e in range(E)] for l, j in lj],
+                                      dtype=i64, device=dev).view(L, R, E)
+        self.dest_start_t = torch.zeros((L, R, E), dtype=i32, device=dev)
+        self.seg_l = [torch.zeros((R, n + 1), dtype=i32, device=dev) if n else None for n in self.n_own]
+        self.out_rows_y_t = torch.zeros((L, R, ar.cap), dtype=i64, device=dev)
+        self.out_rows_dx_t = torch.zeros((L, R, ar.cap), dtype=i64, device=dev)
+        self.shifts_t = torch.zeros((L, R, 8), dtype=i32, device=dev)
+        self.top_t = torch.zeros((L,), dtype=i32, device=dev)
+        self.err_t = torch.zeros((1,), dtype=i32, device=dev)
+        self.counts_t = torch.zeros((L, R, W, E), dtype=i32, device=dev)
 
     # signalling helpers
     def _signal(self, kind, receivers):
@@ -812,6 +887,31 @@ class ZpP2PExecutor(ZpExecutor):
     # task handlers
     def _attn_permute(self, l, j, zd, r):
         pass  # the permute runs fused with the dispatch, once the receive layout is known
+
+    def _disp_f(self, l, j):
+        if not self.device_layout:
+            return super()._disp_f(l, j)
+        # count all-gather, then the receive layout on the device: no host read of the counts
+        s, be, ar = self.s, self.be, self.arena
+        mine = self.my_counts.get((l, j))
+        if mine is None:
+            mine = be.tensor((s.E,), torch.int32).zero_()
+        cnt = self.counts_t[l - 1, j - 1]
+        dist.all_gather_into_tensor(cnt, mine.to(torch.int32).contiguous(), group=self.disp_group)
+        n = self.n_own[l - 1]
+        be.zp_layout(cnt, self.M, self.owners_t[l - 1], self.rank, n, ar.cap, self.y_base_t[l - 1, j - 1],
+                     self.dx_delta, ar.rb, self.dest_start_t[l - 1, j - 1],
+                     self.seg_l[l - 1][j - 1] if n else None, self.out_rows_y_t[l - 1, j - 1],
+                     self.out_rows_dx_t[l - 1, j - 1], self.shifts_t[l - 1, j - 1], self.top_t[l - 1:l],
+                     self.pool_base[l - 1], self.pool_rows[l - 1], self.err_t)
+        if self.is_attn:
+            x_perm, row_of = be.permute_p2p(self.zd[(l, j)], self.route[(l, j)], self.dest_x_t[l - 1, j - 1],
+                                            self.dest_start_t[l - 1, j - 1])
+            self.x_perm[(l, j)], self.row_of[(l, j)] = x_perm, row_of
+            self._signal(ar.DF, self.owner_sets[l - 1])
+        if self.st.own[l - 1]:
+            self._wait(ar.DF, range(self.M))
+        return None
 
     def _disp_f_finish(self, l, j, gathered):
         s, be, ar = self.s, self.be, self.arena
@@ -849,6 +949,12 @@ class ZpP2PExecutor(ZpExecutor):
         st, be = self.st, self.be
         if not st.own[l - 1]:  # every expert of this rank is offloaded at this layer
             return
+        if self.device_layout:
+            ar = self.arena
+            be.ffn_fwd_pool(ar.view(l, j, "x", ar.cap), self.seg_l[l - 1][j - 1], st.w_ug[l], st.w_d[l],
+                            self.h_pool, self.act_pool, self.shifts_t[l - 1, j - 1],
+                            self.out_rows_y_t[l - 1, j - 1], ar.cap)
+            return
         seg = self.seg[(l, j)]
         self.seg_t[(l, j)] = seg_t = be.seg_tensor(seg)
         x = self.x_recv[(l, j)]
@@ -872,16 +978,24 @@ class ZpP2PExecutor(ZpExecutor):
             if l == self.L:
                 self.dh_next[(l, j)] = self.out_grads[j]
             r = self.route[(l, j)]
+            if self.device_layout:
+                dest_dy, dest_start = self.dest_dy_t[l - 1, j - 1], self.dest_start_t[l - 1, j - 1]
+            else:
+                dest_dy, dest_start = self.dest_dy[(l, j)], self.dest_start[(l, j)]
             self.dw[(l, j)] = be.combine_bwd_p2p(self.dh_next[(l, j)], self.y_perm[(l, j)], self.row_of[(l, j)],
-                                                 r, self.dest_dy[(l, j)], self.dest_start[(l, j)])
+                                                 r, dest_dy, dest_start)
             self._signal(ar.DB, self.owner_sets[l - 1])
         if self.st.own[l - 1]:
             self._wait(ar.DB, range(self.M))
-        self.dy_recv[(l, j)] = ar.view(l, j, "dy", max(self.seg[(l, j)][-1], 1))
+        if not self.device_layout:
+            self.dy_recv[(l, j)] = ar.view(l, j, "dy", max(self.seg[(l, j)][-1], 1))
 
     def _exp_b(self, l, j):
         st, be, ar = self.st, self.be, self.arena
         if not st.own[l - 1]:
+            return
+        if self.device_layout:
+            self._exp_b_pool(l, j)
             return
         seg = self.seg[(l, j)]
         if (l, j) not in self.out_rows_dx:
@@ -901,6 +1015,24 @@ class ZpP2PExecutor(ZpExecutor):
                 self.dh.pop((l, jj), None)
                 self.h_save.pop((l, jj), None)
 
+    def _exp_b_pool(self, l, j):
+        """EXP_B with the device layout: dH lands in the layer's dh buffer addressed by the pool
+        rows of this micro-batch (the buffer pointer is moved back by the layer's first pool row),
+        dX goes straight back to the senders; after the layer's last micro-batch one grouped GEMM
+        per weight forms the layer's weight gradients over all R micro-batches."""
+        st, be, ar, s = self.st, self.be, self.arena, self.s
+        rb_dh = 2 * s.f * 2
+        dh_ptr = self.dh_pool.data_ptr() - self.pool_base[l - 1] * rb_dh
+        dh_rows = self.pool_base[l - 1] + self.pool_rows[l - 1]
+        be.ffn_bwd_data_pool(ar.view(l, j, "dy", ar.cap), self.seg_l[l - 1][j - 1], st.w_ug[l], st.w_d[l],
+                             self.h_pool, dh_ptr, dh_rows, self.shifts_t[l - 1, j - 1],
+                             self.out_rows_dx_t[l - 1, j - 1], ar.cap)
+        if j == self.R:
+            R, me = self.R, self.rank
+            ug = ([dh_ptr] * R, [ar.addr(me, l, jj, "x") for jj in range(1, R + 1)])
+            down = ([ar.addr(me, l, jj, "dy") for jj in range(1, R + 1)], [self.act_pool.data_ptr()] * R)
+            be.ffn_wgrad_pool(ug, down, self.seg_l[l - 1], self.shifts_t[l - 1, :, 1], st.gw_ug[l], st.gw_d[l])
+
     def _comb_b(self, l, j):
         ar = self.arena
         if self.st.own[l - 1]:
@@ -912,7 +1044,17 @@ class ZpP2PExecutor(ZpExecutor):
     def run(self) -> dict:
         for name in ("dest_start", "dest_x", "dest_dy", "out_rows", "out_rows_dx"):
             setattr(self, name, {})
-        return super().run()
+        if self.device_layout:
+            self.top_t.zero_()
+            self.err_t.zero_()
+        out = super().run()
+        if self.device_layout:
+            err = int(self.err_t.item())  # after the step's final synchronise
+            if err:
+                raise RuntimeError(
+                    f"rank {self.rank}: device receive layout overflow (code {err}: 1 = activation pool, "
+                    f"4 = receive slot); raise HM_ZP_POOL_FACTOR (now {self.pool_factor})")
+        return out
 
 
 def merge_rank_intervals(graph: TaskGraph, per_rank: list, M: int) -> MeasuredTimeline:

@@ -467,6 +467,100 @@ def grouped_ffn_bwd_data_rows(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, o
     return dh
 
 
+# Device-side receive layout + pool-placed expert activations (executor.ZpP2PExecutor, no host
+# read of the routed counts)
+
+
+def zp_layout(counts_all, M: int, owners, me: int, n_own: int, cap: int, y_base, dx_delta: int,
+              row_bytes: int, dest_start, seg, out_rows_y, out_rows_dx, shifts, top, pool_base: int,
+              pool_rows: int, err) -> None:
+    """hm_zp_layout: from the all-gathered counts [>=M, E] (device), this rank's send table
+    dest_start[E] (attention ranks) and, for an owner of n_own experts, its segment table, the
+    per-row return addresses and the pool row shifts of its four expert GEMMs."""
+    E = owners.shape[0]
+    _tk = _begin("zp_layout")
+    rc = _native.load().hm_zp_layout(
+        _ptr(counts_all), M, E, _ptr(owners), me, n_own, cap, _ptr(y_base), dx_delta, row_bytes,
+        _ptr(dest_start), _ptr(seg), _ptr(out_rows_y), _ptr(out_rows_dx), _ptr(shifts), _ptr(top),
+        pool_base, pool_rows, _ptr(err), _stream())
+    _end(_tk)
+    _native.check(rc, "hm_zp_layout")
+    _count(1)
+
+
+def _gemm_shifted(mode, a_ptr: int, b, seg, E, rows, a_rows, N, K, out=None, ldo=0, out2=None, ldo2=0,
+                  aux=None, ld_aux=0, out_rows=None, row_shift=None, max_ctas=0, name="grouped_gemm"):
+    _tk = _begin(name)
+    rc = _native.load().hm_grouped_gemm_shifted(
+        mode, a_ptr, _ptr(b), _ptr(seg), E, rows, a_rows, 0, N, K, _ptr(out), ldo if ldo else N, _ptr(out2), ldo2,
+        _ptr(aux), ld_aux, None, _ptr(out_rows), _ptr(row_shift), max_ctas, _stream())
+    _end(_tk)
+    _native.check(rc, "hm_grouped_gemm_shifted")
+    _count(1)
+
+
+def grouped_ffn_fwd_pool(x_slot, seg, w_ug, w_d, h_pool, act_pool, shifts, out_rows, cap: int,
+                         max_ctas: int = 0) -> None:
+    """Forward over a receive slot (x_slot[:cap], expert segments in seg, device) whose h / act go
+    to pool rows at the device-computed base (shifts[0:2]) and whose down projection stores row r
+    at out_rows[r] (the combine return), reading act at shifts[2:4]."""
+    _require_cuda(x_slot, seg, w_ug, w_d, h_pool, act_pool, shifts, out_rows)
+    d = x_slot.shape[1]
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    _gemm_shifted(_native.GEMM_FWD_UPGATE, x_slot.data_ptr(), w_ug, seg, E, cap, cap, 2 * f, d,
+                  out=act_pool, ldo=f, out2=h_pool, ldo2=2 * f, row_shift=shifts[0:2], max_ctas=max_ctas,
+                  name="gemm_fwd_upgate")
+    _gemm_shifted(_native.GEMM_FWD_DOWN, act_pool.data_ptr(), w_d, seg, E, cap, act_pool.shape[0], d, f,
+                  out_rows=out_rows, row_shift=shifts[2:4], max_ctas=max_ctas, name="gemm_fwd_down_p2p")
+
+
+def grouped_ffn_bwd_data_pool(dy_slot, seg, w_ug, w_d, h_pool, dh_ptr: int, dh_rows: int, shifts, out_rows,
+                              cap: int, max_ctas: int = 0) -> None:
+    """Data-gradient backward over a receive slot: dH (SwiGLU backward, reading h at the pool base)
+    goes to the dh buffer at dh_ptr (addressed with the same pool rows, dh_rows of them), and the
+    dX GEMM stores row r at out_rows[r]."""
+    _require_cuda(dy_slot, seg, w_ug, w_d, h_pool, shifts, out_rows)
+    d = dy_slot.shape[1]
+    E, two_f, _ = w_ug.shape
+    f = two_f // 2
+    lib = _native.load()
+    _tk = _begin("gemm_bwd_dact")
+    rc = lib.hm_grouped_gemm_shifted(
+        _native.GEMM_BWD_DACT, dy_slot.data_ptr(), _ptr(w_d), _ptr(seg), E, cap, cap, 0, f, d, dh_ptr, 2 * f,
+        None, 0, _ptr(h_pool), 2 * f, None, None, _ptr(shifts[4:6]), max_ctas, _stream())
+    _end(_tk)
+    _native.check(rc, "hm_grouped_gemm_shifted")
+    _count(1)
+    _gemm_shifted(_native.GEMM_BWD_DX, dh_ptr, w_ug, seg, E, cap, dh_rows, d, 2 * f, out_rows=out_rows,
+                  row_shift=shifts[6:8], max_ctas=max_ctas, name="gemm_bwd_dx_p2p")
+
+
+def grouped_wgrad_multi_shifted(a_ptrs, b_ptrs, M: int, N: int, seg_multi, out, shift_a=None, shift_b=None,
+                                shift_stride: int = 0, max_ctas: int = 0, name: str = "gemm_wgrad_multi") -> None:
+    """out[e] += sum_j A_j[seg_j(e) + sa_j]^T . B_j[seg_j(e) + sb_j] (fp32 accumulate), the per-segment
+    row offsets sa_j = shift_a[j * shift_stride], sb_j likewise (device int32 tensors or None)."""
+    lib = _native.load()
+    R = len(a_ptrs)
+    if R > 16 or out.dtype != torch.float32:
+        raise ValueError("grouped_wgrad_multi_shifted: at most 16 segments, fp32 out")
+    E = seg_multi.shape[1] - 1
+    nbytes = lib.hm_grouped_wgrad_multi_workspace_bytes(E, R)
+    ws = torch.empty((nbytes + 128,), dtype=torch.uint8, device=out.device)
+    off = (-ws.data_ptr()) % 128
+    ws = ws[off:off + nbytes]
+    ap = (ctypes.c_void_p * R)(*a_ptrs)
+    bp = (ctypes.c_void_p * R)(*b_ptrs)
+    rows = (ctypes.c_int * R)(*([1] * R))
+    _tk = _begin(name)
+    rc = lib.hm_grouped_wgrad_multi_shifted(1, ap, bp, rows, _ptr(seg_multi), R, E, M, N, _ptr(out), N,
+                                            _ptr(shift_a), _ptr(shift_b), shift_stride, _ptr(ws), max_ctas,
+                                            _stream())
+    _end(_tk)
+    _native.check(rc, "hm_grouped_wgrad_multi_shifted")
+    _count(2)
+
+
 def signal_peers(flag_ptrs) -> None:
     """+1 (release, system scope) on each listed device counter after this stream's prior work."""
     n = len(flag_ptrs)

@@ -25,7 +25,7 @@ def test_library_exports_all_symbols():
 
 def test_pure_host_entry_points():
     lib = _native.load()
-    assert lib.hm_abi_version() == 2
+    assert lib.hm_abi_version() == 3
     # per-chunk table + the fused router's completion counter
     assert lib.hm_router_chunk_elems(4096, 8) == 64 * 8 + 1
     assert lib.hm_router_chunk_elems(1, 64) == 64 + 1

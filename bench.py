@@ -589,6 +589,10 @@ def run_zp(args, ws, rank, local):
     tl = execute(graph, ex)  # one more iteration, measured per task
     hw = torch.tensor([ex.host_wait_s], device=dev)
     dist.all_reduce(hw, op=dist.ReduceOp.MAX)
+    dl = bool(getattr(ex, "device_layout", False))
+    pool = torch.tensor([float(getattr(ex, "pool_regrows", 0)), (ex.h_pool.numel() + ex.act_pool.numel() +
+                         ex.dh_pool.numel()) * 2 / 2 ** 30 if dl else 0.0], device=dev)
+    dist.all_reduce(pool, op=dist.ReduceOp.MAX)
     # peak device memory of the ZP run: per role (attention / expert ranks), max over ranks
     mem = torch.zeros(2, device=dev)
     mem[0 if rank < M else 1] = torch.cuda.max_memory_allocated(dev) / 2 ** 30
@@ -699,6 +703,9 @@ def run_zp(args, ws, rank, local):
                    graph.assignment, graph.forward_only)
     out["zp"]["resimulated_makespan_ms"] = simulate(g2, default_orders(g2)).makespan / 1e6
     out["zp"]["host_count_wait_ms_max_rank"] = round(float(hw) * 1e3, 3)
+    out["zp"]["receive_layout"] = ({"where": "device (hm_zp_layout)", "pool_factor": getattr(ex, "pool_factor", None),
+                                    "pool_regrows_max_rank": int(pool[0]), "pool_gib_max_rank": round(float(pool[1]), 2)}
+                                   if dl else {"where": "host"})
     out["zp"]["peak_mem_gib"] = {"attention_ranks": round(float(mem[0]), 1),
                                  "expert_ranks": round(float(mem[1]), 1),
                                  "rank0_after_scaling_reference": round(torch.cuda.max_memory_allocated(dev) / 2 ** 30, 1)}

@@ -38,6 +38,7 @@ import contextlib
 import math
 import os
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -817,6 +818,7 @@ class ZpP2PExecutor(ZpExecutor):
                  device_layout: Optional[bool] = None):
         super().__init__(graph, shape, M, N, rank, backend, disp_group, comb_group, seed, durations_hint,
                          expert_loads, expert_capacity)
+        self.expert_loads = expert_loads
         if self.W > 8:
             raise ValueError("p2p transport supports at most 8 ranks (one NVSwitch domain)")
         s = shape
@@ -834,26 +836,37 @@ class ZpP2PExecutor(ZpExecutor):
         if self.device_layout:
             self._init_device_layout()
 
+    def _alloc_pools(self) -> None:
+        """Per-layer pool regions for the saved expert activations of its R micro-batches:
+        pool_factor x the expected rows (the router's per-expert loads when known, else uniform
+        routing), capped at the worst case; dH shares the row numbering, one layer at a time."""
+        s, be, st = self.s, self.be, self.st
+        M, R, E = self.M, self.R, s.E
+        loads = self.expert_loads
+        share = [1.0 / E] * E if not loads or sum(loads) <= 0 else [v / sum(loads) for v in loads]
+        self.pool_base, self.pool_rows = [], []
+        base = 0
+        for own in st.own:
+            rows = 0
+            if own:
+                worst = R * s.tokens_per_mb * M * min(s.k, len(own))
+                expect = R * s.tokens_per_mb * M * s.k * sum(share[e] for e in own)
+                rows = min(worst, int(math.ceil(self.pool_factor * expect / 128.0)) * 128)
+            self.pool_base.append(base)
+            self.pool_rows.append(rows)
+            base += rows
+        self.h_pool = self.act_pool = self.dh_pool = None  # release before reallocating
+        self.h_pool = be.tensor((max(base, 1), 2 * s.f))
+        self.act_pool = be.tensor((max(base, 1), s.f))
+        self.dh_pool = be.tensor((max(max(self.pool_rows), 1), 2 * s.f))
+
     def _init_device_layout(self) -> None:
         s, be, ar, st = self.s, self.be, self.arena, self.st
         L, R, M, W, E = self.L, self.R, self.M, self.W, s.E
         dev = be.device
         self.n_own = [len(o) for o in st.own]
         self.pool_factor = float(os.environ.get("HM_ZP_POOL_FACTOR", "1.5"))
-        self.pool_base, self.pool_rows = [], []
-        base = 0
-        for n in self.n_own:  # per layer: a pool region for its R micro-batches
-            rows = 0
-            if n:
-                worst = R * s.tokens_per_mb * M * min(s.k, n)
-                expect = R * s.tokens_per_mb * M * s.k * n / E
-                rows = min(worst, int(math.ceil(self.pool_factor * expect / 128.0)) * 128)
-            self.pool_base.append(base)
-            self.pool_rows.append(rows)
-            base += rows
-        self.h_pool = be.tensor((max(base, 1), 2 * s.f))
-        self.act_pool = be.tensor((max(base, 1), s.f))
-        self.dh_pool = be.tensor((max(max(self.pool_rows), 1), 2 * s.f))  # one layer at a time
+        self._alloc_pools()
         i32, i64 = torch.int32, torch.int64
         self.owners_t = torch.tensor(st.owners, dtype=i32, device=dev)
         lj = [(l, j) for l in range(1, L + 1) for j in range(1, R + 1)]
@@ -1044,16 +1057,27 @@ class ZpP2PExecutor(ZpExecutor):
     def run(self) -> dict:
         for name in ("dest_start", "dest_x", "dest_dy", "out_rows", "out_rows_dx"):
             setattr(self, name, {})
-        if self.device_layout:
+        if not self.device_layout:
+            return super().run()
+        for attempt in range(4):
             self.top_t.zero_()
             self.err_t.zero_()
-        out = super().run()
-        if self.device_layout:
-            err = int(self.err_t.item())  # after the step's final synchronise
-            if err:
-                raise RuntimeError(
-                    f"rank {self.rank}: device receive layout overflow (code {err}: 1 = activation pool, "
-                    f"4 = receive slot); raise HM_ZP_POOL_FACTOR (now {self.pool_factor})")
+            out = super().run()
+            # every rank learns whether any owner's pool overflowed (then a micro-batch was
+            # skipped there): grow the pools and run the iteration again
+            err = self.err_t.clone()
+            dist.all_reduce(err, op=dist.ReduceOp.MAX, group=self.disp_group)
+            err = int(err.item())
+            if not err:
+                return out
+            if err & 4 or attempt == 3:
+                raise RuntimeError(f"rank {self.rank}: device receive layout overflow (code {err}: 1 = activation "
+                                   f"pool, 4 = receive slot) at HM_ZP_POOL_FACTOR {self.pool_factor}")
+            self.pool_factor *= 1.5
+            self.pool_regrows = getattr(self, "pool_regrows", 0) + 1
+            warnings.warn(f"rank {self.rank}: activation pool overflow; pool factor -> {self.pool_factor:.2f}, "
+                          "iteration repeated")
+            self._alloc_pools()
         return out
 
 

@@ -130,10 +130,10 @@ struct TileBound {
   }
 };
 
-template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS, int NSUB = 1>
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS, int NSUB = 1, bool SHIFT = false>
 int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p,
                 const TileBound& tb, int max_ctas, cudaStream_t stream) {
-  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI, CTAS, NSUB>;
+  auto kern = hm::grouped_gemm_kernel<GROUP_K, A_MN, B_MN, EPI, CTAS, NSUB, SHIFT>;
   using Cfg = hm::TileCfg<CTAS, NSUB>;
   constexpr int smem = Cfg::kSmemBytes;
   const long ub_tiles = tb.tiles(Cfg::kTileM, Cfg::kTileN);
@@ -186,20 +186,20 @@ bool gemm_wide_explicit();
 int gemm_group_m(int mode, long M);
 int g_early_release = getenv("HM_GEMM_NO_EARLY_RELEASE") ? 0 : 1;
 
-template <bool GROUP_K, bool A_MN, bool B_MN, int EPI>
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, bool SHIFT = false>
 int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedGemmParams& p0,
                 const TileBound& tb, int max_ctas, cudaStream_t st) {
   hm::GroupedGemmParams p = p0;
   p.group_m = gemm_group_m(mode, tb.M);
   p.early_release = g_early_release;
-  if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1>(ma, mb, p, tb, max_ctas, st);
+  if (gemm_ctas() == 1) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 1, 1, SHIFT>(ma, mb, p, tb, max_ctas, st);
   bool wide = (gemm_wide_mask() >> mode) & 1;
   // the SwiGLU backward's drain-then-release epilogue holds the single wide accumulator for a
   // fixed few microseconds: worth it against a long K (C2, K = d = 4096: 1043 -> 1165 TFLOP/s),
   // not a short one (C3, K = 2048: 967 -> 764), unless HM_GEMM_WIDE forces the mask
   if (mode == HM_GEMM_BWD_DACT && !gemm_wide_explicit() && tb.K < 4096) wide = false;
-  if (wide) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2>(ma, mb, p, tb, max_ctas, st);
-  return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1>(ma, mb, p, tb, max_ctas, st);
+  if (wide) return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 2, SHIFT>(ma, mb, p, tb, max_ctas, st);
+  return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1, SHIFT>(ma, mb, p, tb, max_ctas, st);
 }
 
 // raster group height per GEMM mode (HM_GEMM_GROUPM = one value for every mode). The per-mode
@@ -568,6 +568,12 @@ int hm_combine_bwd(const void* dy, const void* y_perm, const int32_t* row_of, co
 
 // the dlogit region of the router-backward workspace, padded to 64 floats so the dWg partials
 // after it stay 16-byte aligned (router_wgrad_perm_kernel stores float4; T*k % 4 != 0 faulted)
+// K splits of the router weight-gradient GEMM (E > 8): about two waves of 256-column tiles
+static int router_wgrad_gemm_splits(int d) {
+  const int ntiles = (d + 255) / 256;
+  int s = (2 * num_sms() / 2) / ntiles;  // CTA pairs
+  return s < 1 ? 1 : (s > 16 ? 16 : s);
+}
 static size_t router_bwd_dl_elems(int T, int k) {
   return (static_cast<size_t>(T) * k + 63) & ~static_cast<size_t>(63);
 }
@@ -640,9 +646,17 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
   }
   const bool streamed = dwg && E <= 8 && x && d % hm::kWgCols == 0 && aligned16(x) && !perm_forced &&
                         !getenv("HM_ROUTER_WGRAD_TOK");
+  // E > 8 with the token rows: dWg^T = dl^T . x as a K-split tensor-core GEMM (K3 WGRAD_ACC into
+  // fp32 split partials over S token ranges, then the split reduction), from dense bf16 dlogit rows
+  const size_t dl_el = router_bwd_dl_elems(T, k);
+  const int wg_splits = router_wgrad_gemm_splits(d);
+  const size_t dense_el = ((static_cast<size_t>(T) * E / 2) + 63) & ~static_cast<size_t>(63);
+  const size_t gemm_need = dl_el + dense_el + 64 + 2 * 32 * wg_splits + 32 + static_cast<size_t>(wg_splits) * E * d;
+  const bool gemm_wg = dwg && E > 8 && E % 8 == 0 && x && aligned16(x) && !perm_forced &&
+                       !getenv("HM_ROUTER_WGRAD_TOK") && gemm_need <= hm_router_bwd_part_elems(T, d, E, k);
   const bool tok = dwg && !streamed && E <= 8 && k <= 3 && d % 64 == 0 && !perm_forced;
-  float* dl_perm = (dwg && !tok && !streamed) ? part : nullptr;
-  float* dl_tok = dlogit ? dlogit : (tok ? part : nullptr);
+  float* dl_perm = (dwg && !tok && !streamed && !gemm_wg) ? part : nullptr;
+  float* dl_tok = dlogit ? dlogit : ((tok || gemm_wg) ? part : nullptr);
   float* coef8 = streamed ? part + router_bwd_dl_elems(T, k) : nullptr;
   // k >= 4: metadata broadcast by shuffles, no row prefetch (C3, k = 6: 0.099 vs 0.121 ms);
   // k <= 3: the v1 kernel (C2, k = 2: 0.080 vs 0.088 ms). Both produce bit-identical dx / dlogit
@@ -668,6 +682,27 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
     hm::router_wgrad_stream_kernel<<<dim3(d / hm::kWgCols, S), hm::kWgThreads, smem, st>>>(
         static_cast<const __nv_bfloat16*>(x), coef8, T, d, E, partials);
     if (int rc = check_launch("router_wgrad_stream")) return rc;
+    const long n = static_cast<long>(d) * E;
+    hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(partials, S, d, E, static_cast<__nv_bfloat16*>(dwg));
+    return check_launch("router_wgrad_reduce");
+  }
+  if (gemm_wg) {
+    const int S = wg_splits;
+    auto* dense = reinterpret_cast<__nv_bfloat16*>(part + dl_el);
+    auto* seg = reinterpret_cast<int32_t*>(part + dl_el + dense_el);
+    // 128-byte aligned workspace for the per-split TMA views, then the fp32 split partials
+    uintptr_t wsa = reinterpret_cast<uintptr_t>(part + dl_el + dense_el + 64);
+    wsa = (wsa + 127) & ~static_cast<uintptr_t>(127);
+    void* ws = reinterpret_cast<void*>(wsa);
+    float* partials = reinterpret_cast<float*>(wsa + 2 * 128 * S + 128);
+    const long nchunk = static_cast<long>(T) * (E / 8);
+    HM_K_SWITCH(k, (hm::dense_dlogit_kernel<K><<<static_cast<int>((nchunk + 255) / 256 > 0 ? (nchunk + 255) / 256 : 1),
+                                               256, 0, st>>>(idx, dl_tok, T, E, S, dense, seg)));
+    if (int rc = check_launch("dense_dlogit")) return rc;
+    cudaMemsetAsync(partials, 0, sizeof(float) * static_cast<size_t>(S) * E * d, st);
+    if (int rc = hm_grouped_gemm(HM_GEMM_WGRAD_ACC, dense, x, seg, S, T, E, d, 0, partials, d, nullptr, 0,
+                                 nullptr, 0, ws, 0, stream))
+      return rc;
     const long n = static_cast<long>(d) * E;
     hm::router_wgrad_reduce_kernel<<<(n + 255) / 256, 256, 0, st>>>(partials, S, d, E, static_cast<__nv_bfloat16*>(dwg));
     return check_launch("router_wgrad_reduce");
@@ -899,16 +934,22 @@ int hm_grouped_gemm_shifted(int mode, const void* a, const void* b, const int32_
   p.out_elems = wgrad ? static_cast<long>(E) * M * ldo : static_cast<long>(rows) * ldo;
   const TileBound tb{wgrad, rows, M, N, E, K};
   switch (mode) {
+    // pool-placed operands (row_shift) run their own instantiation, so the plain GEMMs compile
+    // exactly as without the feature
     case HM_GEMM_FWD_UPGATE:
       if (N % 256 != 0 || !out2) return fail(HM_E_SHAPE, "upgate: N=2f must be a multiple of 256 and h given");
-      return launch_kind<false, false, false, hm::EPI_SWIGLU_FWD>(mode, ma, mb, p, tb, max_ctas, st);
+      return row_shift ? launch_kind<false, false, false, hm::EPI_SWIGLU_FWD, true>(mode, ma, mb, p, tb, max_ctas, st)
+                       : launch_kind<false, false, false, hm::EPI_SWIGLU_FWD>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_FWD_DOWN:
-      return launch_kind<false, false, false, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
+      return row_shift ? launch_kind<false, false, false, hm::EPI_STORE, true>(mode, ma, mb, p, tb, max_ctas, st)
+                       : launch_kind<false, false, false, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_BWD_DACT:
       if (N % 128 != 0 || !aux) return fail(HM_E_SHAPE, "dact: N=f must be a multiple of 128 and h given");
-      return launch_kind<false, false, true, hm::EPI_SWIGLU_BWD>(mode, ma, mb, p, tb, max_ctas, st);
+      return row_shift ? launch_kind<false, false, true, hm::EPI_SWIGLU_BWD, true>(mode, ma, mb, p, tb, max_ctas, st)
+                       : launch_kind<false, false, true, hm::EPI_SWIGLU_BWD>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_BWD_DX:
-      return launch_kind<false, false, true, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
+      return row_shift ? launch_kind<false, false, true, hm::EPI_STORE, true>(mode, ma, mb, p, tb, max_ctas, st)
+                       : launch_kind<false, false, true, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_WGRAD:
       return launch_kind<true, true, true, hm::EPI_STORE>(mode, ma, mb, p, tb, max_ctas, st);
     case HM_GEMM_WGRAD_ACC:

@@ -83,7 +83,14 @@ struct GroupedGemmParams {
   const __nv_bfloat16* aux;  // SWIGLU_BWD: h saved by the forward [rows, 2N]
   int ld_aux;
   int group_m;    // raster: m-tiles per group (m fastest inside a group, then n, then next group)
-  const CUtensorMap* expert_maps;  // GROUP_K: per-(expert, segment) TMA views, [(e*R+j)*2] = A, +1 = B
+  union {  // (keeps the parameter block at 128 bytes: a larger one is read through a generic
+           // pointer, which cost the SwiGLU-backward epilogue 20 %)
+    const CUtensorMap* expert_maps;  // GROUP_K: per-(expert, segment) TMA views, [(e*R+j)*2] = A, +1 = B
+    const int* row_shift;  // GROUP_M kernels instantiated with SHIFT: device int[2] {a, o}, rows
+                           // added to the segment rows of the A operand (a) and of the out / out2
+                           // / aux buffers (o), for operands placed in a pool at a device-computed
+                           // base; o must be 0 when out_rows is given (indexed by segment row)
+  };
   int R;                           // GROUP_K: segments per expert (seg_offsets is [R][E+1])
   float* out_f32;                  // EPI_ACC_F32: fp32 accumulation target (same indexing as out)
   int dynamic;  // 1: one cluster per tile + cluster-launch-control work stealing; 0: persistent
@@ -91,10 +98,6 @@ struct GroupedGemmParams {
   const unsigned long long* out_rows;  // EPI_STORE: optional per-output-row destination pointer
                                        // (row r -> bf16* out_rows[r], may be a peer GPU's memory)
   long out_elems;  // elements of out (bounds checks in HM_BOUNDS_CHECK builds)
-  const int* row_shift;  // GROUP_M, optional device int[2] {a, o}: rows added to the segment rows
-                         // of the A operand (a) and of the out / out2 / aux buffers (o), for
-                         // operands placed in a pool at a device-computed base; o must be 0 when
-                         // out_rows is given (out_rows is indexed by segment row)
   int early_release;  // wide plain-store epilogue: release the accumulator before the last stores
 };
 
@@ -309,7 +312,7 @@ HM_DEV void store_row32(__nv_bfloat16* dst, const float* v, int valid_cols) {
   }
 }
 
-template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS, int NSUB>
+template <bool GROUP_K, bool A_MN, bool B_MN, int EPI, int CTAS, int NSUB, bool SHIFT>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b, GroupedGemmParams p) {
@@ -383,7 +386,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
 
   const int total_tiles = sh.tile_prefix[E];
-
   const uint32_t tmem_base = sh.tmem_base;
 
   if (warp == 0) {
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // 4x the DRAM reads, profiles/r1_gemm_full_2cta_policies.md)
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = pol_a;
-      const int a_shift = (!GROUP_K && p.row_shift) ? p.row_shift[0] : 0;
+      const int a_shift = (SHIFT && !GROUP_K) ? p.row_shift[0] : 0;
       uint32_t it = 0;
       unsigned long long st_empty = 0;
       uint32_t ci = 0;
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     // ======================= epilogue (warps 2..9) =======================
     // pool-placed out / out2 / aux rows (device-computed base; 0 whenever out_rows is used)
-    const int o_shift = (!GROUP_K && p.row_shift) ? p.row_shift[1] : 0;
+    const int o_shift = (SHIFT && !GROUP_K) ? p.row_shift[1] : 0;
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;  // column half of the 256-wide accumulator
     const int row_in_tile = static_cast<int>(rank) * kBM + quad * 32 + lane;

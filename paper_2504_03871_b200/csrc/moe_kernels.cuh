@@ -1397,6 +1397,29 @@ __global__ void __launch_bounds__(17 * 32, 1)
   }
 }
 
+// Dense bf16 dlogit rows dl[T][E] (zero except the k routed experts of each token) from the
+// per-slot dlogits in token order, and the K-split segment table {0, T/S, ..., T}: the operands
+// of the router weight gradient as one tensor-core GEMM, dWg^T[E][d] = sum_t dl[t]^T x[t]
+// (E > 8: each token row of x read once, instead of once per routed copy).
+template <int K>
+__global__ void __launch_bounds__(256)
+    dense_dlogit_kernel(const int32_t* __restrict__ idx, const float* __restrict__ dl_tok, int T, int E,
+                        int S, __nv_bfloat16* __restrict__ dl, int32_t* __restrict__ seg) {
+  if (blockIdx.x == 0 && threadIdx.x <= S) seg[threadIdx.x] = static_cast<int>(static_cast<long>(T) * threadIdx.x / S);
+  const int nc = E >> 3;
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(T) * nc) return;
+  const int t = static_cast<int>(i / nc), c = static_cast<int>(i % nc);
+  float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int e = idx[static_cast<long>(t) * K + s];
+    if ((e >> 3) == c) v[e & 7] = dl_tok[static_cast<long>(t) * K + s];
+  }
+  *reinterpret_cast<uint4*>(dl + static_cast<long>(t) * E + c * 8) =
+      make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+}
+
 __global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int nsplit, int d, int E,
                                            __nv_bfloat16* __restrict__ dwg /*[d][E]*/) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;

@@ -225,6 +225,36 @@ def test_router_bwd_streamed_wgrad_vs_fp32(cfg):
         assert orc.rel_err(outs[v][2], ref) < 5e-3, v
 
 
+@pytest.mark.parametrize("cfg", [LayerConfig("E64d2048k6", 64, 6, 2048, 128, 3000),
+                                 LayerConfig("E16d1024k4", 16, 4, 1024, 128, 777)], ids=lambda c: c.name)
+def test_router_bwd_gemm_wgrad_vs_fp32(cfg):
+    """E > 8: the router weight gradient as a K-split tensor-core GEMM over the token rows (dense
+    bf16 dlogit rows, fp32 split partials) against the per-expert path over the routed copies
+    (HM_ROUTER_WGRAD_PERM) and a plain fp32 x^T . dlogit_dense; dx and dlogit bitwise equal."""
+    import os
+
+    inp = make_inputs(cfg, seed=23)
+    x, wg = inp.x.cuda(), inp.wg.cuda()
+    r = ops.router_topk(x, wg, cfg.k)
+    xp, _, row_of = ops.dispatch_permute(x, r)
+    g = torch.Generator(device="cuda").manual_seed(6)
+    dxp = torch.randn(xp.shape, generator=g, device="cuda").to(xp.dtype)
+    dw = torch.randn(r.w.shape, generator=g, device="cuda")
+    wg_t = ops.transpose_bf16(wg)
+    gemm = ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x)
+    os.environ["HM_ROUTER_WGRAD_PERM"] = "1"
+    try:
+        perm = ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=x)
+    finally:
+        os.environ.pop("HM_ROUTER_WGRAD_PERM")
+    torch.cuda.synchronize()
+    assert torch.equal(gemm[0], perm[0]) and torch.equal(gemm[1], perm[1])
+    dense = torch.zeros((cfg.T, cfg.E), device="cuda").scatter_(1, r.idx.long(), gemm[1].float())
+    ref = x.float().t() @ dense
+    assert orc.rel_err(perm[2], ref) < 5e-3
+    assert orc.rel_err(gemm[2], ref) < 5e-3
+
+
 def test_c_abi_grouped_ffn_entry_points_match_ops():
     """hm_grouped_ffn_fwd / hm_grouped_ffn_bwd — the C-ABI compositions a C/C++ runtime calls for
     EXP_F / EXP_B (include/hetermoe.h) — called through ctypes exactly as INTEGRATION.md shows,

@@ -506,7 +506,8 @@ def run_zp(args, ws, rank, local):
         loads = [int(v) for v in lt.tolist()]
     # the planner's expert GPU is the slowest expert rank (Algorithm 1 models one expert class)
     durs = measure_durations(shape, M, N, expert_max_ctas=ctas(min(caps)), device=dev, loads=loads,
-                             capacity=caps if hetero else None)
+                             capacity=caps if hetero else None, microbatches=args.microbatches,
+                             balance_roles=not args.raw_attention_duration)
     # profiler -> planner, memory and transport: measured bytes per expert,
     # activation bytes per role and the device capacity become the spec's memory model (n_min /
     # n_max bounds of Algorithm 1); the (layer, micro-batch) exchange is timed on NCCL
@@ -538,7 +539,9 @@ def run_zp(args, ws, rank, local):
     from fractions import Fraction
 
     durs.update(transport_ns)
-    plan_durs = {k_: v for k_, v in durs.items() if k_ != "gamma_x100"}
+    from paper_2504_03871_b200.profiler import PLANNER_DURATION_KEYS
+
+    plan_durs = {k_: v for k_, v in durs.items() if k_ in PLANNER_DURATION_KEYS}
     spec = make_zp_spec(M, N, args.layers, args.microbatches, c.E, c.k, args.mb_tokens, c.d,
                         asym_ea=not args.no_asym_ea, gamma=Fraction(durs["gamma_x100"], 100),
                         **plan_durs, **mem_fields)
@@ -894,6 +897,8 @@ def main():
     ap.add_argument("--microbatches", type=int, default=8, help="ZP (N>1): micro-batches R")
     ap.add_argument("--mb-tokens", type=int, default=4096, help="ZP (N>1): tokens per micro-batch per attention rank")
     ap.add_argument("--no-attention", action="store_true", help="ZP: identity attention block")
+    ap.add_argument("--raw-attention-duration", action="store_true",
+                    help="ZP: plan with the attention forward as measured (no fwd+bwd role normalisation)")
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
     ap.add_argument("--router-skew", type=float, default=0.0,
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")

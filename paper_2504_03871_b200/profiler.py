@@ -64,13 +64,23 @@ def measure_loads(shape, device="cuda", seed: int = 0) -> list:
 
 
 def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_ctas: int = 0,
-                      device="cuda", seed: int = 0, loads=None, capacity=None) -> dict:
+                      device="cuda", seed: int = 0, loads=None, capacity=None, microbatches: int = 8,
+                      balance_roles: bool = True) -> dict:
     """Duration table (ns) for ``planner.make_zp_spec`` measured with the native kernels.
     With ``loads`` (``measure_loads``) the expert layer is timed on the busiest expert rank of
     the load-balanced placement (the reference's ``load_factor`` for skew, costmodel.py:54-63),
     with that rank's real per-expert row counts; with per-rank ``capacity`` weights the busiest
     rank is the one with the largest load / capacity, and ``expert_max_ctas`` should be that
-    rank's grid cap (the caller passes the slowest rank's)."""
+    rank's grid cap (the caller passes the slowest rank's).
+
+    Backward: the reference prices every backward task at gamma x its forward (one gamma for all
+    kinds, ``core.py:113-122``). gamma is measured on the expert layer as the executor runs it
+    (data gradients per micro-batch, the layer's weight gradients once over ``microbatches``
+    micro-batches, so 1/R of that launch per micro-batch). The attention rank's backward (router
+    backward, attention + pre-norm autograd, combine backward) has a larger ratio on B200 (~3 vs
+    ~2), so with ``balance_roles`` the attention forward handed to the planner is normalised to
+    (fwd + bwd) / (1 + gamma): its forward + backward total is the measured one and Algorithm 1
+    balances the roles on their real per-micro-batch work. The raw times are returned beside it."""
     from . import ops
     from .executor import attention_block, rms_norm
 
@@ -97,6 +107,24 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
         ops.dispatch_permute(z, r)
 
     attn_ms = _time_ms(attn_step)
+    # the attention rank's backward of one micro-batch, as ATTN_B / DISP_B run it
+    wqkv_p, wo_p = wqkv.clone().requires_grad_(), wo.clone().requires_grad_()
+    wg_t = ops.transpose_bf16(wg)
+    y_perm, dxp, dh_out = rnd(T * k, d), rnd(T * k, d), rnd(T, d)
+
+    def attn_fwd_bwd():
+        hh = x.detach().requires_grad_()
+        with torch.enable_grad():
+            u = attention_block(hh, wqkv_p, wo_p, heads) if shape.attention else hh * 1
+            z = rms_norm(u)
+        zd = z.detach()
+        r = ops.router_topk(zd, wg, k, bias)
+        xp, _, row_of = ops.dispatch_permute(zd, r)
+        _dy_perm, dw = ops.combine_bwd(dh_out, y_perm, row_of, r.w)
+        dz, _dl, _dwg = ops.router_bwd(dxp, row_of, r, dw, xp, wg_t, want_dwg=True, x=zd)
+        torch.autograd.backward([u, z], [dh_out, dz.to(z.dtype)])
+
+    attn_bwd_ms = max(_time_ms(attn_fwd_bwd) - attn_ms, 0.0)
 
     B = T * M * k // N
     e_local = E // N
@@ -124,22 +152,39 @@ def measure_durations(shape, M: int, N: int, expert_max_ctas: int = 0, attn_max_
     seg1 = torch.tensor([0, min(B1, B)], dtype=torch.int32, device=dev)
     single_ms = _time_ms(lambda: ops.grouped_ffn_fwd(xb, seg1, w_ug[:1].contiguous(), w_d[:1].contiguous(),
                                                      attn_max_ctas))
-    # backward factor gamma: the expert layer's measured backward / forward time (the reference
-    # applies one gamma to every task kind, core.py:113-122)
+    # backward factor gamma: the expert layer's backward as the executor runs it (data gradients
+    # per micro-batch + 1/R of the layer's once-per-layer weight-gradient launch) / forward
     y, h, act = ops.grouped_ffn_fwd(xb, seg, w_ug, w_d, expert_max_ctas)
     gw_ug = torch.zeros(w_ug.shape, dtype=torch.float32, device=dev)
     gw_d = torch.zeros(w_d.shape, dtype=torch.float32, device=dev)
-    bwd_ms = _time_ms(lambda: ops.grouped_ffn_bwd_acc(y, xb, h, act, seg, w_ug, w_d, gw_ug, gw_d,
-                                                      expert_max_ctas))
+    data_ms = _time_ms(lambda: ops.grouped_ffn_bwd_data(y, xb, h, act, seg, w_ug, w_d, expert_max_ctas))
+    _dx, dh = ops.grouped_ffn_bwd_data(y, xb, h, act, seg, w_ug, w_d, expert_max_ctas)
+    R = max(1, int(microbatches))
+    seg_multi = seg.view(1, -1).repeat(R, 1).contiguous()
+
+    def wgrad_layer():
+        ops.grouped_wgrad_multi([dh] * R, [xb] * R, seg_multi, gw_ug, max_ctas=expert_max_ctas)
+        ops.grouped_wgrad_multi([y] * R, [act] * R, seg_multi, gw_d, max_ctas=expert_max_ctas)
+
+    bwd_ms = data_ms + _time_ms(wgrad_layer, reps=2, warmup=1) / R
+    gamma = bwd_ms / exp_ms
+    attn_plan_ms = (attn_ms + attn_bwd_ms) / (1.0 + gamma) if balance_roles else attn_ms
     comm_ns = T * k * d * 2 / (NVLINK_GBS * 1e9) * 1e9
     return {
-        "gamma_x100": int(round(100 * bwd_ms / exp_ms)),
-        "attn_fwd_ns": int(attn_ms * 1e6),
+        "gamma_x100": int(round(100 * gamma)),
+        "attn_fwd_ns": int(attn_plan_ms * 1e6),
         "expert_layer_fwd_ns": int(exp_ms * 1e6),
         "single_expert_fwd_ns": int(single_ms * 1e6),
         "dispatch_ns": int(comm_ns),
         "combine_ns": int(comm_ns),
+        # measured, for the record (not planner inputs)
+        "attn_fwd_measured_ns": int(attn_ms * 1e6),
+        "attn_bwd_measured_ns": int(attn_bwd_ms * 1e6),
+        "expert_layer_bwd_measured_ns": int(bwd_ms * 1e6),
     }
+
+
+PLANNER_DURATION_KEYS = ("attn_fwd_ns", "expert_layer_fwd_ns", "single_expert_fwd_ns", "dispatch_ns", "combine_ns")
 
 
 def measure_memory(shape, device="cuda", seed: int = 0) -> dict:

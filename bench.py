@@ -565,7 +565,8 @@ def run_zp(args, ws, rank, local):
         graph = build_zp_graph(spec, dur, assignment, mode="zp-full")
     disp = dist.new_group(list(range(ws)))
     comb = dist.new_group(list(range(ws)))
-    be = NativeBackend(dev, max_ctas=exp_ctas if rank >= M else 0)
+    be = NativeBackend(dev, max_ctas=exp_ctas if rank >= M else args.attn_gemm_ctas,
+                       comm_priority=args.comm_priority)
     ex_cls = ZpP2PExecutor if args.transport == "p2p" else ZpExecutor
     ex = ex_cls(graph, shape, M, N, rank, be, disp, comb, seed=1234, expert_loads=loads,
                 expert_capacity=caps if hetero else None)
@@ -631,6 +632,8 @@ def run_zp(args, ws, rank, local):
             "attention_block": not args.no_attention, "parallelism": f"zp{M}+{N}",
             "asym_ea_offload": list(assignment.offload),
             "transport": args.transport, "schedule": args.schedule, "expert_capacity": caps,
+            "comm_stream_priority": "high" if args.comm_priority else "default",
+            "attention_rank_gemm_ctas": args.attn_gemm_ctas or sms,
             "expert_grid_ctas": [ctas(w) or sms for w in caps],
             "router_skew_zipf": args.router_skew,
             "expert_placement": ("contiguous" if loads is None and not hetero else
@@ -897,6 +900,9 @@ def main():
     ap.add_argument("--microbatches", type=int, default=8, help="ZP (N>1): micro-batches R")
     ap.add_argument("--mb-tokens", type=int, default=4096, help="ZP (N>1): tokens per micro-batch per attention rank")
     ap.add_argument("--no-attention", action="store_true", help="ZP: identity attention block")
+    ap.add_argument("--attn-gemm-ctas", type=int, default=0,
+                    help="ZP: cap the offloaded-expert GEMM grid on attention ranks (SMs left to the comm kernels)")
+    ap.add_argument("--comm-priority", action="store_true", help="ZP: high stream priority for the comm lanes")
     ap.add_argument("--raw-attention-duration", action="store_true",
                     help="ZP: plan with the attention forward as measured (no fwd+bwd role normalisation)")
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")

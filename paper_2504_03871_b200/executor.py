@@ -130,13 +130,18 @@ class NativeBackend:
     # task's host-blocking half without changing any communicator's op order on the device
     defer_host_sync = True
 
-    def __init__(self, device, max_ctas: int = 0):
+    def __init__(self, device, max_ctas: int = 0, comm_priority: bool = False):
         from . import ops  # requires the built extension; fails loudly otherwise
 
         self.ops = ops
         self.device = torch.device(device)
         self.max_ctas = max_ctas
-        self.streams = {lane: torch.cuda.Stream(self.device) for lane in ("compute", "dispatch", "combine")}
+        # comm_priority: the dispatch / combine lanes' kernels (permute with peer stores, combine
+        # backward, flags) get the high stream priority, so the CTA scheduler places them ahead
+        # of pending GEMM clusters of the compute lane
+        prio = {"compute": 0, "dispatch": -1 if comm_priority else 0, "combine": -1 if comm_priority else 0}
+        self.streams = {lane: torch.cuda.Stream(self.device, priority=prio[lane])
+                        for lane in ("compute", "dispatch", "combine")}
         self.dtype = torch.bfloat16
 
     # streams / events

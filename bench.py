@@ -495,6 +495,16 @@ def run_zp(args, ws, rank, local):
     hetero = len(set(caps)) > 1
     shape = ZpLayerShape(c.E, c.k, c.d, c.f, args.mb_tokens, attention=not args.no_attention,
                          router_skew=args.router_skew)
+    # the per-GPU scaling comparator (rank 0): the identical stack on ONE GPU, measured first,
+    # while the device holds nothing else (at 8 GPUs the ZP arena and activation pools alone take
+    # ~100 GB per rank); every other rank waits at the barrier
+    stack_ref = None
+    if not args.no_stack_reference:
+        if rank == 0:
+            stack_ref = stack_single_gpu(shape, args.layers, M * args.microbatches, dev)
+            torch.cuda.empty_cache()
+            torch.cuda.reset_peak_memory_stats(dev)
+        barrier(ws)
     loads = None
     if args.router_skew and not args.no_balanced_placement:
         # skewed router: expected per-expert loads (rank 0's measurement) drive a load-balanced
@@ -665,16 +675,16 @@ def run_zp(args, ws, rank, local):
     }
     from paper_2504_03871_b200 import simulate, default_orders
 
-    if not args.no_stack_reference:
+    if stack_ref is not None:
         # the same work (all M x R micro-batches, all layers, attention + MoE) on this one GPU
         # without the pipeline: the per-GPU comparator for scaling (the N = 1 bench line is the
         # bare MoE layer, BASELINE configs[1])
-        v1, ms1 = stack_single_gpu(shape, args.layers, M * args.microbatches, dev)
+        v1, ms1 = stack_ref
         out["scaling_reference"] = {
             "value": v1, "unit": UNIT, "ms_per_iteration": round(ms1, 3),
             "workload": ("identical stack and token count on ONE GPU, no pipeline, in 8192-token chunks "
                          "(weight gradients formed once per chunk and layer, as the "
-                         "executor forms them once per layer) — rank 0, after the timed region"),
+                         "executor forms them once per layer) — rank 0, before the ZP setup"),
             "per_gpu_efficiency": value / (ws * v1),
         }
     out["zp"]["simulated_makespan_ms"] = simulate(graph, default_orders(graph)).makespan / 1e6
@@ -714,7 +724,7 @@ def run_zp(args, ws, rank, local):
                                    if dl else {"where": "host"})
     out["zp"]["peak_mem_gib"] = {"attention_ranks": round(float(mem[0]), 1),
                                  "expert_ranks": round(float(mem[1]), 1),
-                                 "rank0_after_scaling_reference": round(torch.cuda.max_memory_allocated(dev) / 2 ** 30, 1)}
+                                 "rank0_zp_run": round(torch.cuda.max_memory_allocated(dev) / 2 ** 30, 1)}
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(c, args.cpu_baseline_tokens)
     _emit(out)

@@ -814,7 +814,7 @@ class ZpP2PExecutor(ZpExecutor):
     stream right after the count all-gather, computes every sender's destination rows, the
     owner's expert segments and per-row return addresses, and bump-allocates the micro-batch's
     saved activations (h, act; dH shares their row numbering) in a per-layer region of a pool
-    sized HM_ZP_POOL_FACTOR (1.5) x the uniform-routing expectation (capped at the worst case).
+    sized HM_ZP_POOL_FACTOR (1.25) x the expected rows (capped at the worst case and by free memory).
     The expert GEMMs read the segment table and pool row shifts from device memory and are sized
     by the receive capacity; a pool overflow is flagged on the device and raised after the step."""
 
@@ -849,18 +849,37 @@ class ZpP2PExecutor(ZpExecutor):
         M, R, E = self.M, self.R, s.E
         loads = self.expert_loads
         share = [1.0 / E] * E if not loads or sum(loads) <= 0 else [v / sum(loads) for v in loads]
-        self.pool_base, self.pool_rows = [], []
-        base = 0
-        for own in st.own:
-            rows = 0
-            if own:
-                worst = R * s.tokens_per_mb * M * min(s.k, len(own))
-                expect = R * s.tokens_per_mb * M * s.k * sum(share[e] for e in own)
-                rows = min(worst, int(math.ceil(self.pool_factor * expect / 128.0)) * 128)
-            self.pool_base.append(base)
-            self.pool_rows.append(rows)
-            base += rows
+
+        def regions(factor):
+            bases, rows_l, base = [], [], 0
+            for own in st.own:
+                rows = 0
+                if own:
+                    worst = R * s.tokens_per_mb * M * min(s.k, len(own))
+                    expect = R * s.tokens_per_mb * M * s.k * sum(share[e] for e in own)
+                    rows = min(worst, int(math.ceil(factor * expect / 128.0)) * 128)
+                bases.append(base)
+                rows_l.append(rows)
+                base += rows
+            return bases, rows_l, base
+
         self.h_pool = self.act_pool = self.dh_pool = None  # release before reallocating
+        bases, rows_l, base = regions(self.pool_factor)
+        row_bytes = 3 * s.f * 2  # h + act per pool row; dH: one layer's rows
+        need = base * row_bytes + max(rows_l) * 2 * s.f * 2
+        if be.device.type == "cuda":
+            # fit the pools in what the device has left (8 GiB headroom for the step's transients)
+            torch.cuda.empty_cache()
+            free = torch.cuda.mem_get_info(be.device)[0] - (8 << 30)
+            if need > free:
+                fit = self.pool_factor * free / need
+                if fit < 1.0:
+                    raise RuntimeError(f"rank {self.rank}: activation pools need {need / 2**30:.1f} GiB at the "
+                                       f"expected routed rows, {free / 2**30:.1f} GiB free")
+                warnings.warn(f"rank {self.rank}: pool factor {self.pool_factor:.2f} -> {fit:.2f} to fit memory")
+                self.pool_factor = fit
+                bases, rows_l, base = regions(fit)
+        self.pool_base, self.pool_rows = bases, rows_l
         self.h_pool = be.tensor((max(base, 1), 2 * s.f))
         self.act_pool = be.tensor((max(base, 1), s.f))
         self.dh_pool = be.tensor((max(max(self.pool_rows), 1), 2 * s.f))
@@ -870,7 +889,7 @@ class ZpP2PExecutor(ZpExecutor):
         L, R, M, W, E = self.L, self.R, self.M, self.W, s.E
         dev = be.device
         self.n_own = [len(o) for o in st.own]
-        self.pool_factor = float(os.environ.get("HM_ZP_POOL_FACTOR", "1.5"))
+        self.pool_factor = float(os.environ.get("HM_ZP_POOL_FACTOR", "1.25"))
         self._alloc_pools()
         i32, i64 = torch.int32, torch.int64
         self.owners_t = torch.tensor(st.owners, dtype=i32, device=dev)

@@ -62,6 +62,8 @@ class ClockSampler:
     def __init__(self, index: int, period: float = 0.02):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
+        self.power_w = []
+        self.limit_w = None
         self._stop = threading.Event()
         self._thread = None
         self.max_mhz = None
@@ -72,6 +74,10 @@ class ClockSampler:
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self._h) / 1000.0
+            except Exception:  # noqa: BLE001
+                self.limit_w = None
         except Exception:  # noqa: BLE001 - clocks are best effort
             self._nv = None
 
@@ -79,6 +85,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                try:
+                    self.power_w.append(self._nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
+                except Exception:  # noqa: BLE001
+                    pass
                 mask = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
                 for name, bit in self.REASONS.items():
                     if mask & bit and name != "gpu_idle":
@@ -101,8 +111,10 @@ class ClockSampler:
     def summary(self):
         s = sorted(self.samples)
         med = s[len(s) // 2] if s else None
+        pw = sorted(self.power_w)
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(s)}
+                "samples": len(s), "power_w_median": pw[len(pw) // 2] if pw else None,
+                "power_limit_w": self.limit_w}
 
 
 # ---------------------------------------------------------------------------------------------

@@ -142,7 +142,8 @@ int hm_grouped_gemm_shifted(int mode, const void* a, const void* b, const int32_
  *                                     region of pool_rows rows (*top: device counter, zeroed by the
  *                                     caller before the layer's first micro-batch)
  * A pool or slot overflow ORs 1 / 4 (pool / receive slot) into *err and empties the segments (the
- * GEMMs then skip this micro-batch); the caller checks *err after the step.
+ * GEMMs then skip this micro-batch), an owner id outside [0, 16) ORs 8; the caller checks *err
+ * after the step.
  * Replaces the host-side receive layout of the count exchange. */
 int hm_zp_layout(const int32_t* counts_all, int M, int E, const int32_t* owners, int me, int n_own,
                  int cap, const unsigned long long* y_base, long long dx_delta, int row_bytes,

@@ -1616,6 +1616,11 @@ __global__ void __launch_bounds__(kZpLayoutThreads)
       int tot = 0;
       for (int a = 0; a < M; ++a) tot += s_cnt[a][e];
       const int o = s_own[e];
+      if (o < 0 || o >= kZpMaxPeersLayout) {  // not a rank of the exchange: flag, place nowhere
+        atomicOr(err, 8);
+        s_start[e] = 0;
+        continue;
+      }
       s_start[e] = run[o];
       run[o] += tot;
     }

@@ -1094,9 +1094,10 @@ class ZpP2PExecutor(ZpExecutor):
             err = int(err.item())
             if not err:
                 return out
-            if err & 4 or attempt == 3:
-                raise RuntimeError(f"rank {self.rank}: device receive layout overflow (code {err}: 1 = activation "
-                                   f"pool, 4 = receive slot) at HM_ZP_POOL_FACTOR {self.pool_factor}")
+            if err & ~1 or attempt == 3:
+                raise RuntimeError(f"rank {self.rank}: device receive layout error (code {err}: 1 = activation "
+                                   f"pool overflow, 4 = receive slot overflow, 8 = owner outside the exchange) "
+                                   f"at HM_ZP_POOL_FACTOR {self.pool_factor}")
             self.pool_factor *= 1.5
             self.pool_regrows = getattr(self, "pool_regrows", 0) + 1
             warnings.warn(f"rank {self.rank}: activation pool overflow; pool factor -> {self.pool_factor:.2f}, "

@@ -63,6 +63,7 @@ class ClockSampler:
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.power_w = []
+        self.power_source = None
         self.limit_w = None
         self._stop = threading.Event()
         self._thread = None
@@ -81,12 +82,28 @@ class ClockSampler:
         except Exception:  # noqa: BLE001 - clocks are best effort
             self._nv = None
 
+    def _power_w(self):
+        # instantaneous board power (NVML_FI_DEV_POWER_INSTANT); nvmlDeviceGetPowerUsage is a
+        # ~1 s running average on B200 and lags a sub-second timed region toward idle
+        nv = self._nv
+        fi = getattr(nv, "NVML_FI_DEV_POWER_INSTANT", None)
+        if fi is not None and self.power_source != "average":
+            try:
+                v = nv.nvmlDeviceGetFieldValues(self._h, [fi])[0]
+                if v.nvmlReturn == 0:
+                    self.power_source = "instant"
+                    return float(v.value.uiVal) / 1000.0
+            except Exception:  # noqa: BLE001
+                pass
+        self.power_source = "average"
+        return nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0
+
     def _run(self):
         while not self._stop.is_set():
             try:
                 self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
                 try:
-                    self.power_w.append(self._nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
+                    self.power_w.append(self._power_w())
                 except Exception:  # noqa: BLE001
                     pass
                 mask = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
@@ -114,7 +131,7 @@ class ClockSampler:
         pw = sorted(self.power_w)
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(s), "power_w_median": pw[len(pw) // 2] if pw else None,
-                "power_limit_w": self.limit_w}
+                "power_limit_w": self.limit_w, "power_source": self.power_source}
 
 
 # ---------------------------------------------------------------------------------------------

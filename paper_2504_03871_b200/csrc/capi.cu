@@ -3,6 +3,7 @@
 // Host-side responsibilities only: argument validation, TMA descriptor encoding
 // (cuTensorMapEncodeTiled through the runtime's driver entry point; no -lcuda), grid sizing
 // and launches on the caller's stream. No allocation, no synchronisation.
+#include <atomic>
 #include <vector>
 #include <cstdarg>
 #include <cstdlib>
@@ -61,6 +62,21 @@ int permute_split_override() {
     }
   }
   return v;
+}
+
+// Opt a kernel into `smem` bytes of dynamic shared memory once per DEVICE (the attribute belongs
+// to the device's context: a process that drives several GPUs must set it on each). `done` is the
+// call site's bitmask of devices already set.
+template <typename Kern>
+int ensure_smem_attr(Kern kern, size_t smem, std::atomic<unsigned long long>& done, const char* what) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return 0;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return fail(static_cast<int>(e), "%s smem attr: %s", what, cudaGetErrorString(e));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return 0;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -137,12 +153,8 @@ int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const hm::GroupedG
   using Cfg = hm::TileCfg<CTAS, NSUB>;
   constexpr int smem = Cfg::kSmemBytes;
   const long ub_tiles = tb.tiles(Cfg::kTileM, Cfg::kTileN);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "smem attr: %s", cudaGetErrorString(e));
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr_set{0};
+  if (int rc = ensure_smem_attr(kern, smem, attr_set, "grouped_gemm")) return rc;
   // Default: one cluster per tile (upper bound `ub_tiles`), scheduled dynamically with cluster
   // launch control. A capacity cap (max_ctas > 0) instead runs a persistent grid of max_ctas
   // CTAs with static tile striding (the per-rank capacity-weight emulation).
@@ -396,12 +408,8 @@ static int launch_router_fused(int groups, cudaStream_t st, const __nv_bfloat16*
                                float* w, int32_t* chunk_base, int32_t* counts, int32_t* offsets) {
   auto kern = hm::router_fused_kernel<EGW, NJ_T, BPW, FUSE>;
   const size_t smem = hm::router_fused_smem_bytes(EGW);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(static_cast<int>(e), "router smem attr: %s", cudaGetErrorString(e));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (int rc = ensure_smem_attr(kern, smem, attr, "router")) return rc;
   const int nj = d / 256;
   const int TG = nj <= 16 ? 4 * (16 / nj) : 4 / BPW;
   const int units = (T + TG - 1) / TG;
@@ -674,11 +682,8 @@ int hm_router_bwd(const void* dx_perm, const int32_t* row_of, const int32_t* idx
     float* partials = coef8 + static_cast<size_t>(T) * 8;
     const int S = router_wgrad_stream_splits(T, d);
     const size_t smem = hm::router_wgrad_stream_smem_bytes();
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(hm::router_wgrad_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if (int rc = ensure_smem_attr(hm::router_wgrad_stream_kernel, smem, attr, "router_wgrad_stream")) return rc;
     hm::router_wgrad_stream_kernel<<<dim3(d / hm::kWgCols, S), hm::kWgThreads, smem, st>>>(
         static_cast<const __nv_bfloat16*>(x), coef8, T, d, E, partials);
     if (int rc = check_launch("router_wgrad_stream")) return rc;

@@ -410,3 +410,30 @@ def test_unpermute_router_bwd_variants_bitwise_equal(cfg):
     for v in ("V2", "V3"):
         for a, b in zip(outs["V1"], outs[v]):
             assert torch.equal(_bits(a), _bits(b)), v
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs two GPUs in one process")
+def test_one_process_two_devices():
+    """The library keeps no per-device state that only the first device gets: the dynamic shared
+    memory opt-ins of the router, the grouped GEMM and the router weight gradient are made on each
+    device's context, so one process can run the layer on cuda:0, then cuda:1, then cuda:0."""
+    from paper_2504_03871_b200.layer import moe_forward
+
+    cfg = LayerConfig("two_dev", E=8, k=2, d=512, f=384, T=700)
+    inp = make_inputs(cfg, seed=11)
+    w_ug = ops.interleave_gate_up(inp.w_gate, inp.w_up)
+    ref = orc.moe_layer(inp.x, inp.wg, w_ug, inp.w_down, cfg.k, dy=inp.dy)
+    for dev in ("cuda:0", "cuda:1", "cuda:0"):
+        with torch.cuda.device(dev):
+            x = inp.x.to(dev).requires_grad_()
+            wg = inp.wg.to(dev).requires_grad_()
+            wug = w_ug.to(dev).requires_grad_()
+            wd = inp.w_down.to(dev).requires_grad_()
+            y, idx = moe_forward(x, wg, wug, wd, cfg.k)
+            y.backward(inp.dy.to(dev))
+            torch.cuda.synchronize()
+        assert np.array_equal(idx.cpu().numpy(), ref["routing"].idx), dev
+        assert orc.rel_err(y, ref["y"]) < TOL_ACT, dev
+        assert orc.rel_err(x.grad, ref["dx"]) < TOL_ACT, dev
+        assert orc.rel_err(wd.grad, ref["dw_down"]) < TOL_W, dev

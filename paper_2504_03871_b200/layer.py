@@ -59,8 +59,9 @@ class _MoEFunction(torch.autograd.Function):
 
 
 def moe_forward(x, wg, w_ug, w_down, k: int, max_ctas: int = 0):
-    """Functional MoE layer: returns (y [T,d], idx [T,k])."""
-    return _MoEFunction.apply(x, wg, w_ug, w_down, k, max_ctas)
+    """Functional MoE layer over token rows x [T,d] (made contiguous if it is a strided view):
+    returns (y [T,d], idx [T,k])."""
+    return _MoEFunction.apply(x.contiguous(), wg, w_ug, w_down, k, max_ctas)
 
 
 class MoELayer(torch.nn.Module):
@@ -87,5 +88,6 @@ class MoELayer(torch.nn.Module):
         return self
 
     def forward(self, x):
-        y, _ = moe_forward(x, self.wg, self.w_ug, self.w_down, self.k, self.max_ctas)
-        return y
+        """x [..., d] (any leading shape, e.g. [batch, seq, d]) -> y of the same shape."""
+        y, _ = moe_forward(x.reshape(-1, self.d), self.wg, self.w_ug, self.w_down, self.k, self.max_ctas)
+        return y.view(x.shape)

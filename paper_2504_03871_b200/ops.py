@@ -83,9 +83,24 @@ def _stream() -> int:
 
 
 def _require_cuda(*ts: torch.Tensor) -> None:
+    dev = None
     for t in ts:
-        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+        if t is None:
+            continue
+        if not t.is_cuda or not t.is_contiguous():
             raise ValueError("hetermoe ops need contiguous CUDA tensors (no CPU fallback)")
+        if dev is None:
+            dev = torch.cuda.current_device()
+        if t.device.index != dev:
+            raise ValueError(f"hetermoe ops run on the current CUDA device (cuda:{dev}); got a tensor "
+                             f"on {t.device} (use torch.cuda.device(...) around the call)")
+
+
+def _require_dtype(**named) -> None:
+    """name=(tensor or None, dtype): the kernels read raw bytes, so a wrong dtype is an error."""
+    for name, (t, dt) in named.items():
+        if t is not None and t.dtype != dt:
+            raise TypeError(f"hetermoe: {name} must be {dt}, got {t.dtype}")
 
 
 @dataclass
@@ -104,6 +119,7 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, bias: torch.Tensor | 
     """K1: fixed-order fp32 logits (+ optional per-expert fp32 bias), top-k (ties -> lower id),
     softmax over the k, per-expert histogram and offsets."""
     _require_cuda(x, wg, bias)
+    _require_dtype(x=(x, torch.bfloat16), wg=(wg, torch.bfloat16), bias=(bias, torch.float32))
     lib = _native.load()
     T, d = x.shape
     E = wg.shape[1]
@@ -129,6 +145,7 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, bias: torch.Tensor | 
 def dispatch_permute(x: torch.Tensor, r: Routing, out: torch.Tensor | None = None):
     """K2: x[T,d] -> (x_perm[T*k,d] grouped by expert, row_src[T*k], row_of[T,k])."""
     _require_cuda(x)
+    _require_dtype(x=(x, torch.bfloat16))
     T, d = x.shape
     k = r.idx.shape[1]
     E = r.counts.shape[0]
@@ -149,6 +166,7 @@ def dispatch_permute(x: torch.Tensor, r: Routing, out: torch.Tensor | None = Non
 
 def unpermute_sum(dx_perm: torch.Tensor, row_of: torch.Tensor) -> torch.Tensor:
     _require_cuda(dx_perm, row_of)
+    _require_dtype(dx_perm=(dx_perm, torch.bfloat16), row_of=(row_of, torch.int32))
     T, k = row_of.shape
     d = dx_perm.shape[1]
     dx = torch.empty((T, d), dtype=dx_perm.dtype, device=dx_perm.device)
@@ -163,6 +181,7 @@ def unpermute_sum(dx_perm: torch.Tensor, row_of: torch.Tensor) -> torch.Tensor:
 def combine(y_perm: torch.Tensor, row_of: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     """K4: y[t] = sum_s w[t,s] * y_perm[row_of[t,s]]."""
     _require_cuda(y_perm, row_of, w)
+    _require_dtype(y_perm=(y_perm, torch.bfloat16), row_of=(row_of, torch.int32), w=(w, torch.float32))
     T, k = row_of.shape
     d = y_perm.shape[1]
     y = torch.empty((T, d), dtype=y_perm.dtype, device=y_perm.device)
@@ -176,6 +195,8 @@ def combine(y_perm: torch.Tensor, row_of: torch.Tensor, w: torch.Tensor) -> torc
 
 def combine_bwd(dy: torch.Tensor, y_perm: torch.Tensor, row_of: torch.Tensor, w: torch.Tensor):
     _require_cuda(dy, y_perm, row_of, w)
+    _require_dtype(dy=(dy, torch.bfloat16), y_perm=(y_perm, torch.bfloat16), row_of=(row_of, torch.int32),
+                   w=(w, torch.float32))
     T, k = row_of.shape
     d = dy.shape[1]
     dy_perm = torch.empty_like(y_perm)
@@ -255,6 +276,8 @@ def grouped_ffn_fwd(x_perm, seg_offsets, w_ug, w_d, max_ctas: int = 0):
     h = x_perm . w_ug[e]^T (gate|up), act = silu(gate)*up, y_perm = act . w_d[e]^T.
     Returns (y_perm, h, act). w_ug [E,2f,d] interleaved, w_d [E,d,f]."""
     _require_cuda(x_perm, seg_offsets, w_ug, w_d)
+    _require_dtype(x_perm=(x_perm, torch.bfloat16), seg_offsets=(seg_offsets, torch.int32),
+                   w_ug=(w_ug, torch.bfloat16), w_d=(w_d, torch.bfloat16))
     rows, d = x_perm.shape
     E, two_f, _ = w_ug.shape
     f = two_f // 2
@@ -273,6 +296,9 @@ def grouped_ffn_bwd(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ctas: i
     """K3 backward: dh = SwiGLU'(dy_perm . w_d[e]); dx_perm = dh . w_ug[e];
     dw_ug[e] = dh_e^T . x_e; dw_d[e] = dy_e^T . act_e. Returns (dx_perm, dw_ug, dw_d)."""
     _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d)
+    _require_dtype(dy_perm=(dy_perm, torch.bfloat16), x_perm=(x_perm, torch.bfloat16), h=(h, torch.bfloat16),
+                   act=(act, torch.bfloat16), seg_offsets=(seg_offsets, torch.int32),
+                   w_ug=(w_ug, torch.bfloat16), w_d=(w_d, torch.bfloat16))
     rows, d = x_perm.shape
     E, two_f, _ = w_ug.shape
     f = two_f // 2
@@ -296,6 +322,9 @@ def grouped_ffn_bwd_data(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d, max_ct
     """Data-gradient half of the FFN backward: dh = SwiGLU'(dy . w_d[e]), dx = dh . w_ug[e].
     Returns (dx_perm, dh); the weight gradients are formed later by grouped_wgrad_multi."""
     _require_cuda(dy_perm, x_perm, h, act, seg_offsets, w_ug, w_d)
+    _require_dtype(dy_perm=(dy_perm, torch.bfloat16), x_perm=(x_perm, torch.bfloat16), h=(h, torch.bfloat16),
+                   act=(act, torch.bfloat16), seg_offsets=(seg_offsets, torch.int32),
+                   w_ug=(w_ug, torch.bfloat16), w_d=(w_d, torch.bfloat16))
     rows, d = x_perm.shape
     E, two_f, _ = w_ug.shape
     f = two_f // 2

@@ -437,3 +437,66 @@ def test_one_process_two_devices():
         assert orc.rel_err(y, ref["y"]) < TOL_ACT, dev
         assert orc.rel_err(x.grad, ref["dx"]) < TOL_ACT, dev
         assert orc.rel_err(wd.grad, ref["dw_down"]) < TOL_W, dev
+
+
+def test_ops_reject_wrong_dtype_and_layout():
+    """The C ABI reads raw bytes: a wrong dtype, a CPU or a non-contiguous tensor is an error at
+    the operator boundary, never a silent reinterpretation (the reference raises ValueError /
+    TypeError for bad inputs the same way)."""
+    cfg = LayerConfig("dtype", E=8, k=2, d=256, f=128, T=64)
+    inp = make_inputs(cfg, seed=3)
+    x, wg = inp.x.cuda(), inp.wg.cuda()
+    with pytest.raises(TypeError):
+        ops.router_topk(x.float(), wg, cfg.k)
+    with pytest.raises(TypeError):
+        ops.router_topk(x, wg.float(), cfg.k)
+    with pytest.raises(ValueError):
+        ops.router_topk(inp.x, wg, cfg.k)
+    with pytest.raises(ValueError):
+        ops.router_topk(x.t().contiguous().t(), wg, cfg.k)
+    r = ops.router_topk(x, wg, cfg.k)
+    xp, _, row_of = ops.dispatch_permute(x, r)
+    with pytest.raises(TypeError):
+        ops.combine(xp, row_of.long(), r.w)
+    with pytest.raises(TypeError):
+        ops.combine(xp, row_of, r.w.bfloat16())
+    with pytest.raises(TypeError):
+        ops.dispatch_permute(x.half(), r)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs two GPUs in one process")
+def test_ops_reject_tensor_on_other_device():
+    cfg = LayerConfig("dev", E=8, k=2, d=256, f=128, T=64)
+    inp = make_inputs(cfg, seed=3)
+    with torch.cuda.device(0):
+        with pytest.raises(ValueError, match="current CUDA device"):
+            ops.router_topk(inp.x.to("cuda:1"), inp.wg.to("cuda:1"), cfg.k)
+
+
+def test_moe_layer_module_batched_input_matches_oracle():
+    """MoELayer (the nn.Module face of the layer) over a [batch, seq, d] input, and moe_forward
+    over a strided view of the token rows, against the oracle."""
+    from paper_2504_03871_b200.layer import MoELayer, moe_forward
+
+    cfg = LayerConfig("module", E=8, k=2, d=512, f=384, T=600)
+    inp = make_inputs(cfg, seed=5)
+    w_ug = ops.interleave_gate_up(inp.w_gate, inp.w_up)
+    ref = orc.moe_layer(inp.x, inp.wg, w_ug, inp.w_down, cfg.k, dy=inp.dy)
+    layer = MoELayer(cfg.d, cfg.f, cfg.E, cfg.k).load(inp.wg.cuda(), inp.w_gate.cuda(), inp.w_up.cuda(),
+                                                      inp.w_down.cuda())
+    x = inp.x.cuda().view(3, 200, cfg.d).requires_grad_()
+    y = layer(x)
+    assert y.shape == x.shape
+    y.backward(inp.dy.cuda().view(3, 200, cfg.d))
+    torch.cuda.synchronize()
+    assert orc.rel_err(y.reshape(cfg.T, cfg.d), ref["y"]) < TOL_ACT
+    assert orc.rel_err(x.grad.reshape(cfg.T, cfg.d), ref["dx"]) < TOL_ACT
+    assert orc.rel_err(layer.wg.grad, ref["dwg"]) < TOL_W
+    assert orc.rel_err(layer.w_down.grad, ref["dw_down"]) < TOL_W
+    # a column-strided view of the token rows is made contiguous at the boundary
+    wide = torch.zeros((cfg.T, 2 * cfg.d), dtype=torch.bfloat16, device="cuda")
+    wide[:, : cfg.d] = inp.x.cuda()
+    y2, idx2 = moe_forward(wide[:, : cfg.d], layer.wg.detach(), layer.w_ug.detach(), layer.w_down.detach(), cfg.k)
+    assert np.array_equal(idx2.cpu().numpy(), ref["routing"].idx)
+    assert torch.equal(y2, y.detach().reshape(cfg.T, cfg.d))

@@ -508,8 +508,10 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200.simulator import compute_metrics, validate_measured_timeline
 
     c = CONFIGS[args.config]
-    M = ws // 2
+    M = args.attention_ranks or ws // 2
     N = ws - M
+    if not 0 < M < ws or (M % N and N % M):
+        raise SystemExit(f"--attention-ranks {M} of {ws}: need 0 < M < {ws} and M | N or N | M")
     dev = torch.device("cuda", local)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     caps = [float(v) for v in str(args.expert_capacity).split(",")]
@@ -938,6 +940,9 @@ def main():
     ap.add_argument("--layers", type=int, default=8, help="ZP (N>1): MoE transformer layers")
     ap.add_argument("--microbatches", type=int, default=8, help="ZP (N>1): micro-batches R")
     ap.add_argument("--mb-tokens", type=int, default=4096, help="ZP (N>1): tokens per micro-batch per attention rank")
+    ap.add_argument("--attention-ranks", type=int, default=0,
+                    help="ZP: attention ranks M (default N/2, e.g. 4 + 4 at 8 GPUs; 6 gives BASELINE C5's "
+                         "6 + 2, 3 the 3 + 1 analogue at 4 GPUs)")
     ap.add_argument("--no-attention", action="store_true", help="ZP: identity attention block")
     ap.add_argument("--attn-gemm-ctas", type=int, default=0,
                     help="ZP: cap the offloaded-expert GEMM grid on attention ranks (SMs left to the comm kernels)")

@@ -130,9 +130,10 @@ def _close(a, b, tol=1e-4):
     (4, 4, (1, 1), False),  # the 8-GPU layout of BASELINE C4 (2 experts per expert rank)
     (4, 4, (2, 0), False),  # a layer whose expert ranks keep no expert at all (all offloaded)
     (2, 2, "distep", False),  # DistEP lockstep ablation on the same executor
+    (6, 2, (3, 0), False),  # the 6 + 2 layout of BASELINE C5 at 8 GPUs (n_2 = 3: 3 of 4 experts move)
 ])
 def test_executor_matches_single_process_reference(M, N, offload, attention):
-    L, R, E, k, T, d, f = 2, 2, (8 if N == 4 else 4), 2, 16, 256, 128
+    L, R, E, k, T, d, f = 2, 2, (8 if M + N == 8 else 4), 2, 16, 256, 128
     args = (L, R, E, k, T, d, f, offload if offload == "distep" else list(offload), attention)
     W = M + N
     ctx = mp.get_context("spawn")

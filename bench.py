@@ -503,7 +503,7 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200.configs import CONFIGS
     from paper_2504_03871_b200.executor import (NativeBackend, ZpExecutor, ZpLayerShape, ZpP2PExecutor,
                                                 execute)
-    from paper_2504_03871_b200.planner import make_zp_spec, plan_assignment
+    from paper_2504_03871_b200.planner import clamp_to_layer_capacity, make_zp_spec, plan_assignment
     from paper_2504_03871_b200.profiler import measure_durations
     from paper_2504_03871_b200.simulator import compute_metrics, validate_measured_timeline
 
@@ -592,6 +592,7 @@ def run_zp(args, ws, rank, local):
     dur = derive_task_durations(spec)
     from paper_2504_03871_b200 import build_distep_graph
 
+    clamped_layers = 0
     if args.schedule == "distep":  # lockstep ablation (no cross-micro-batch overlap, no offload)
         graph = build_distep_graph(spec, dur)
         assignment = graph.assignment
@@ -603,6 +604,7 @@ def run_zp(args, ws, rank, local):
             assignment = ExpertAssignment(tuple(int(v) for v in args.offload.split(",")))
         else:
             assignment = plan_assignment(spec, dur)
+            assignment, clamped_layers = clamp_to_layer_capacity(assignment, c.E, M, N)
         graph = build_zp_graph(spec, dur, assignment, mode="zp-full")
     disp = dist.new_group(list(range(ws)))
     comb = dist.new_group(list(range(ws)))
@@ -672,6 +674,7 @@ def run_zp(args, ws, rank, local):
             "microbatches": args.microbatches, "tokens_per_microbatch": args.mb_tokens,
             "attention_block": not args.no_attention, "parallelism": f"zp{M}+{N}",
             "asym_ea_offload": list(assignment.offload),
+            "asym_ea_layers_clamped_to_n_over_N": clamped_layers,
             "transport": args.transport, "schedule": args.schedule, "expert_capacity": caps,
             "comm_stream_priority": "high" if args.comm_priority else "default",
             "attention_rank_gemm_ctas": args.attn_gemm_ctas or sms,

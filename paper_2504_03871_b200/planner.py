@@ -58,6 +58,19 @@ def plan_assignment(spec: Spec, durations: TaskDurations) -> ExpertAssignment:
     return ExpertAssignment.zeros(spec.model.layers)
 
 
+def clamp_to_layer_capacity(assignment: ExpertAssignment, experts: int, M: int, N: int):
+    """Algorithm 1 (``scheduler.asym_ea_offload``, reference ``scheduler.py:264-283``) bounds the
+    offload summed over layers (alpha / n_max) but not per layer: with a large bubble (e.g. 3
+    attention + 1 expert GPU) it can ask one layer for more experts than an expert GPU holds, which
+    ``build_zp_graph`` then rejects (offload outside [0, n/N], reference ``taskgraph.py:178-194``).
+    This clamps each layer to the largest whole number of n_2-chunks that fits in n/N and returns
+    (assignment, layers clamped). The planner's parity path does not call it; the B200 bench does."""
+    _, n2 = scheduler.chunk_sizes(M, N)
+    cap = (experts // N) // n2 * n2
+    out = tuple(min(o, cap) for o in assignment.offload)
+    return ExpertAssignment(out), sum(1 for a, b in zip(assignment.offload, out) if a != b)
+
+
 def make_zp_spec(M: int, N: int, layers: int, microbatches: int, experts: int, top_k: int,
                  tokens_per_mb: int, hidden: int, attn_fwd_ns: int, expert_layer_fwd_ns: int,
                  single_expert_fwd_ns: int, dispatch_ns: int = 0, combine_ns: int = 0,

@@ -246,3 +246,17 @@ def test_costmodel_known_answers():
     assert memory_bounds(spec(M=2, N=4, n=8, L=2, expert_mem=100, attn_cap=600, exp_cap=10**9)).n_max == 3
     with pytest.raises(InfeasibleError):
         memory_bounds(spec(L=4, n=24, N=6, M=6, expert_mem=100, exp_cap=1200, attn_cap=99))
+
+
+def test_clamp_to_layer_capacity():
+    """Algorithm 1 bounds the offload over all layers, not per layer; the bench clamps each layer
+    to whole n_2-chunks within n/N so build_zp_graph accepts the plan (3 + 1: n_2 = 3, n/N = 8)."""
+    from paper_2504_03871_b200 import ExpertAssignment
+    from paper_2504_03871_b200.planner import clamp_to_layer_capacity
+
+    a, k = clamp_to_layer_capacity(ExpertAssignment((9, 3, 0, 12)), 8, 3, 1)
+    assert a.offload == (6, 3, 0, 6) and k == 2
+    a, k = clamp_to_layer_capacity(ExpertAssignment((1, 2, 0)), 8, 4, 4)
+    assert a.offload == (1, 2, 0) and k == 0
+    a, k = clamp_to_layer_capacity(ExpertAssignment((3, 6)), 8, 6, 2)  # n_2 = 3, n/N = 4
+    assert a.offload == (3, 3) and k == 1

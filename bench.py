@@ -731,7 +731,8 @@ def run_zp(args, ws, rank, local):
         if args.schedule == "distep":
             g_ = build_distep_graph(spec, dur)
         else:
-            g_ = build_zp_graph(spec, dur, plan_assignment(spec, dur), mode="zp-full")
+            a_ = plan_assignment(spec, dur) if not args.offload else assignment
+            g_ = build_zp_graph(spec, dur, clamp_to_layer_capacity(a_, c.E, M, N)[0], mode="zp-full")
         simulate(g_, default_orders(g_))
     out["zp"]["planning_ms"] = round((time.perf_counter() - tp0) / reps * 1e3, 3)
     out["zp"]["planning_tasks"] = len(graph.tasks)

@@ -214,21 +214,25 @@ int launch_kind(int mode, const CUtensorMap& ma, const CUtensorMap& mb, const hm
   return launch_gemm<GROUP_K, A_MN, B_MN, EPI, 2, 1, SHIFT>(ma, mb, p, tb, max_ctas, st);
 }
 
-// raster group height per GEMM mode (HM_GEMM_GROUPM = one value for every mode). The per-mode
-// defaults minimise DRAM traffic at equal time (C2 sweep of 8/16/32/64, profiles/r2_gemm_groupm.md):
-// up+gate 32 (5.6 -> 3.6 GB read), SwiGLU backward 64; the weight gradients 32 when the output
-// has at most 32 row tiles (dW_d, M = d: 2.4 -> 1.6 GB) and 8 otherwise (dW_ug, M = 2f: 4.2 GB
-// at 8, 7.3 at 32); the others keep 8 (dX: 8.9 GB at 8, 10.4 at 16).
+// raster group height per GEMM mode (HM_GEMM_GROUPM = one value for every mode; a negative value
+// -g selects the transposed raster: groups of g n-tiles, n fastest). The per-mode defaults
+// minimise DRAM traffic at equal time (C2 sweeps of 8/16/32/64 and -2/-4/-8/-16,
+// profiles/r2_gemm_groupm.md): up+gate 32 (5.6 -> 3.6 GB read), SwiGLU backward 64, down and dX
+// transposed in groups of 4 n-tiles (dX 8.2 -> 7.6 GB); the bf16 weight gradients 32 when the
+// output has at most 32 row tiles (dW_d, M = d: 2.4 -> 1.6 GB), else transposed in groups of 8
+// (dW_ug, M = 2f: 4.2 -> 2.7 GB); the fp32-accumulating multi-segment weight gradient of the ZP
+// executor keeps 32 / 8.
 int g_group_m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 int gemm_group_m(int mode, long M = 0) {
-  static const int kDefault[8] = {32, 8, 64, 8, 0, 0, 8, 8};  // by HM_GEMM_* mode; 0 = by M
+  static const int kDefault[8] = {32, -4, 64, -4, 0, 0, 8, 8};  // by HM_GEMM_* mode; 0 = by M
   if (mode < 0 || mode >= 8) return hm::kGroupM;
-  if (g_group_m[mode] <= 0) {
+  if (g_group_m[mode] == 0) {
     const char* s = getenv("HM_GEMM_GROUPM");
     const int v = s ? atoi(s) : 0;
-    if (v > 0) g_group_m[mode] = v;
-    else if (kDefault[mode] > 0) g_group_m[mode] = kDefault[mode];
-    else return (M + 255) / 256 <= 32 ? 32 : 8;
+    if (v != 0) g_group_m[mode] = v;
+    else if (kDefault[mode] != 0) g_group_m[mode] = kDefault[mode];
+    else if ((M + 255) / 256 <= 32) return 32;
+    else return mode == HM_GEMM_WGRAD ? -8 : 8;
   }
   return g_group_m[mode];
 }
@@ -356,7 +360,8 @@ int hm_debug_set_gemm_wide(int mask) {
   return old;
 }
 // tuning aid (not part of the ABI): raster group height of one GEMM mode (mode < 0: all modes;
-// value <= 0: back to the default); returns the previous value of `mode` (or of mode 0)
+// value == 0: back to the default; value < 0: the transposed raster, -value n-tiles per group);
+// returns the previous value of `mode` (or of mode 0)
 int hm_debug_set_gemm_groupm(int mode, int value) {
   const int old = gemm_group_m(mode < 0 ? 0 : mode, 0);
   for (int m = 0; m < 8; ++m)

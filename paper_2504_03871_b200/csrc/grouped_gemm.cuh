@@ -82,7 +82,8 @@ struct GroupedGemmParams {
   int ldo2;
   const __nv_bfloat16* aux;  // SWIGLU_BWD: h saved by the forward [rows, 2N]
   int ld_aux;
-  int group_m;    // raster: m-tiles per group (m fastest inside a group, then n, then next group)
+  int group_m;    // raster: m-tiles per group (m fastest inside a group, then n, then next group);
+                  // < 0: -group_m n-tiles per group, n fastest
   union {  // (keeps the parameter block at 128 bytes: a larger one is read through a generic
            // pointer, which cost the SwiGLU-backward epilogue 20 %)
     const CUtensorMap* expert_maps;  // GROUP_K: per-(expert, segment) TMA views, [(e*R+j)*2] = A, +1 = B
@@ -247,6 +248,16 @@ HM_DEV TileCoord decode_tile(const GemmShared& sh, int E, int tile, int mtiles_f
   // grouped raster: groups of group_m m-tiles, m fastest inside a group, then n, then the
   // next group. With group_m = 8 the ~74 concurrently running tiles form an ~8 x 9 block, so
   // every A and B panel they stream is shared by ~8 concurrent tiles (L2 reuse along long K).
+  // group_m < 0: the transposed raster, groups of -group_m n-tiles, n fastest inside a group
+  if (group_m < 0) {
+    const int gnmax = -group_m;
+    const int group = local / (gnmax * mtiles);
+    const int rem = local - group * gnmax * mtiles;
+    const int gn = min(gnmax, ntiles - group * gnmax);
+    c.nt = group * gnmax + rem % gn;
+    c.mt = rem / gn;
+    return c;
+  }
   const int gmax = group_m;
   const int group = local / (gmax * ntiles);
   const int rem = local - group * gmax * ntiles;

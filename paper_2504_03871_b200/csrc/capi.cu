@@ -331,6 +331,13 @@ int hm_debug_expert_maps(const void* a, const void* b, const int32_t* seg_offset
   return 0;
 }
 
+// debugging aid (not part of the ABI): the fused router's per-CTA phase stamps of the last
+// launch (HM_ROUTER_TIMELINE builds only; zeros otherwise), 512 x 5 u64 into out
+int hm_debug_router_timeline(unsigned long long* out) {
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(out, hm::g_router_tl, sizeof(hm::g_router_tl));
+  return static_cast<int>(e);
+}
 // debugging aid (not part of the ABI): first out-of-range access recorded by an
 // HM_BOUNDS_CHECK build of the grouped GEMM; reads and clears the record
 int hm_debug_read(long long* out8) {

@@ -201,6 +201,22 @@ HM_DEV void router_scan_block(int32_t* __restrict__ chunk_counts /*in: counts, o
   }
 }
 
+// HM_ROUTER_TIMELINE builds: per-CTA globaltimer stamps (ns) of the fused router's phases,
+// [cta][0] entry, [1] weights in registers (after the first CTA barrier), [2] last compute stage
+// done (compute warp 0), [3] last epilogue stage done (epilogue warp 16), [4] CTA exit; [511][0..1]
+// the last CTA's scan begin / end. Read by hm_debug_router_timeline (tools/router_timeline.py).
+__device__ unsigned long long g_router_tl[512][5];
+HM_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef HM_ROUTER_TIMELINE
+#define HM_RT_STAMP(i) g_router_tl[blockIdx.x][i] = globaltimer_ns()
+#else
+#define HM_RT_STAMP(i) do { } while (0)
+#endif
+
 struct RouterShared {
   uint64_t full[kRouterStages];
   uint64_t pfull[kRouterStages];
@@ -266,6 +282,9 @@ HM_DEV void router_select_lanes(float v, int e, int E, int k, bool write, int32_
 //   nj > 16:  BPW = ceil(nj / 16) blocks per warp (w + 16 b), every token of a TG = 4 / BPW stage.
 // FUSE: one expert group (E <= EGW): top-k, softmax, the per-chunk histogram (atomics into the
 // zeroed chunk_counts) and, in the last CTA, the scan.
+// the epilogue warp that handles the CTA's last stage (stage nst - 1 goes to warp (nst-1) % 4)
+HM_DEV bool s_last_epi(int nst, int epi) { return nst > 0 && (nst - 1) % kRouterEpiWarps == epi; }
+
 template <int EGW, int NJ_T, int BPW, bool FUSE>
 __global__ void __launch_bounds__(kRouterThreads, 1)
     router_fused_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
@@ -295,6 +314,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   const int nst = t_end > t_begin ? (t_end - t_begin + TG - 1) / TG : 0;
 
   if (threadIdx.x == 0) {
+    HM_RT_STAMP(0);
     for (int s = 0; s < kRouterStages; ++s) {
       mbar_init(&sh.full[s], 1);
       mbar_init(&sh.pfull[s], kRouterWarps);
@@ -360,6 +380,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   // a lane's expert in the epilogue is lane % EGW in every round (32 % EGW == 0)
   const float bias_lane = (bias && e0 + lane % EGW < E) ? bias[e0 + lane % EGW] : 0.f;
   __syncthreads();
+  if (threadIdx.x == 0) HM_RT_STAMP(1);
 
   if (warp < kRouterWarps) {
     // ============ compute warps ============
@@ -407,6 +428,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.pfull[slot]);  // releases this warp's ring reads and table writes
     }
+    if (threadIdx.x == 0) HM_RT_STAMP(2);
   } else {
     // ============ epilogue warps: stage s is warp 16 + s % 4's; it refills ring slot s % 4 ============
     for (int s = warp - kRouterWarps; s < nst; s += kRouterEpiWarps) {
@@ -451,6 +473,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.pempty[slot]);
     }
+    if (lane == 0 && s_last_epi(nst, warp - kRouterWarps)) HM_RT_STAMP(3);
   }
   if (FUSE) {
     // the last CTA to finish turns the per-chunk counts into totals, offsets and chunk bases
@@ -464,10 +487,18 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     __syncthreads();
     if (sh.is_last) {
       __threadfence();
+#ifdef HM_ROUTER_TIMELINE
+      if (threadIdx.x == 0) g_router_tl[511][0] = globaltimer_ns();
+#endif
       const int nchunk = (T + kChunk - 1) / kChunk;
       router_scan_block(chunk_counts, nchunk, E, counts, offsets, reinterpret_cast<int*>(ring), sh.scan_off);
+#ifdef HM_ROUTER_TIMELINE
+      __syncthreads();
+      if (threadIdx.x == 0) g_router_tl[511][1] = globaltimer_ns();
+#endif
     }
   }
+  if (threadIdx.x == 0) HM_RT_STAMP(4);
 }
 
 constexpr size_t router_fused_smem_bytes(int egw) {

@@ -873,6 +873,7 @@ int hm_grouped_gemm_shifted(int mode, const void* a, const void* b, const int32_
                             void* out2, int ldo2, const void* aux, int ld_aux, void* workspace,
                             const unsigned long long* out_rows, const int32_t* row_shift,
                             int max_ctas, void* stream) {
+  if (mode < HM_GEMM_FWD_UPGATE || mode > HM_GEMM_WGRAD_ACC) return fail(HM_E_ARG, "gemm: unknown mode %d", mode);
   if (E < 1 || E > hm::kMaxExperts) return fail(HM_E_SHAPE, "gemm: E=%d out of range", E);
   if (rows < 0 || N <= 0 || N % 8 != 0) return fail(HM_E_SHAPE, "gemm: bad rows/N");
   if (!aligned16(a) || !aligned16(b) || (!out_rows && !aligned16(out))) return fail(HM_E_ALIGN, "gemm: alignment");

@@ -500,3 +500,36 @@ def test_moe_layer_module_batched_input_matches_oracle():
     y2, idx2 = moe_forward(wide[:, : cfg.d], layer.wg.detach(), layer.w_ug.detach(), layer.w_down.detach(), cfg.k)
     assert np.array_equal(idx2.cpu().numpy(), ref["routing"].idx)
     assert torch.equal(y2, y.detach().reshape(cfg.T, cfg.d))
+
+
+@pytest.mark.parametrize("groupm", [1, 3, -1, -3, -8], ids=lambda g: f"groupm{g}")
+def test_grouped_ffn_any_raster_is_bitwise_equal(groupm):
+    """The raster (tile order) only changes which CTA computes a tile, never its arithmetic: every
+    row-grouped (g > 0) and transposed (g < 0) raster gives the default's bits, on ragged experts
+    with several m- and n-tiles per expert."""
+    from paper_2504_03871_b200 import _native
+
+    lib = _native.load()
+    segs = [700, 0, 513, 1, 256, 300]
+    d, f = 1024, 640  # 2 wide n-tiles for the d-wide GEMMs, 3 for the 2f-wide up+gate
+    E, rows = len(segs), sum(segs)
+    g = torch.Generator().manual_seed(5)
+    bf = lambda *s, std=1.0: (torch.randn(s, generator=g) * std).to(torch.bfloat16).cuda()  # noqa: E731
+    x_perm, dy = bf(rows, d), bf(rows, d)
+    w_ug, w_d = bf(E, 2 * f, d, std=d ** -0.5), bf(E, d, f, std=f ** -0.5)
+    seg = torch.from_numpy(_ragged_offsets(segs)).cuda()
+
+    def run():
+        y, h, act = ops.grouped_ffn_fwd(x_perm, seg, w_ug, w_d)
+        dx, dw_ug, dw_d = ops.grouped_ffn_bwd(dy, x_perm, h, act, seg, w_ug, w_d)
+        torch.cuda.synchronize()
+        return [t.clone() for t in (y, h, act, dx, dw_ug, dw_d)]
+
+    ref = run()
+    lib.hm_debug_set_gemm_groupm(-1, groupm)
+    try:
+        got = run()
+    finally:
+        lib.hm_debug_set_gemm_groupm(-1, 0)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)

@@ -24,7 +24,7 @@ from . import _native
 BLOCK_F = 128  # gate/up interleave block of the fused W_ug layout
 
 # number of native kernel launches issued through this module (bench.py's gpu_launches);
-# the executor issues from one thread per stream, hence the lock
+# (a lock, in case several host threads issue native ops)
 LAUNCHES = [0]
 _LAUNCH_LOCK = threading.Lock()
 

@@ -759,24 +759,37 @@ __global__ void __launch_bounds__(256)
       rows[s] = row_of[static_cast<long>(t) * K + s];
       ws[s] = w[static_cast<long>(t) * K + s];
     }
-    for (int q = lane; q < nv; q += 32) {
-      float acc[8];
+    // CU column segments per lane in flight before any is consumed (memory-level parallelism:
+    // one segment per row at a time left the C2 combine at ~74 % of HBM)
+    constexpr int CU = K <= 2 ? 4 : (K <= 4 ? 2 : 1);
+    for (int q0 = lane; q0 < nv; q0 += 32 * CU) {
+      uint4 v[CU][K];
 #pragma unroll
-      for (int z = 0; z < 8; ++z) acc[z] = 0.f;
-      uint4 v[kMaxTopK];
-      for (int s = 0; s < K; ++s)
-        v[s] = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q);
-      for (int s = 0; s < K; ++s) {
-        const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[s]);
+      for (int u = 0; u < CU; ++u)
 #pragma unroll
-        for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(ws[s], bf16_to_f32(h[z]), acc[z]);
+        for (int s = 0; s < K; ++s)
+          if (q0 + 32 * u < nv)
+            v[u][s] = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q0 + 32 * u);
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int q = q0 + 32 * u;
+        if (q >= nv) break;
+        float acc[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+          const uint16_t* h = reinterpret_cast<const uint16_t*>(&v[u][s]);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) acc[z] = __fmaf_rn(ws[s], bf16_to_f32(h[z]), acc[z]);
+        }
+        uint4 o;
+        o.x = pack_bf16x2(acc[0], acc[1]);
+        o.y = pack_bf16x2(acc[2], acc[3]);
+        o.z = pack_bf16x2(acc[4], acc[5]);
+        o.w = pack_bf16x2(acc[6], acc[7]);
+        reinterpret_cast<uint4*>(y + static_cast<long>(t) * d)[q] = o;
       }
-      uint4 o;
-      o.x = pack_bf16x2(acc[0], acc[1]);
-      o.y = pack_bf16x2(acc[2], acc[3]);
-      o.z = pack_bf16x2(acc[4], acc[5]);
-      o.w = pack_bf16x2(acc[6], acc[7]);
-      reinterpret_cast<uint4*>(y + static_cast<long>(t) * d)[q] = o;
     }
   }
 }

@@ -811,23 +811,42 @@ __global__ void __launch_bounds__(256)
       ws[s] = w[static_cast<long>(t) * K + s];
       dot[s] = 0.f;
     }
-    for (int q = lane; q < nv; q += 32) {
-      const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy + static_cast<long>(t) * d) + q);
-      const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g);
-      float gf[8];
+    // CU column segments per lane loaded before any is consumed (memory-level parallelism); the
+    // segments are then consumed in column order, so dw keeps its summation order
+#ifndef HM_COMBINE_BWD_CU
+#define HM_COMBINE_BWD_CU 4
+#endif
+    constexpr int CU = K <= 2 ? HM_COMBINE_BWD_CU : 1;
+    for (int q0 = lane; q0 < nv; q0 += 32 * CU) {
+      uint4 g[CU], yv[CU][K];
 #pragma unroll
-      for (int z = 0; z < 8; ++z) gf[z] = bf16_to_f32(gh[z]);
-      for (int s = 0; s < K; ++s) {
-        const uint4 yv = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q);
-        const uint16_t* yh = reinterpret_cast<const uint16_t*>(&yv);
+      for (int u = 0; u < CU; ++u)
+        if (q0 + 32 * u < nv) {
+          g[u] = __ldg(reinterpret_cast<const uint4*>(dy + static_cast<long>(t) * d) + q0 + 32 * u);
 #pragma unroll
-        for (int z = 0; z < 8; ++z) dot[s] = __fmaf_rn(gf[z], bf16_to_f32(yh[z]), dot[s]);
-        uint4 o;
-        o.x = pack_bf16x2(ws[s] * gf[0], ws[s] * gf[1]);
-        o.y = pack_bf16x2(ws[s] * gf[2], ws[s] * gf[3]);
-        o.z = pack_bf16x2(ws[s] * gf[4], ws[s] * gf[5]);
-        o.w = pack_bf16x2(ws[s] * gf[6], ws[s] * gf[7]);
-        reinterpret_cast<uint4*>(dy_perm + static_cast<long>(rows[s]) * d)[q] = o;
+          for (int s = 0; s < K; ++s)
+            yv[u][s] = __ldg(reinterpret_cast<const uint4*>(y_perm + static_cast<long>(rows[s]) * d) + q0 + 32 * u);
+        }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int q = q0 + 32 * u;
+        if (q >= nv) break;
+        const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g[u]);
+        float gf[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) gf[z] = bf16_to_f32(gh[z]);
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+          const uint16_t* yh = reinterpret_cast<const uint16_t*>(&yv[u][s]);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) dot[s] = __fmaf_rn(gf[z], bf16_to_f32(yh[z]), dot[s]);
+          uint4 o;
+          o.x = pack_bf16x2(ws[s] * gf[0], ws[s] * gf[1]);
+          o.y = pack_bf16x2(ws[s] * gf[2], ws[s] * gf[3]);
+          o.z = pack_bf16x2(ws[s] * gf[4], ws[s] * gf[5]);
+          o.w = pack_bf16x2(ws[s] * gf[6], ws[s] * gf[7]);
+          reinterpret_cast<uint4*>(dy_perm + static_cast<long>(rows[s]) * d)[q] = o;
+        }
       }
     }
     for (int s = 0; s < K; ++s) {
@@ -876,27 +895,46 @@ __global__ void __launch_bounds__(256, 4)
       for (int s = 0; s < K; ++s) c = (ex[s] == lane) ? dl[s] : c;
       coef8[static_cast<long>(t) * 8 + lane] = c;
     }
-    for (int q = lane; q < nv; q += 32) {
-      float acc[8];
+    // CU column segments per lane loaded before any is consumed (memory-level parallelism)
+#ifndef HM_UNPERMUTE_CU
+#define HM_UNPERMUTE_CU 2
+#endif
+    constexpr int CU = K <= 2 ? HM_UNPERMUTE_CU : 1;
+    for (int q0 = lane; q0 < nv; q0 += 32 * CU) {
+      uint4 v[CU][K], g[CU][K];
 #pragma unroll
-      for (int z = 0; z < 8; ++z) acc[z] = 0.f;
-      for (int s = 0; s < K; ++s) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(dx_perm + static_cast<long>(rows[s]) * d) + q);
-        const uint4 g = __ldg(reinterpret_cast<const uint4*>(wg_t + static_cast<long>(ex[s]) * d) + q);
-        const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v);
-        const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g);
+      for (int u = 0; u < CU; ++u)
+        if (q0 + 32 * u < nv) {
 #pragma unroll
-        for (int z = 0; z < 8; ++z) {
-          acc[z] += bf16_to_f32(vh[z]);
-          acc[z] = __fmaf_rn(dl[s], bf16_to_f32(gh[z]), acc[z]);
+          for (int s = 0; s < K; ++s) {
+            v[u][s] = __ldg(reinterpret_cast<const uint4*>(dx_perm + static_cast<long>(rows[s]) * d) + q0 + 32 * u);
+            g[u][s] = __ldg(reinterpret_cast<const uint4*>(wg_t + static_cast<long>(ex[s]) * d) + q0 + 32 * u);
+          }
         }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const int q = q0 + 32 * u;
+        if (q >= nv) break;
+        float acc[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z) acc[z] = 0.f;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+          const uint16_t* vh = reinterpret_cast<const uint16_t*>(&v[u][s]);
+          const uint16_t* gh = reinterpret_cast<const uint16_t*>(&g[u][s]);
+#pragma unroll
+          for (int z = 0; z < 8; ++z) {
+            acc[z] += bf16_to_f32(vh[z]);
+            acc[z] = __fmaf_rn(dl[s], bf16_to_f32(gh[z]), acc[z]);
+          }
+        }
+        uint4 o;
+        o.x = pack_bf16x2(acc[0], acc[1]);
+        o.y = pack_bf16x2(acc[2], acc[3]);
+        o.z = pack_bf16x2(acc[4], acc[5]);
+        o.w = pack_bf16x2(acc[6], acc[7]);
+        reinterpret_cast<uint4*>(dx + static_cast<long>(t) * d)[q] = o;
       }
-      uint4 o;
-      o.x = pack_bf16x2(acc[0], acc[1]);
-      o.y = pack_bf16x2(acc[2], acc[3]);
-      o.z = pack_bf16x2(acc[4], acc[5]);
-      o.w = pack_bf16x2(acc[6], acc[7]);
-      reinterpret_cast<uint4*>(dx + static_cast<long>(t) * d)[q] = o;
     }
   }
 }

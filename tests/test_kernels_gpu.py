@@ -533,3 +533,28 @@ def test_grouped_ffn_any_raster_is_bitwise_equal(groupm):
         lib.hm_debug_set_gemm_groupm(-1, 0)
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 6])
+@pytest.mark.parametrize("d", [296, 1032])
+def test_combine_any_width_vs_fp32(k, d):
+    """K4 on widths that are not a multiple of 256 (nv = d / 8 column segments not a multiple of
+    32 lanes, so the last group of in-flight segments is partial) against an fp32 reference."""
+    T = 333
+    g = torch.Generator().manual_seed(9)
+    row_of = torch.randperm(T * k, generator=g).to(torch.int32).reshape(T, k)
+    w = torch.softmax(torch.randn((T, k), generator=g), 1)
+    y_perm = torch.randn((T * k, d), generator=g).to(torch.bfloat16)
+    dy = torch.randn((T, d), generator=g).to(torch.bfloat16)
+    y = ops.combine(y_perm.cuda(), row_of.cuda(), w.cuda())
+    dy_perm, dw = ops.combine_bwd(dy.cuda(), y_perm.cuda(), row_of.cuda(), w.cuda())
+    torch.cuda.synchronize()
+    ro = row_of.long()
+    yp = y_perm.float()
+    y_ref = (yp[ro.reshape(-1)].reshape(T, k, -1) * w[:, :, None]).sum(1)
+    assert orc.rel_err(y, y_ref) < TOL_ACT
+    dyp_ref = torch.zeros_like(yp)
+    dyp_ref[ro.reshape(-1)] = (w[:, :, None] * dy.float()[:, None, :]).reshape(-1, d)
+    assert orc.rel_err(dy_perm, dyp_ref) < TOL_ACT
+    dw_ref = (yp[ro.reshape(-1)].reshape(T, k, -1) * dy.float()[:, None, :]).sum(-1)
+    assert orc.rel_err(dw, dw_ref) < 1e-4

@@ -598,6 +598,7 @@ def run_zp(args, ws, rank, local):
     from paper_2504_03871_b200 import build_distep_graph
 
     clamped_layers = 0
+    calibration = None
     if args.schedule == "distep":  # lockstep ablation (no cross-micro-batch overlap, no offload)
         graph = build_distep_graph(spec, dur)
         assignment = graph.assignment
@@ -610,6 +611,33 @@ def run_zp(args, ws, rank, local):
         else:
             assignment = plan_assignment(spec, dur)
             assignment, clamped_layers = clamp_to_layer_capacity(assignment, c.E, M, N)
+            if args.calibrate and not args.no_asym_ea:
+                # re-plan from durations measured inside a short pipeline run of this plan's
+                # offloads (profiler.calibrate_in_pipeline): sustained clocks, real loads under skew
+                from paper_2504_03871_b200.profiler import calibrate_in_pipeline
+
+                offs = list(assignment.offload)
+                cal_off = (min(offs), max(offs))
+                cal = calibrate_in_pipeline(
+                    shape, M, N, NativeBackend(dev, max_ctas=exp_ctas if rank >= M else args.attn_gemm_ctas),
+                    cal_off, args.transport, *disp_groups, microbatches=args.microbatches,
+                    expert_loads=loads, expert_capacity=caps if hetero else None, base=durs)
+                keys = ("attn_fwd_ns", "expert_layer_fwd_ns", "single_expert_fwd_ns", "gamma_x100")
+                ct = torch.tensor([cal[k_] for k_ in keys], dtype=torch.int64, device=dev)
+                dist.broadcast(ct, 0)
+                cal = dict(zip(keys, (int(v) for v in ct.tolist())))
+                durs_cal = dict(durs, **cal)
+                plan_cal = {k_: v for k_, v in durs_cal.items() if k_ in PLANNER_DURATION_KEYS}
+                spec = make_zp_spec(M, N, args.layers, args.microbatches, c.E, c.k, args.mb_tokens, c.d,
+                                    asym_ea=True, gamma=Fraction(durs_cal["gamma_x100"], 100),
+                                    **plan_cal, **mem_fields)
+                bounds = memory_bounds(spec)
+                dur = derive_task_durations(spec)
+                first = list(assignment.offload)
+                assignment, clamped_layers = clamp_to_layer_capacity(plan_assignment(spec, dur), c.E, M, N)
+                calibration = {"calibration_offload": list(cal_off), "durations_ns": cal,
+                               "profiled_ns": {k_: durs[k_] for k_ in keys}, "offload_before": first,
+                               "offload_after": list(assignment.offload)}
         graph = build_zp_graph(spec, dur, assignment, mode="zp-full")
     disp = dist.new_group(list(range(ws)))
     comb = dist.new_group(list(range(ws)))
@@ -741,6 +769,8 @@ def run_zp(args, ws, rank, local):
         simulate(g_, default_orders(g_))
     out["zp"]["planning_ms"] = round((time.perf_counter() - tp0) / reps * 1e3, 3)
     out["zp"]["planning_tasks"] = len(graph.tasks)
+    if calibration is not None:
+        out["zp"]["calibration"] = calibration
     # the same schedule replayed with each compute task at its measured duration (slowest rank
     # of its role): what the executor would reach with no issue stalls (communication tasks
     # keep their planned time)
@@ -959,6 +989,8 @@ def main():
     ap.add_argument("--raw-attention-duration", action="store_true",
                     help="ZP: plan with the attention forward as measured (no fwd+bwd role normalisation)")
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
+    ap.add_argument("--calibrate", action="store_true",
+                    help="ZP: re-plan Asym-EA from durations measured inside a short pipeline run")
     ap.add_argument("--router-skew", type=float, default=0.0,
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
     ap.add_argument("--no-balanced-placement", action="store_true",

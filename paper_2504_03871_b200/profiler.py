@@ -22,6 +22,8 @@ spec's ``expert_mem`` / ``memory_capacity`` / ``non_expert_mem_*`` fields.
 
 from __future__ import annotations
 
+from typing import Optional
+
 import torch
 
 NVLINK_GBS = 770.0  # peer copy bandwidth per direction (B200_PROFILING.md); fallback only
@@ -340,3 +342,72 @@ def measure_transport(shape, M: int, N: int, backend, transport: str = "p2p", di
     del ex
     torch.cuda.empty_cache()
     return {"dispatch_ns": out["DispF"], "combine_ns": out["CombF"]}
+
+
+def calibrate_in_pipeline(shape, M: int, N: int, backend, offload, transport: str = "p2p",
+                          disp_group=None, comb_group=None, microbatches: int = 8, reps: int = 2,
+                          expert_loads=None, expert_capacity=None, base: Optional[dict] = None,
+                          seed: int = 13) -> dict:
+    """Planner durations measured INSIDE the pipeline (collective: every rank calls it).
+
+    The isolated probes of ``measure_durations`` run at burst clocks and without the exchange
+    kernels beside them; in the pipeline every task runs at sustained-power clocks, and under a
+    skewed router the busiest expert rank and the offloaded experts carry other loads than one
+    routed micro-batch suggests. This runs a ``len(offload)``-layer ZP graph with the given
+    per-layer offloads and ``microbatches`` micro-batches through the real executor and inverts the
+    reference's duration model (``taskgraph.py:253-263``: ExpF = T_exp·(1 − o·N/n),
+    OffExpF = T_single·o·N²/(n·M), backward = γ × forward) on the measured tasks, each task's
+    duration taken as the max over its role's ranks and averaged over micro-batches and layers.
+    Returns the planner's duration keys (``attn_fwd_ns`` normalised to (fwd + bwd) / (1 + γ) as in
+    ``measure_durations``); ``single_expert_fwd_ns`` falls back to ``base`` scaled by the measured /
+    profiled expert-layer ratio when no calibration layer offloads."""
+    import torch.distributed as dist
+
+    from .core import ExpertAssignment
+    from .costmodel import derive_task_durations
+    from .executor import ZpExecutor, ZpP2PExecutor, execute
+    from .planner import make_zp_spec
+    from .taskgraph import TaskKind, build_zp_graph
+
+    L = len(offload)
+    n = shape.E
+    spec = make_zp_spec(M, N, L, microbatches, shape.E, shape.k, shape.tokens_per_mb, shape.d,
+                        attn_fwd_ns=1000, expert_layer_fwd_ns=1000, single_expert_fwd_ns=1000,
+                        dispatch_ns=100, combine_ns=100)
+    graph = build_zp_graph(spec, derive_task_durations(spec), ExpertAssignment(tuple(offload)), mode="zp-full")
+    cls = ZpP2PExecutor if transport == "p2p" else ZpExecutor
+    ex = cls(graph, shape, M, N, dist.get_rank(), backend, disp_group, comb_group, seed=seed,
+             expert_loads=expert_loads, expert_capacity=expert_capacity)
+    ex.run()
+    ex.run()  # warm-up: sustained clocks before the measured iterations
+    acc = {}
+    for _ in range(reps):
+        tl = execute(graph, ex)
+        for t in graph.tasks:
+            role = range(0, M) if t.device == "attn" else range(M, M + N)
+            ds = [tl.per_rank[r][t.id][1] - tl.per_rank[r][t.id][0] for r in role if t.id in tl.per_rank[r]]
+            if ds:
+                acc.setdefault((t.kind, t.layer), []).append(max(ds))
+    del ex
+    torch.cuda.empty_cache()
+    mean = lambda v: sum(v) / len(v)  # noqa: E731
+    kind = lambda kd: [mean(v) for (k_, l_), v in acc.items() if k_ == kd]  # noqa: E731
+    attn_f, attn_b = mean(kind(TaskKind.ATTN_F)), mean(kind(TaskKind.ATTN_B))
+    t_exp, t_exp_b, t_single = [], [], []
+    for (k_, l_), v in acc.items():
+        o = offload[l_ - 1]
+        if k_ in (TaskKind.EXP_F, TaskKind.EXP_B) and o * N < n:
+            (t_exp if k_ == TaskKind.EXP_F else t_exp_b).append(mean(v) / (1 - o * N / n))
+        if k_ == TaskKind.OFF_EXP_F and o > 0:
+            t_single.append(mean(v) / (o * N * N / (n * M)))
+    exp_f = mean(t_exp)
+    gamma = mean(t_exp_b) / exp_f
+    if t_single:
+        single = mean(t_single)
+    elif base:
+        single = base["single_expert_fwd_ns"] * exp_f / base["expert_layer_fwd_ns"]
+    else:
+        single = exp_f * N / n
+    return {"attn_fwd_ns": int((attn_f + attn_b) / (1 + gamma)), "expert_layer_fwd_ns": int(exp_f),
+            "single_expert_fwd_ns": int(single), "gamma_x100": int(round(100 * gamma)),
+            "attn_fwd_raw_ns": int(attn_f), "attn_bwd_raw_ns": int(attn_b)}

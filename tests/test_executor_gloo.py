@@ -381,3 +381,47 @@ def test_measure_transport_runs_the_executor_exchange():
     for o in outs:
         assert "error" not in o, o.get("error")
         assert o["out"]["dispatch_ns"] > 0 and o["out"]["combine_ns"] > 0
+
+
+def _calibrate_worker(rank, W, M, N, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=W)
+    try:
+        from cpu_backend import CpuBackend
+        from paper_2504_03871_b200.executor import ZpLayerShape
+        from paper_2504_03871_b200.profiler import calibrate_in_pipeline
+
+        shape = ZpLayerShape(8, 2, 256, 128, 16, heads=2, attention=True)
+        g1, g2 = dist.new_group(list(range(W))), dist.new_group(list(range(W)))
+        out = calibrate_in_pipeline(shape, M, N, CpuBackend(), (1, 0), "nccl", g1, g2, microbatches=2, reps=1)
+        q.put({"rank": rank, "out": out})
+    except Exception:  # report instead of hanging the parent
+        import traceback
+
+        q.put({"rank": rank, "error": traceback.format_exc()})
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_calibrate_in_pipeline_inverts_the_duration_model():
+    """In-pipeline calibration (a 2-layer ZP run through the executor, one layer with an offload)
+    returns positive planner durations on every rank, with the offloaded expert's time inverted
+    from OffExpF (not the fallback)."""
+    M, N = 2, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_calibrate_worker, args=(r, M + N, M, N, port, q)) for r in range(M + N)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for o in outs:
+        assert "error" not in o, o.get("error")
+        d = o["out"]
+        for k in ("attn_fwd_ns", "expert_layer_fwd_ns", "single_expert_fwd_ns", "gamma_x100"):
+            assert d[k] > 0, (k, d)

@@ -611,7 +611,7 @@ def run_zp(args, ws, rank, local):
         else:
             assignment = plan_assignment(spec, dur)
             assignment, clamped_layers = clamp_to_layer_capacity(assignment, c.E, M, N)
-            if args.calibrate and not args.no_asym_ea:
+            if (args.calibrate or args.router_skew > 0) and not args.no_calibrate and not args.no_asym_ea:
                 # re-plan from durations measured inside a short pipeline run of this plan's
                 # offloads (profiler.calibrate_in_pipeline): sustained clocks, real loads under skew
                 from paper_2504_03871_b200.profiler import calibrate_in_pipeline
@@ -990,7 +990,9 @@ def main():
                     help="ZP: plan with the attention forward as measured (no fwd+bwd role normalisation)")
     ap.add_argument("--no-asym-ea", action="store_true", help="ZP: keep all experts on expert ranks")
     ap.add_argument("--calibrate", action="store_true",
-                    help="ZP: re-plan Asym-EA from durations measured inside a short pipeline run")
+                    help="ZP: re-plan Asym-EA from durations measured inside a short pipeline run "
+                         "(on by default with --router-skew > 0)")
+    ap.add_argument("--no-calibrate", action="store_true", help="ZP: never re-plan from the pipeline run")
     ap.add_argument("--router-skew", type=float, default=0.0,
                     help="ZP: Zipf exponent of a per-expert router bias (skewed expert loads)")
     ap.add_argument("--no-balanced-placement", action="store_true",

@@ -980,7 +980,7 @@ def main():
     ap.add_argument("--microbatches", type=int, default=8, help="ZP (N>1): micro-batches R")
     ap.add_argument("--mb-tokens", type=int, default=4096, help="ZP (N>1): tokens per micro-batch per attention rank")
     ap.add_argument("--attention-ranks", type=int, default=0,
-                    help="ZP: attention ranks M (default N/2, e.g. 4 + 4 at 8 GPUs; 6 gives BASELINE C5's "
+                    help="ZP: attention ranks M (default half the ranks, e.g. 4 + 4 at 8 GPUs; 6 gives BASELINE C5's "
                          "6 + 2, 3 the 3 + 1 analogue at 4 GPUs)")
     ap.add_argument("--no-attention", action="store_true", help="ZP: identity attention block")
     ap.add_argument("--attn-gemm-ctas", type=int, default=0,

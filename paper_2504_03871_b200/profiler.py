@@ -400,8 +400,15 @@ def calibrate_in_pipeline(shape, M: int, N: int, backend, offload, transport: st
             (t_exp if k_ == TaskKind.EXP_F else t_exp_b).append(mean(v) / (1 - o * N / n))
         if k_ == TaskKind.OFF_EXP_F and o > 0:
             t_single.append(mean(v) / (o * N * N / (n * M)))
-    exp_f = mean(t_exp)
-    gamma = mean(t_exp_b) / exp_f
+    if not t_exp or not t_exp_b:  # every calibration layer offloaded all experts: keep the probe's
+        if not base:
+            raise ValueError("calibrate_in_pipeline: no expert-rank task to invert and no base durations")
+        exp_f = base["expert_layer_fwd_ns"] * (mean(kind(TaskKind.ATTN_F)) / base["attn_fwd_measured_ns"]
+                                               if base.get("attn_fwd_measured_ns") else 1.0)
+        gamma = base["gamma_x100"] / 100
+    else:
+        exp_f = mean(t_exp)
+        gamma = mean(t_exp_b) / exp_f
     if t_single:
         single = mean(t_single)
     elif base:

@@ -396,7 +396,13 @@ def _calibrate_worker(rank, W, M, N, port, q):
         shape = ZpLayerShape(8, 2, 256, 128, 16, heads=2, attention=True)
         g1, g2 = dist.new_group(list(range(W))), dist.new_group(list(range(W)))
         out = calibrate_in_pipeline(shape, M, N, CpuBackend(), (1, 0), "nccl", g1, g2, microbatches=2, reps=1)
-        q.put({"rank": rank, "out": out})
+        # every expert given away in both layers: nothing to invert on the expert ranks, so the
+        # expert-layer time falls back to the probe's, scaled by the measured attention forward
+        base = {"expert_layer_fwd_ns": 1000, "attn_fwd_measured_ns": out["attn_fwd_raw_ns"],
+                "single_expert_fwd_ns": 500, "gamma_x100": 200}
+        out_all = calibrate_in_pipeline(shape, M, N, CpuBackend(), (4, 4), "nccl", g1, g2, microbatches=2,
+                                        reps=1, base=base)
+        q.put({"rank": rank, "out": out, "out_all": out_all})
     except Exception:  # report instead of hanging the parent
         import traceback
 
@@ -408,8 +414,8 @@ def _calibrate_worker(rank, W, M, N, port, q):
 
 def test_calibrate_in_pipeline_inverts_the_duration_model():
     """In-pipeline calibration (a 2-layer ZP run through the executor, one layer with an offload)
-    returns positive planner durations on every rank, with the offloaded expert's time inverted
-    from OffExpF (not the fallback)."""
+    returns positive planner durations on every rank; with every expert offloaded in both layers
+    it falls back to the probe's expert-layer time and gamma."""
     M, N = 2, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -425,3 +431,6 @@ def test_calibrate_in_pipeline_inverts_the_duration_model():
         d = o["out"]
         for k in ("attn_fwd_ns", "expert_layer_fwd_ns", "single_expert_fwd_ns", "gamma_x100"):
             assert d[k] > 0, (k, d)
+        a = o["out_all"]
+        assert a["gamma_x100"] == 200 and a["single_expert_fwd_ns"] > 0
+        assert 0 < a["expert_layer_fwd_ns"] < 10 * 1000  # the probe's 1000 ns, scaled by ~1
